@@ -1,0 +1,125 @@
+/*
+ * bandix_b200 -- C ABI of the B200-native batched band-SLAE solvers.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * bandix 0.1.0 (/root/reference/pkg/src/bandix).  The reference is pure
+ * Python and has no FFI of its own; each entry point below replaces one
+ * reference solver function, batched over a system index, and is what a
+ * ctypes / cffi binding of the reference would call (INTEGRATION.md shows
+ * the binding).  No torch types cross this boundary: plain device pointers,
+ * sizes and a cudaStream_t passed as void*.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - All arrays are DEVICE pointers to IEEE binary64 (or int32 for status).
+ *  - A band system of order n is stored by diagonals, ROW-ALIGNED: every
+ *    diagonal array has n rows and row i holds the coefficient of equation
+ *    i (sub2[i] = A[i,i-2], sub1[i] = A[i,i-1], main[i] = A[i,i],
+ *    sup1[i] = A[i,i+1], sup2[i] = A[i,i+2]).  The reference stores the same
+ *    entries unpadded (core.py:117-164: sub2[i-2], sub1[i-1], ...); slots that
+ *    fall outside the matrix (sub2 rows 0-1, sub1 row 0, sup1 row n-1,
+ *    sup2 rows n-2..n-1) are NEVER read.
+ *  - layout = BX_LAYOUT_INTERLEAVED: element (row i, system s) at p[i*ld + s]
+ *    (system index fastest, ld >= batch).  BX_LAYOUT_SYSTEM_MAJOR: at
+ *    p[s*ld + i] (ld >= n).  One ld applies to every array of the call.
+ *  - status[s] / index[s] (int32, may be NULL): per-system outcome, the
+ *    batched form of the reference's exceptions (errors.py): BX_STATUS_*
+ *    below; index is the failing row (ZeroPivot.index) or -1.
+ *  - Return value: BX_OK, or an argument / launch error (bx_last_error()
+ *    gives the message).  Numerical outcomes never fail the call.
+ *  - Calls are stream-ordered and asynchronous; they do not allocate on the
+ *    hot path -- scratch comes from a caller-provided workspace of at least
+ *    bx_workspace_bytes(...) bytes.  Reentrant on distinct buffers/streams.
+ */
+#ifndef BANDIX_B200_H
+#define BANDIX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes */
+#define BX_OK 0
+#define BX_ERR_ARG 1
+#define BX_ERR_CUDA 2
+#define BX_ERR_WORKSPACE 3
+#define BX_ERR_UNSUPPORTED 4
+
+/* per-system status (errors.py:29-102) */
+#define BX_STATUS_OK 0
+#define BX_STATUS_ZERO_PIVOT 1      /* ZeroPivot(index)            errors.py:29-34 */
+#define BX_STATUS_SINGULAR 2        /* SingularMatrix              errors.py:45-46 */
+#define BX_STATUS_MAX_ITER 3        /* MaxIterationsExceeded       errors.py:49-59 */
+#define BX_STATUS_DIVERGED 4        /* Diverged                    errors.py:62-70 */
+#define BX_STATUS_ZERO_DIAG 5       /* ZeroDiagonal(index)         errors.py:73-78 */
+#define BX_STATUS_WINDOW_OVERFLOW 6 /* fp64 symbolic window exceeded (no reference twin) */
+
+/* layouts */
+#define BX_LAYOUT_INTERLEAVED 0
+#define BX_LAYOUT_SYSTEM_MAJOR 1
+
+/* algorithms for the direct solvers */
+#define BX_ALGO_SEQUENTIAL 0   /* reference operation order, bit-identical results */
+#define BX_ALGO_PARTITIONED 1  /* on-chip partitioned elimination, tolerance parity */
+
+/* solver ids for bx_workspace_bytes */
+#define BX_SOLVER_NTDM 0
+#define BX_SOLVER_NPDM 1
+#define BX_SOLVER_MNPDM 2
+#define BX_SOLVER_STDM 3
+#define BX_SOLVER_SPDM 4
+#define BX_SOLVER_SIP 5
+#define BX_SOLVER_HB 6
+
+const char *bx_version(void);
+const char *bx_last_error(void);
+
+/* Bytes of scratch the given solver needs (0 is a valid answer). */
+size_t bx_workspace_bytes(int32_t solver, int64_t batch, int64_t n, int32_t layout,
+                          int32_t algo);
+
+/* ---- direct solvers ----------------------------------------------------- */
+
+/* Thomas with reciprocal pivots.  Replaces solve_ntdm (direct.py:103-113):
+ * tri_factor_recip + tri_solve_recip (_elim.py:90-122).  n >= 2. */
+int bx_ntdm_f64(const double *sub1, const double *main, const double *sup1,
+                const double *rhs, double *x, int32_t *status, int32_t *index,
+                int64_t batch, int64_t n, int64_t ld, int32_t layout, int32_t algo,
+                void *workspace, size_t workspace_bytes, void *stream);
+
+/* Banded Doolittle LU + substitutions.  Replaces solve_npdm
+ * (direct.py:73-81): penta_factor/penta_forward/penta_backward
+ * (_elim.py:30-87).  n >= 3. */
+int bx_npdm_f64(const double *sub2, const double *sub1, const double *main,
+                const double *sup1, const double *sup2, const double *rhs, double *x,
+                int32_t *status, int32_t *index, int64_t batch, int64_t n, int64_t ld,
+                int32_t layout, int32_t algo, void *workspace, size_t workspace_bytes,
+                void *stream);
+
+/* Sparsity-aware reciprocal-pivot PD solve.  Replaces solve_mnpdm
+ * (direct.py:84-100): mnpdm_sweep (_elim.py:125-190).  nz_sub2 (int64 per
+ * system, may be NULL) receives the structurally nonzero sub2 count that the
+ * reference's op counter uses (direct.py:98-99). */
+int bx_mnpdm_f64(const double *sub2, const double *sub1, const double *main,
+                 const double *sup1, const double *sup2, const double *rhs, double *x,
+                 int32_t *status, int32_t *index, int64_t *nz_sub2, int64_t batch, int64_t n,
+                 int64_t ld, int32_t layout, int32_t algo, void *workspace,
+                 size_t workspace_bytes, void *stream);
+
+/* ||b - A x||_inf per system, the report residual of _finish_report
+ * (direct.py:66-70 -> core.py:243-321), in the reference's row-fused
+ * operation order.  bandwidth 1 (tridiagonal: sub2/sup2 ignored, may be
+ * NULL) or 2 (pentadiagonal). */
+int bx_residual_inf_f64(int32_t bandwidth, const double *sub2, const double *sub1,
+                        const double *main, const double *sup1, const double *sup2,
+                        const double *x, const double *rhs, double *res_inf, int64_t batch,
+                        int64_t n, int64_t ld, int32_t layout, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BANDIX_B200_H */

@@ -1,0 +1,18 @@
+"""bandix_b200: B200-native batched band-SLAE solvers.
+
+Drop-in for the hot path of the reference package ``bandix`` 0.1.0: the
+direct (NTDM/NPDM/MNPDM), symbolic (SPDM/STDM) and iterative (ILU(0)/SIP,
+SIP with Hotelling-Bodewig inverses) solvers, with the reference's entry
+points and argument conventions, batched over a system index and executed
+by hand-written sm_100a CUDA kernels behind a C ABI
+(``include/bandix_b200.h``, ``libbandix_b200.so``).  There is no CPU
+fallback: without the built library or a GPU every solver raises.
+"""
+
+from .core import BandFactors, OpCounter, PentaMatrix, SolveReport, TriMatrix  # noqa: F401
+from .direct import solve_mnpdm, solve_npdm, solve_ntdm  # noqa: F401
+from .errors import (BandixError, DenseCapExceeded, DimensionMismatch, Diverged,  # noqa: F401
+                     InvalidInput, MaxIterationsExceeded, SingularMatrix, SolverError,
+                     ZeroDiagonal, ZeroPivot)
+
+__version__ = "0.1.0"

@@ -1,0 +1,371 @@
+"""Batched band-matrix containers and result records (host side of the C ABI).
+
+Mirrors the reference's value types (``bandix.core``, core.py:69-235) with a
+batch axis and GPU residency:
+
+* ``TriMatrix`` / ``PentaMatrix`` keep the reference constructor
+  ``from_diagonals(...)`` and argument conventions (reference-length diagonals:
+  sub2[i-2], sub1[i-1], main[i], sup1[i], sup2[i] for row i, core.py:117-183),
+  accept one system (1-D sequences, exactly the reference call) or a batch
+  (2-D, one system per row), and hold the diagonals on the GPU in the C ABI's
+  ROW-ALIGNED storage: every diagonal has n rows, row i holds equation i's
+  coefficient.  Default layout is interleaved ``(n, B)`` (system index
+  fastest); ``layout="system"`` keeps ``(B, n)``.
+* ``SolveReport`` carries x, iterations, residual_inf, ops, wall_seconds,
+  history (core.py:226-235) plus the per-system ``status``/``index`` that
+  replace exceptions in batched calls.
+* ``OpCounter`` is the reference's closed-form operation tally (core.py:69-102).
+
+Inputs are never mutated (the reference freezes them, core.py:48-53).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Any, Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import (DimensionMismatch, InvalidInput, STATUS_OK, exception_for)
+
+LAYOUTS = {"interleaved": _lib.LAYOUT_INTERLEAVED, "system": _lib.LAYOUT_SYSTEM_MAJOR}
+
+
+def default_device():
+    if not torch.cuda.is_available():
+        from .errors import CudaError
+        raise CudaError("bandix_b200 needs a CUDA device (there is no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _as_batch(v, what):
+    """-> (float64 numpy/torch 2-D array, single_flag)."""
+    if isinstance(v, torch.Tensor):
+        t = v.detach().to(torch.float64)
+        if t.dim() == 1:
+            return t.unsqueeze(0), True
+        if t.dim() == 2:
+            return t, False
+        raise InvalidInput(f"{what}: expected 1-D or 2-D, got shape {tuple(t.shape)}")
+    if not isinstance(v, np.ndarray) and len(v) and isinstance(v[0], Fraction):
+        v = [float(q) for q in v]          # exact inputs are evaluated in binary64
+    a = np.asarray(v, dtype=np.float64)
+    if a.ndim == 1:
+        return a[None, :], True
+    if a.ndim == 2:
+        return a, False
+    raise InvalidInput(f"{what}: expected 1-D or 2-D, got shape {a.shape}")
+
+
+def _to_device(a, device):
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=torch.float64)
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device=device)
+
+
+def pack_rows(arr, n, first_row, layout, device, batch):
+    """Reference-length diagonal (B, L) -> row-aligned device storage whose
+    rows first_row .. first_row+L-1 hold it (other slots zero)."""
+    t = _to_device(arr, device)
+    if t.shape[0] != batch:
+        raise DimensionMismatch(f"batch {t.shape[0]} != {batch}")
+    L = t.shape[1]
+    if layout == _lib.LAYOUT_INTERLEAVED:
+        out = torch.zeros((n, batch), dtype=torch.float64, device=device)
+        out[first_row:first_row + L].copy_(t.t())
+    else:
+        out = torch.zeros((batch, n), dtype=torch.float64, device=device)
+        out[:, first_row:first_row + L].copy_(t)
+    return out
+
+
+def unpack_rows(t, first_row, length, layout):
+    """Row-aligned device storage -> (B, L) view in reference indexing."""
+    if layout == _lib.LAYOUT_INTERLEAVED:
+        return t[first_row:first_row + length].t()
+    return t[:, first_row:first_row + length]
+
+
+def vector_to_layout(v, n, layout, device):
+    """(B, n) host/device vector -> device storage of the layout."""
+    t = _to_device(v, device)
+    if t.shape[1] != n:
+        raise DimensionMismatch(f"rhs has length {t.shape[1]}, expected {n}")
+    if layout == _lib.LAYOUT_INTERLEAVED:
+        return t.t().contiguous()
+    return t.contiguous()
+
+
+def vector_from_layout(t, layout):
+    """Device storage -> (B, n) view."""
+    return t.t() if layout == _lib.LAYOUT_INTERLEAVED else t
+
+
+def _ld(t, layout):
+    return t.stride(0)
+
+
+class _Band:
+    """Common machinery of the batched containers."""
+
+    names: tuple = ()
+    offsets: tuple = ()
+
+    def __init__(self, n, batch, diags, layout, single, device):
+        self.n = n
+        self.batch = batch
+        self._diags = diags            # row-aligned device tensors, same shape/stride
+        self.layout = layout
+        self.single = single
+        self.device = device
+        self.exact = False
+        t = diags[0]
+        for d in diags:
+            if d.shape != t.shape or d.stride() != t.stride() or d.dtype != torch.float64:
+                raise InvalidInput("diagonals must share shape, stride and dtype float64")
+        self.ld = t.stride(0)
+        if t.stride(1) != 1:
+            raise InvalidInput("row-aligned storage must be contiguous along its last axis")
+
+    @classmethod
+    def _build(cls, arrays, n_from, min_n, layout, device):
+        lay = LAYOUTS[layout] if isinstance(layout, str) else layout
+        device = torch.device(device) if device is not None else default_device()
+        conv = [_as_batch(a, nm) for a, nm in zip(arrays, cls.names)]
+        single = all(s for _, s in conv)
+        mats = [m for m, _ in conv]
+        batch = mats[0].shape[0]
+        n = mats[n_from].shape[1]
+        if n < min_n:
+            raise InvalidInput(f"{cls.__name__} semantics need n >= {min_n}, got {n}")
+        for m, off, nm in zip(mats, cls.offsets, cls.names):
+            if m.shape[0] != batch:
+                raise InvalidInput(f"{nm}: batch {m.shape[0]} != {batch}")
+            if m.shape[1] != n - abs(off):
+                raise InvalidInput(f"diagonal lengths do not match n={n} ({nm} has {m.shape[1]})")
+        diags = [pack_rows(m, n, -off if off < 0 else 0, lay, device, batch)
+                 for m, off in zip(mats, cls.offsets)]
+        return n, batch, diags, lay, single, device
+
+    def diagonals(self):
+        """Reference-length (B, L) views of the stored diagonals (core.py:145-146)."""
+        out = []
+        for d, off in zip(self._diags, self.offsets):
+            first = -off if off < 0 else 0
+            out.append(unpack_rows(d, first, self.n - abs(off), self.layout))
+        return tuple(out)
+
+    def rowaligned(self):
+        return tuple(self._diags)
+
+    def rhs(self, b):
+        """Validate and lay out a right-hand side (or batch of them)."""
+        bb, single = _as_batch(b, "rhs")
+        if bb.shape[0] != self.batch:
+            raise DimensionMismatch(f"rhs batch {bb.shape[0]} != {self.batch}")
+        if bb.shape[1] != self.n:
+            raise DimensionMismatch(f"rhs length {bb.shape[1]}, expected {self.n}")
+        return vector_to_layout(bb, self.n, self.layout, self.device)
+
+    def new_vector(self):
+        if self.layout == _lib.LAYOUT_INTERLEAVED:
+            return torch.empty((self.n, self.batch), dtype=torch.float64, device=self.device)
+        return torch.empty((self.batch, self.n), dtype=torch.float64, device=self.device)
+
+    def to_dense(self):
+        """Dense (B, n, n) float64 host copy, for oracles and small reports (core.py:148-155)."""
+        out = np.zeros((self.batch, self.n, self.n))
+        for d, off in zip(self.diagonals(), self.offsets):
+            dd = d.detach().cpu().numpy()
+            for idx in range(dd.shape[1]):
+                i = idx - min(off, 0)
+                out[:, i, i + off] = dd[:, idx]
+        return out
+
+
+class TriMatrix(_Band):
+    """Batched tridiagonal systems (offsets -1..+1), n >= 2 (core.py:167-202)."""
+
+    names = ("sub1", "main", "sup1")
+    offsets = (-1, 0, 1)
+
+    @staticmethod
+    def from_diagonals(sub1, main, sup1, exact=None, *, layout="interleaved", device=None):
+        n, batch, diags, lay, single, dev = TriMatrix._build((sub1, main, sup1), 1, 2, layout, device)
+        return TriMatrix(n, batch, diags, lay, single, dev)
+
+    @staticmethod
+    def from_rowaligned(sub1, main, sup1, layout="interleaved"):
+        """Wrap device tensors already in the C ABI's row-aligned storage."""
+        lay = LAYOUTS[layout] if isinstance(layout, str) else layout
+        n, batch = (main.shape if lay == _lib.LAYOUT_INTERLEAVED else main.shape[::-1])
+        return TriMatrix(n, batch, [sub1, main, sup1], lay, False, main.device)
+
+    @property
+    def sub1(self):
+        return self.diagonals()[0]
+
+    @property
+    def main(self):
+        return self.diagonals()[1]
+
+    @property
+    def sup1(self):
+        return self.diagonals()[2]
+
+
+class PentaMatrix(_Band):
+    """Batched pentadiagonal systems (offsets -2..+2), n >= 3 (core.py:117-164)."""
+
+    names = ("sub2", "sub1", "main", "sup1", "sup2")
+    offsets = (-2, -1, 0, 1, 2)
+
+    @staticmethod
+    def from_diagonals(sub2, sub1, main, sup1, sup2, exact=None, *, layout="interleaved",
+                       device=None):
+        n, batch, diags, lay, single, dev = PentaMatrix._build(
+            (sub2, sub1, main, sup1, sup2), 2, 3, layout, device)
+        return PentaMatrix(n, batch, diags, lay, single, dev)
+
+    @staticmethod
+    def from_rowaligned(sub2, sub1, main, sup1, sup2, layout="interleaved"):
+        lay = LAYOUTS[layout] if isinstance(layout, str) else layout
+        n, batch = (main.shape if lay == _lib.LAYOUT_INTERLEAVED else main.shape[::-1])
+        return PentaMatrix(n, batch, [sub2, sub1, main, sup1, sup2], lay, False, main.device)
+
+    @property
+    def sub2(self):
+        return self.diagonals()[0]
+
+    @property
+    def sub1(self):
+        return self.diagonals()[1]
+
+    @property
+    def main(self):
+        return self.diagonals()[2]
+
+    @property
+    def sup1(self):
+        return self.diagonals()[3]
+
+    @property
+    def sup2(self):
+        return self.diagonals()[4]
+
+
+@dataclass(frozen=True)
+class OpCounter:
+    """Scalar-operation tally (core.py:69-102), closed form per method."""
+
+    adds: Any = 0
+    subs: Any = 0
+    muls: Any = 0
+    divs: Any = 0
+
+    @property
+    def total(self):
+        return self.adds + self.subs + self.muls + self.divs
+
+    def plus(self, adds=0, subs=0, muls=0, divs=0):
+        return OpCounter(self.adds + adds, self.subs + subs, self.muls + muls, self.divs + divs)
+
+    def merged(self, other):
+        return self.plus(other.adds, other.subs, other.muls, other.divs)
+
+    def as_dict(self):
+        return {"adds": self.adds, "subs": self.subs, "muls": self.muls, "divs": self.divs,
+                "total": self.total}
+
+
+class _Timer:
+    """CUDA-event stopwatch on the current stream; read lazily."""
+
+    def __init__(self):
+        self.start = torch.cuda.Event(enable_timing=True)
+        self.stop = torch.cuda.Event(enable_timing=True)
+        self.start.record()
+
+    def end(self):
+        self.stop.record()
+        return self
+
+    def seconds(self):
+        self.stop.synchronize()
+        return self.start.elapsed_time(self.stop) / 1e3
+
+
+@dataclass
+class SolveReport:
+    """Outcome of a (batched) solve (core.py:226-235).
+
+    Batched: ``x`` is a (B, n) device tensor (a view of the layout storage),
+    ``iterations``/``residual_inf``/``status``/``index`` are (B,) device
+    tensors.  Single-system calls return host values exactly like the
+    reference (numpy x, float residual, int iterations) and raise instead of
+    reporting a status.
+    """
+
+    x: Any
+    iterations: Any
+    residual_inf: Any
+    ops: OpCounter
+    wall_seconds: float
+    history: tuple = ()
+    status: Any = None
+    index: Any = None
+    x_storage: Any = field(default=None, repr=False)
+
+    def ok(self):
+        return bool((self.status == STATUS_OK).all())
+
+    def raise_for_status(self):
+        """Raise the reference exception for the first failing system."""
+        st = self.status.detach().cpu().numpy() if isinstance(self.status, torch.Tensor) else np.asarray(self.status)
+        bad = np.nonzero(st != STATUS_OK)[0]
+        if bad.size:
+            s = int(bad[0])
+            ix = self.index.detach().cpu().numpy() if isinstance(self.index, torch.Tensor) else np.asarray(self.index)
+            it = self.iterations
+            it_s = int(it[s]) if hasattr(it, "__len__") else it
+            res = self.residual_inf
+            res_s = float(res[s]) if hasattr(res, "__len__") else res
+            raise exception_for(int(st[s]), int(ix[s]), best=None, residual=res_s, iterations=it_s)
+
+
+@dataclass(frozen=True)
+class BandFactors:
+    """Banded (I)LU factors, row-aligned device storage (core.py:208-223)."""
+
+    n: int
+    l_sub1: Any
+    l_sub2: Any
+    u_main: Any
+    u_sup1: Any
+    u_sup2: Any
+    m: int = 2
+    exact: bool = False
+
+
+_WS_CACHE: dict = {}
+
+
+def workspace(nbytes, device):
+    """Reusable scratch buffer (grown on demand, never shrunk)."""
+    key = (device.index if device.index is not None else torch.cuda.current_device())
+    buf = _WS_CACHE.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        _WS_CACHE[key] = buf
+    return buf
+
+
+def stream_handle():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()

@@ -1,0 +1,162 @@
+// extern "C" entry points of libbandix_b200.so (declared in include/bandix_b200.h).
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "bx_common.cuh"
+#include "bx_kernels.h"
+
+namespace bxh {
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return BX_ERR_CUDA;
+  }
+  return BX_OK;
+}
+}  // namespace bxh
+
+using bxh::set_error;
+
+static int check_common(const char *fn, int64_t batch, int64_t n, int64_t nmin, int64_t ld,
+                        int32_t layout) {
+  if (batch < 0) { set_error("%s: batch must be >= 0", fn); return BX_ERR_ARG; }
+  if (n < nmin) { set_error("%s: n=%lld below the minimum %lld", fn, (long long)n, (long long)nmin); return BX_ERR_ARG; }
+  if (layout == BX_LAYOUT_INTERLEAVED) {
+    if (ld < batch) { set_error("%s: interleaved ld=%lld < batch=%lld", fn, (long long)ld, (long long)batch); return BX_ERR_ARG; }
+  } else if (layout == BX_LAYOUT_SYSTEM_MAJOR) {
+    if (ld < n) { set_error("%s: system-major ld=%lld < n=%lld", fn, (long long)ld, (long long)n); return BX_ERR_ARG; }
+  } else {
+    set_error("%s: unknown layout %d", fn, layout);
+    return BX_ERR_ARG;
+  }
+  return BX_OK;
+}
+
+#define BX_REQUIRE(cond, ...)            \
+  do {                                   \
+    if (!(cond)) {                       \
+      set_error(__VA_ARGS__);            \
+      return BX_ERR_ARG;                 \
+    }                                    \
+  } while (0)
+
+extern "C" {
+
+const char *bx_version(void) { return "bandix_b200 0.1.0 (sm_100a)"; }
+const char *bx_last_error(void) { return bxh::g_err; }
+
+size_t bx_workspace_bytes(int32_t solver, int64_t batch, int64_t n, int32_t layout, int32_t algo) {
+  (void)layout;
+  const size_t rows = (size_t)batch * (size_t)n * sizeof(double);
+  switch (solver) {
+    case BX_SOLVER_NTDM:
+      return algo == BX_ALGO_SEQUENTIAL ? rows : bx::part_workspace_bytes(1, batch, n);
+    case BX_SOLVER_NPDM:
+    case BX_SOLVER_MNPDM:
+      return algo == BX_ALGO_SEQUENTIAL ? 2 * rows : bx::part_workspace_bytes(2, batch, n);
+    default:
+      return bx::other_workspace_bytes(solver, batch, n);
+  }
+}
+
+int bx_ntdm_f64(const double *sub1, const double *main, const double *sup1, const double *rhs,
+                double *x, int32_t *status, int32_t *index, int64_t batch, int64_t n, int64_t ld,
+                int32_t layout, int32_t algo, void *workspace, size_t workspace_bytes,
+                void *stream) {
+  int rc = check_common("bx_ntdm_f64", batch, n, 2, ld, layout);
+  if (rc) return rc;
+  BX_REQUIRE(sub1 && main && sup1 && rhs && x, "bx_ntdm_f64: null array pointer");
+  if (batch == 0) return BX_OK;
+  const size_t need = bx_workspace_bytes(BX_SOLVER_NTDM, batch, n, layout, algo);
+  if (workspace_bytes < need || (need && !workspace)) {
+    set_error("bx_ntdm_f64: workspace %zu bytes < required %zu", workspace_bytes, need);
+    return BX_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (algo == BX_ALGO_SEQUENTIAL) {
+    bx::ntdm_seq(sub1, main, sup1, rhs, x, (double *)workspace, status, index, batch, n, ld,
+                 layout, st);
+  } else if (algo == BX_ALGO_PARTITIONED) {
+    rc = bx::ntdm_part(sub1, main, sup1, rhs, x, (double *)workspace, status, index, batch, n,
+                       ld, layout, st);
+    if (rc) return rc;
+  } else {
+    set_error("bx_ntdm_f64: unknown algo %d", algo);
+    return BX_ERR_ARG;
+  }
+  return bxh::check_launch("bx_ntdm_f64");
+}
+
+static int penta_common(const char *fn, bool mod, const double *sub2, const double *sub1,
+                        const double *main, const double *sup1, const double *sup2,
+                        const double *rhs, double *x, int32_t *status, int32_t *index,
+                        int64_t *nz, int64_t batch, int64_t n, int64_t ld, int32_t layout,
+                        int32_t algo, void *workspace, size_t workspace_bytes, void *stream) {
+  int rc = check_common(fn, batch, n, 3, ld, layout);
+  if (rc) return rc;
+  BX_REQUIRE(sub2 && sub1 && main && sup1 && sup2 && rhs && x, "%s: null array pointer", fn);
+  if (batch == 0) return BX_OK;
+  const size_t need = bx_workspace_bytes(mod ? BX_SOLVER_MNPDM : BX_SOLVER_NPDM, batch, n, layout, algo);
+  if (workspace_bytes < need || (need && !workspace)) {
+    set_error("%s: workspace %zu bytes < required %zu", fn, workspace_bytes, need);
+    return BX_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (algo == BX_ALGO_SEQUENTIAL) {
+    bx::penta_seq(mod, sub2, sub1, main, sup1, sup2, rhs, x, (double *)workspace, status, index,
+                  nz, batch, n, ld, layout, st);
+  } else if (algo == BX_ALGO_PARTITIONED) {
+    rc = bx::penta_part(mod, sub2, sub1, main, sup1, sup2, rhs, x, (double *)workspace, status,
+                        index, nz, batch, n, ld, layout, st);
+    if (rc) return rc;
+  } else {
+    set_error("%s: unknown algo %d", fn, algo);
+    return BX_ERR_ARG;
+  }
+  return bxh::check_launch(fn);
+}
+
+int bx_npdm_f64(const double *sub2, const double *sub1, const double *main, const double *sup1,
+                const double *sup2, const double *rhs, double *x, int32_t *status, int32_t *index,
+                int64_t batch, int64_t n, int64_t ld, int32_t layout, int32_t algo,
+                void *workspace, size_t workspace_bytes, void *stream) {
+  return penta_common("bx_npdm_f64", false, sub2, sub1, main, sup1, sup2, rhs, x, status, index,
+                      nullptr, batch, n, ld, layout, algo, workspace, workspace_bytes, stream);
+}
+
+int bx_mnpdm_f64(const double *sub2, const double *sub1, const double *main, const double *sup1,
+                 const double *sup2, const double *rhs, double *x, int32_t *status,
+                 int32_t *index, int64_t *nz_sub2, int64_t batch, int64_t n, int64_t ld,
+                 int32_t layout, int32_t algo, void *workspace, size_t workspace_bytes,
+                 void *stream) {
+  return penta_common("bx_mnpdm_f64", true, sub2, sub1, main, sup1, sup2, rhs, x, status, index,
+                      nz_sub2, batch, n, ld, layout, algo, workspace, workspace_bytes, stream);
+}
+
+int bx_residual_inf_f64(int32_t bandwidth, const double *sub2, const double *sub1,
+                        const double *main, const double *sup1, const double *sup2,
+                        const double *x, const double *rhs, double *res_inf, int64_t batch,
+                        int64_t n, int64_t ld, int32_t layout, void *stream) {
+  BX_REQUIRE(bandwidth == 1 || bandwidth == 2, "bx_residual_inf_f64: bandwidth must be 1 or 2");
+  int rc = check_common("bx_residual_inf_f64", batch, n, bandwidth == 1 ? 2 : 3, ld, layout);
+  if (rc) return rc;
+  BX_REQUIRE(sub1 && main && sup1 && x && rhs && res_inf, "bx_residual_inf_f64: null pointer");
+  BX_REQUIRE(bandwidth == 1 || (sub2 && sup2), "bx_residual_inf_f64: null sub2/sup2");
+  if (batch == 0) return BX_OK;
+  bx::residual_inf(bandwidth, sub2, sub1, main, sup1, sup2, x, rhs, res_inf, batch, n, ld, layout,
+                   (cudaStream_t)stream);
+  return bxh::check_launch("bx_residual_inf_f64");
+}
+
+}  // extern "C"

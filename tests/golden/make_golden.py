@@ -1,0 +1,239 @@
+"""Generate the golden vectors by running the REFERENCE (bandix 0.1.0) itself.
+
+Run in the build container (the only place /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+Every case feeds seeded inputs (paper_1804_09666_b200.workloads, or a small
+hand case from SPEC.md) through the reference's public functions, one system
+per call exactly as the reference API works, and stores inputs and outputs in
+``tests/golden/*.npz``.  The files are committed; nothing at test time reads
+/root/reference.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+from fractions import Fraction
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from bandix import core, direct, exact, inverse, iterative  # noqa: E402
+from bandix.errors import (MaxIterationsExceeded, ZeroPivot)  # noqa: E402
+
+from paper_1804_09666_b200 import workloads as W  # noqa: E402
+
+
+def _save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path}")
+
+
+def _run_direct(kind, diags, rhs):
+    """One reference call per system; x=NaN + index on ZeroPivot."""
+    bsz, n = rhs.shape
+    xs = np.full((bsz, n), np.nan)
+    res = np.full(bsz, np.nan)
+    ops = np.zeros(bsz, dtype=np.int64)
+    status = np.zeros(bsz, dtype=np.int32)
+    index = np.full(bsz, -1, dtype=np.int32)
+    for s in range(bsz):
+        cols = [d[s] for d in diags]
+        try:
+            if kind == "ntdm":
+                rep = direct.solve_ntdm(core.TriMatrix.from_diagonals(*cols), rhs[s])
+            else:
+                a = core.PentaMatrix.from_diagonals(*cols)
+                rep = (direct.solve_npdm if kind == "npdm" else direct.solve_mnpdm)(a, rhs[s])
+            xs[s] = rep.x
+            res[s] = rep.residual_inf
+            ops[s] = rep.ops.total
+        except ZeroPivot as zp:
+            status[s] = 1
+            index[s] = zp.index
+    return xs, res, ops, status, index
+
+
+def golden_direct():
+    out = {}
+    # config 1 sample (seeded exactly as config 1, reduced batch)
+    d = W.td_dominant(16, 1024, seed=0)
+    x, r, o, st, ix = _run_direct("ntdm", d[:3], d[3])
+    out.update(ntdm_sub1=d[0], ntdm_main=d[1], ntdm_sup1=d[2], ntdm_rhs=d[3],
+               ntdm_x=x, ntdm_res=r, ntdm_ops=o, ntdm_status=st, ntdm_index=ix)
+    # ntdm edge cases: n=2, n=3, zero pivot at 0 and at 5
+    sub = np.array([[-1.0, -1.0]]); main = np.array([[2.0, 2.0, 2.0]]); sup = np.array([[-1.0, -1.0]])
+    b = np.array([[1.0, 0.0, 1.0]])
+    x, *_ = _run_direct("ntdm", (sub, main, sup), b)
+    out.update(ntdm_spec_x=x)
+    e = W.td_dominant(3, 16, seed=11)
+    sub1, main, sup1, rhs = (a.copy() for a in e)
+    main[0, 0] = 0.0                         # pivot 0 at row 0
+    # make row 5 of system 1 an exact zero pivot: decouple (sub=main=0)
+    sub1[1, 4] = 0.0; main[1, 5] = 0.0
+    x, r, o, st, ix = _run_direct("ntdm", (sub1, main, sup1), rhs)
+    out.update(ntdmz_sub1=sub1, ntdmz_main=main, ntdmz_sup1=sup1, ntdmz_rhs=rhs,
+               ntdmz_x=x, ntdmz_status=st, ntdmz_index=ix)
+    n2 = W.td_dominant(4, 2, seed=12)
+    x, r, o, st, ix = _run_direct("ntdm", n2[:3], n2[3])
+    out.update(ntdm2_sub1=n2[0], ntdm2_main=n2[1], ntdm2_sup1=n2[2], ntdm2_rhs=n2[3], ntdm2_x=x)
+
+    # config 2 sample, full band and sparse outer (MNPDM family)
+    for tag, sparse in (("pd", False), ("pds", True)):
+        p = W.pd_dominant(8, 512, seed=1, sparse_outer=sparse)
+        out.update({f"{tag}_{k}": v for k, v in zip(("sub2", "sub1", "main", "sup1", "sup2", "rhs"), p)})
+        for kind in ("npdm", "mnpdm"):
+            x, r, o, st, ix = _run_direct(kind, p[:5], p[5])
+            out.update({f"{tag}_{kind}_x": x, f"{tag}_{kind}_res": r, f"{tag}_{kind}_ops": o})
+    # small orders n = 3, 4, 5 and zero pivots
+    for n in (3, 4, 5):
+        p = W.pd_dominant(3, n, seed=20 + n)
+        out.update({f"pd{n}_{k}": v for k, v in zip(("sub2", "sub1", "main", "sup1", "sup2", "rhs"), p)})
+        for kind in ("npdm", "mnpdm"):
+            x, *_ = _run_direct(kind, p[:5], p[5])
+            out[f"pd{n}_{kind}_x"] = x
+    p = [a.copy() for a in W.pd_dominant(3, 32, seed=30)]
+    p[2][0, 0] = 0.0                                          # zero at row 0
+    p[0][1, 7] = 0.0; p[1][1, 8] = 0.0; p[2][1, 9] = 0.0      # decoupled row 9
+    p[1][2, 0] = p[2][2, 1] * p[2][2, 0] / p[3][2, 0]         # near-singular 2x2 lead (row 1)
+    out.update({f"pdz_{k}": v for k, v in zip(("sub2", "sub1", "main", "sup1", "sup2", "rhs"), p)})
+    for kind in ("npdm", "mnpdm"):
+        x, r, o, st, ix = _run_direct(kind, p[:5], p[5])
+        out.update({f"pdz_{kind}_x": x, f"pdz_{kind}_status": st, f"pdz_{kind}_index": ix})
+    _save("direct", **out)
+
+
+def golden_iterative():
+    out = {}
+    cases = {
+        # ladder twin of config 4 (m = 2 five-point), reference-representable
+        "ladder": W.five_point(4, 512, 2, seed=3),
+        # full-band DD pentadiagonal: ILU(0) == LU, k = 1
+        "full": W.pd_dominant(2, 256, seed=1),
+    }
+    q = [a.copy() for a in W.pd_dominant(3, 200, seed=5)]
+    rng = np.random.default_rng(55)
+    q[1][rng.random(q[1].shape) < 0.3] = 0.0                   # 30% zero +-1 entries
+    q[3][rng.random(q[3].shape) < 0.3] = 0.0
+    cases["holes"] = tuple(q)
+    for tag, p in cases.items():
+        out.update({f"{tag}_{k}": v for k, v in zip(("sub2", "sub1", "main", "sup1", "sup2", "rhs"), p)})
+        bsz, n = p[5].shape
+        tol = W.sip_tolerance(p[5])
+        keys = ("l_sub1", "l_sub2", "u_main", "u_sup1", "u_sup2")
+        fac = {k: np.zeros((bsz, len(getattr_len(k, n)))) for k in keys}
+        kdiag = {k: np.zeros((bsz, L)) for k, L in zip(("k_sub2", "k_sub1", "k_main", "k_sup1", "k_sup2"),
+                                                     (n - 2, n - 1, n, n - 1, n - 2))}
+        xs = np.zeros((bsz, n)); its = np.zeros(bsz, np.int64); res = np.zeros(bsz)
+        hist = np.full((bsz, 600), np.nan)
+        t0 = time.time()
+        for s in range(bsz):
+            a = core.PentaMatrix.from_diagonals(*[d[s] for d in p[:5]])
+            f = iterative.ilu0_penta(a)
+            for k in keys:
+                fac[k][s] = np.asarray(getattr(f, k))
+            km = iterative.defect_matrix(f, a).matrix
+            for k, dg in zip(kdiag, km.diagonals()):
+                kdiag[k][s] = np.asarray(dg)
+            rep = iterative.sip_solve(a, p[5][s], iterative.SipConfig(tolerance=float(tol[s]),
+                                                                      max_iterations=500),
+                                      record_history=True)
+            xs[s] = rep.x; its[s] = rep.iterations; res[s] = rep.residual_inf
+            for kk, rr in rep.history:
+                hist[s, kk - 1] = rr
+        print(f"{tag}: sip k={its.tolist()} ({time.time()-t0:.1f}s)")
+        out.update({f"{tag}_{k}": v for k, v in fac.items()})
+        out.update({f"{tag}_{k}": v for k, v in kdiag.items()})
+        out.update({f"{tag}_tol": tol, f"{tag}_x": xs, f"{tag}_k": its, f"{tag}_res": res,
+                    f"{tag}_hist": hist})
+    # MaxIterationsExceeded: ladder with a 2-iteration budget -> best iterate
+    p = cases["ladder"]
+    a = core.PentaMatrix.from_diagonals(*[d[0] for d in p[:5]])
+    try:
+        iterative.sip_solve(a, p[5][0], iterative.SipConfig(tolerance=1e-14, max_iterations=2))
+        raise AssertionError("expected MaxIterationsExceeded")
+    except MaxIterationsExceeded as e:
+        out.update(maxit_best=np.asarray(e.best), maxit_res=np.float64(e.residual_inf),
+                   maxit_k=np.int64(e.iterations))
+    _save("iterative", **out)
+
+
+def getattr_len(key, n):
+    return range({"l_sub1": n - 1, "l_sub2": n - 2, "u_main": n, "u_sup1": n - 1, "u_sup2": n - 2}[key])
+
+
+def golden_inverse():
+    out = {}
+    p = W.five_point(2, 256, 2, seed=3)
+    out.update({f"hb_{k}": v for k, v in zip(("sub2", "sub1", "main", "sup1", "sup2", "rhs"), p)})
+    tol = W.sip_tolerance(p[5])
+    bsz, n = p[5].shape
+    xs = np.zeros((bsz, n)); its = np.zeros(bsz, np.int64); res = np.zeros(bsz)
+    li = np.zeros(bsz, np.int64); ui = np.zeros(bsz, np.int64)
+    for s in range(bsz):
+        a = core.PentaMatrix.from_diagonals(*[d[s] for d in p[:5]])
+        rep = inverse.sip_hb_solve(a, p[5][s], iterative.SipConfig(tolerance=float(tol[s]),
+                                                                   max_iterations=500))
+        xs[s] = rep.x; its[s] = rep.iterations; res[s] = rep.residual_inf
+        f = iterative.ilu0_penta(a)
+        li[s] = inverse.hb_invert_dense(inverse.dense_lower_factor(f), float(tol[s])).iterations
+        ui[s] = inverse.hb_invert_dense(inverse.dense_upper_factor(f), float(tol[s])).iterations
+    out.update(hb_tol=tol, hb_x=xs, hb_k=its, hb_res=res, hb_linv_iters=li, hb_uinv_iters=ui)
+    # [[1,0],[3,1]] inverts in one iteration
+    r = inverse.hb_invert_dense(np.array([[1.0, 0.0], [3.0, 1.0]]))
+    out.update(hb_spec_iters=np.int64(r.iterations), hb_spec_inv=np.asarray(r.inverse))
+    _save("inverse", **out)
+
+
+def golden_exact():
+    """Small-N symbolic solves through the reference's exact solvers (float
+    inputs converted losslessly with to_exact, exact.py:15-16)."""
+    out = {}
+    t0 = time.time()
+    sub1, main, sup1, rhs, rows = W.td_symbolic(3, 40, seed=2, zeros=2)
+    xs = np.zeros((3, 40)); subs = np.zeros(3, np.int64)
+    for s in range(3):
+        t = core.TriMatrix.from_diagonals(*[[core.to_exact(v) for v in d[s]] for d in (sub1, main, sup1)])
+        r = exact.exact_solve_stdm(t, [core.to_exact(v) for v in rhs[s]])
+        xs[s] = [float(v) for v in r.x]; subs[s] = r.pivot_substitutions
+    out.update(stdm_sub1=sub1, stdm_main=main, stdm_sup1=sup1, stdm_rhs=rhs, stdm_rows=rows,
+               stdm_x=xs, stdm_subs=subs)
+    print(f"stdm {time.time()-t0:.1f}s subs={subs.tolist()}")
+    t0 = time.time()
+    p = W.pd_symbolic(2, 24, seed=2, zeros=2)
+    xs = np.zeros((2, 24)); subs = np.zeros(2, np.int64)
+    for s in range(2):
+        a = core.PentaMatrix.from_diagonals(*[[core.to_exact(v) for v in d[s]] for d in p[:5]])
+        r = exact.exact_solve_spdm(a, [core.to_exact(v) for v in p[5][s]])
+        xs[s] = [float(v) for v in r.x]; subs[s] = r.pivot_substitutions
+    out.update({f"spdm_{k}": v for k, v in zip(("sub2", "sub1", "main", "sup1", "sup2", "rhs", "rows"), p)})
+    out.update(spdm_x=xs, spdm_subs=subs)
+    print(f"spdm {time.time()-t0:.1f}s subs={subs.tolist()}")
+    # no-zero-pivot exact solves agree with float solves to rounding
+    q = W.td_symbolic(2, 64, seed=7, zeros=0)
+    xs = np.zeros((2, 64)); subs = np.zeros(2, np.int64)
+    for s in range(2):
+        t = core.TriMatrix.from_diagonals(*[[core.to_exact(v) for v in d[s]] for d in q[:3]])
+        r = exact.exact_solve_stdm(t, [core.to_exact(v) for v in q[3][s]])
+        xs[s] = [float(v) for v in r.x]; subs[s] = r.pivot_substitutions
+    out.update(stdm0_sub1=q[0], stdm0_main=q[1], stdm0_sup1=q[2], stdm0_rhs=q[3], stdm0_x=xs,
+               stdm0_subs=subs)
+    # exact determinant sign/zero gate on a singular 3x3 (rows 0 and 2 equal)
+    F = Fraction
+    t = core.TriMatrix.from_diagonals([F(1), F(1)], [F(1), F(1), F(1)], [F(1), F(1)])
+    out.update(det_singular=np.float64(float(exact.exact_det_band(t))))
+    _save("exact", **out)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["direct", "iterative", "inverse", "exact"]
+    for w in which:
+        globals()["golden_" + w]()

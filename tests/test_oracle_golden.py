@@ -1,0 +1,107 @@
+"""The oracle is pinned to the reference: golden vectors produced by running
+bandix 0.1.0 itself (tests/golden/make_golden.py) must be reproduced
+BIT-FOR-BIT by the batched restatement."""
+
+import numpy as np
+import pytest
+
+from oracle import STATUS_MAX_ITER, STATUS_ZERO_PIVOT
+from oracle import direct as D
+from oracle import inverse as H
+from oracle import iterative as I
+
+PD = ("sub2", "sub1", "main", "sup1", "sup2", "rhs")
+
+
+def eq(a, b):
+    return np.array_equal(a, b, equal_nan=True)
+
+
+def test_ntdm_config1_sample(golden):
+    g = golden("direct")
+    x, st, ix = D.ntdm(g["ntdm_sub1"], g["ntdm_main"], g["ntdm_sup1"], g["ntdm_rhs"])
+    assert eq(x, g["ntdm_x"])
+    res = D.residual_inf_tri(g["ntdm_sub1"], g["ntdm_main"], g["ntdm_sup1"], x, g["ntdm_rhs"])
+    assert eq(res, g["ntdm_res"])
+    n = x.shape[1]
+    assert sum(D.ops_ntdm(n).values()) == g["ntdm_ops"][0] == 9 * n - 7
+
+
+def test_ntdm_spec_and_edges(golden):
+    g = golden("direct")
+    x, *_ = D.ntdm([[-1.0, -1.0]], [[2.0, 2.0, 2.0]], [[-1.0, -1.0]], [[1.0, 0.0, 1.0]])
+    assert eq(x, g["ntdm_spec_x"]) and np.allclose(x, 1.0)
+    x, *_ = D.ntdm(g["ntdm2_sub1"], g["ntdm2_main"], g["ntdm2_sup1"], g["ntdm2_rhs"])
+    assert eq(x, g["ntdm2_x"])
+
+
+def test_ntdm_zero_pivots(golden):
+    g = golden("direct")
+    x, st, ix = D.ntdm(g["ntdmz_sub1"], g["ntdmz_main"], g["ntdmz_sup1"], g["ntdmz_rhs"])
+    assert eq(st, g["ntdmz_status"]) and eq(ix, g["ntdmz_index"])
+    assert list(st) == [STATUS_ZERO_PIVOT, STATUS_ZERO_PIVOT, 0] and list(ix) == [0, 5, -1]
+    assert eq(x, g["ntdmz_x"])
+
+
+@pytest.mark.parametrize("tag", ["pd", "pds", "pd3", "pd4", "pd5", "pdz"])
+def test_penta_direct(golden, tag):
+    g = golden("direct")
+    a = [g[f"{tag}_{k}"] for k in PD]
+    x, st, ix = D.npdm(*a)
+    x2, st2, ix2, nz = D.mnpdm(*a)
+    assert eq(x, g[f"{tag}_npdm_x"])
+    assert eq(x2, g[f"{tag}_mnpdm_x"])
+    if tag == "pdz":
+        assert eq(st, g["pdz_npdm_status"]) and eq(ix, g["pdz_npdm_index"])
+        assert eq(st2, g["pdz_mnpdm_status"]) and eq(ix2, g["pdz_mnpdm_index"])
+    if tag in ("pd", "pds"):
+        n = x.shape[1]
+        assert sum(D.ops_npdm(n).values()) == g[f"{tag}_npdm_ops"][0] == 19 * n - 29
+        assert sum(D.ops_mnpdm(n, int(nz[0])).values()) == g[f"{tag}_mnpdm_ops"][0]
+        res = D.residual_inf_penta(*a[:5], x, a[5])
+        assert eq(res, g[f"{tag}_npdm_res"])
+    if tag == "pds":
+        assert (nz == 2).all()
+
+
+@pytest.mark.parametrize("tag", ["ladder", "full", "holes"])
+def test_ilu0_defect_sip(golden, tag):
+    g = golden("iterative")
+    a = [g[f"{tag}_{k}"] for k in PD]
+    n = a[2].shape[1]
+    f, st, ix = I.ilu0(*a[:5], m=2)
+    assert eq(f["l1"][:, 1:], g[f"{tag}_l_sub1"]) and eq(f["l2"][:, 2:], g[f"{tag}_l_sub2"])
+    assert eq(f["mu"], g[f"{tag}_u_main"])
+    assert eq(f["phi"][:, :n - 1], g[f"{tag}_u_sup1"]) and eq(f["psi"][:, :n - 2], g[f"{tag}_u_sup2"])
+    k = I.defect(f, *a[:5])
+    assert eq(k[-2][:, 2:], g[f"{tag}_k_sub2"]) and eq(k[-1][:, 1:], g[f"{tag}_k_sub1"])
+    assert eq(k[0], g[f"{tag}_k_main"])
+    assert eq(k[1][:, :n - 1], g[f"{tag}_k_sup1"]) and eq(k[2][:, :n - 2], g[f"{tag}_k_sup2"])
+    r = I.sip(*a, tol=g[f"{tag}_tol"], max_iter=500, record_history=True)
+    assert eq(r["x"], g[f"{tag}_x"])
+    assert eq(r["iterations"], g[f"{tag}_k"])
+    assert eq(r["residual"], g[f"{tag}_res"])
+    hist = np.stack(r["history"], axis=1)
+    kmax = hist.shape[1]
+    assert eq(hist, g[f"{tag}_hist"][:, :kmax])
+
+
+def test_sip_max_iterations(golden):
+    g = golden("iterative")
+    a = [g[f"ladder_{k}"][:1] for k in PD]
+    r = I.sip(*a, tol=1e-14, max_iter=2)
+    assert r["status"][0] == STATUS_MAX_ITER and r["iterations"][0] == g["maxit_k"]
+    assert eq(r["best_x"][0], g["maxit_best"]) and r["best_residual"][0] == g["maxit_res"]
+
+
+def test_hb_dense(golden):
+    g = golden("inverse")
+    a = [g[f"hb_{k}"] for k in PD]
+    r = H.sip_hb(*a, tol=g["hb_tol"], max_iter=500)
+    assert eq(r["iterations"], g["hb_k"])
+    assert eq(r["inv_iterations"][:, 0], g["hb_linv_iters"])
+    assert eq(r["inv_iterations"][:, 1], g["hb_uinv_iters"])
+    # BLAS-ordered products: tolerance, not bits
+    assert np.abs(r["x"] - g["hb_x"]).max() <= 1e-12 * np.abs(g["hb_x"]).max()
+    x, it, res, hist, st = H.hb_invert_dense(np.array([[1.0, 0.0], [3.0, 1.0]]))
+    assert it == g["hb_spec_iters"] == 1 and eq(x, g["hb_spec_inv"])
