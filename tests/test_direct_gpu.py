@@ -1,0 +1,123 @@
+"""GPU parity of the direct solvers through the public API / C ABI.
+
+Sequential algorithm: BIT-IDENTICAL to the reference (golden vectors) and to
+the oracle at config sizes.  Partitioned algorithm: relative error <= 1e-10
+(north-star tolerance) on the diagonally dominant configs."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import direct as D
+from paper_1804_09666_b200 import (PentaMatrix, TriMatrix, ZeroPivot, solve_mnpdm, solve_npdm,
+                                   solve_ntdm)
+from paper_1804_09666_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+PD = ("sub2", "sub1", "main", "sup1", "sup2", "rhs")
+LAYOUTS = ["interleaved", "system"]
+REL_TOL = 1e-10   # north_star: max relative error <= 1e-10 for the direct solvers
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def rel_err(x, ref):
+    return np.max(np.abs(x - ref), axis=1) / np.max(np.abs(ref), axis=1)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_ntdm_golden_bitexact(cuda, golden, layout):
+    g = golden("direct")
+    t = TriMatrix.from_diagonals(g["ntdm_sub1"], g["ntdm_main"], g["ntdm_sup1"], layout=layout)
+    rep = solve_ntdm(t, g["ntdm_rhs"])
+    assert np.array_equal(host(rep.x), g["ntdm_x"])
+    assert np.array_equal(host(rep.residual_inf), g["ntdm_res"])
+    assert (host(rep.status) == 0).all()
+    assert rep.ops.total == g["ntdm_ops"][0]
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_ntdm_zero_pivot_status(cuda, golden, layout):
+    g = golden("direct")
+    t = TriMatrix.from_diagonals(g["ntdmz_sub1"], g["ntdmz_main"], g["ntdmz_sup1"], layout=layout)
+    rep = solve_ntdm(t, g["ntdmz_rhs"])
+    assert np.array_equal(host(rep.status), g["ntdmz_status"])
+    assert np.array_equal(host(rep.index), g["ntdmz_index"])
+    assert np.array_equal(host(rep.x), g["ntdmz_x"], equal_nan=True)
+
+
+def test_single_system_api_matches_reference(cuda, golden):
+    g = golden("direct")
+    t = TriMatrix.from_diagonals([-1.0, -1.0], [2.0, 2.0, 2.0], [-1.0, -1.0])
+    rep = solve_ntdm(t, [1.0, 0.0, 1.0])
+    assert isinstance(rep.x, np.ndarray) and np.array_equal(rep.x, g["ntdm_spec_x"][0])
+    assert rep.iterations == 0 and rep.ops.total == 9 * 3 - 7
+    z = TriMatrix.from_diagonals(g["ntdmz_sub1"][1], g["ntdmz_main"][1], g["ntdmz_sup1"][1])
+    with pytest.raises(ZeroPivot) as ei:
+        solve_ntdm(z, g["ntdmz_rhs"][1])
+    assert ei.value.index == 5
+    two = TriMatrix.from_diagonals(g["ntdm2_sub1"][0], g["ntdm2_main"][0], g["ntdm2_sup1"][0])
+    assert np.array_equal(solve_ntdm(two, g["ntdm2_rhs"][0]).x, g["ntdm2_x"][0])
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("tag", ["pd", "pds", "pd3", "pd4", "pd5", "pdz"])
+def test_penta_golden_bitexact(cuda, golden, layout, tag):
+    g = golden("direct")
+    a = [g[f"{tag}_{k}"] for k in PD]
+    A = PentaMatrix.from_diagonals(*a[:5], layout=layout)
+    for kind, fn in (("npdm", solve_npdm), ("mnpdm", solve_mnpdm)):
+        rep = fn(A, a[5])
+        assert np.array_equal(host(rep.x), g[f"{tag}_{kind}_x"], equal_nan=True), kind
+        if tag == "pdz":
+            assert np.array_equal(host(rep.status), g[f"pdz_{kind}_status"])
+            assert np.array_equal(host(rep.index), g[f"pdz_{kind}_index"])
+        if tag in ("pd", "pds"):
+            assert np.array_equal(host(rep.residual_inf), g[f"{tag}_{kind}_res"])
+            tot = rep.ops.total
+            tot = host(tot) if isinstance(tot, torch.Tensor) else tot
+            assert np.all(tot == g[f"{tag}_{kind}_ops"])
+
+
+def test_single_system_penta_raises(cuda, golden):
+    g = golden("direct")
+    a = [g[f"pdz_{k}"][1] for k in PD]
+    A = PentaMatrix.from_diagonals(*a[:5])
+    with pytest.raises(ZeroPivot) as ei:
+        solve_npdm(A, a[5])
+    assert ei.value.index == 9
+    with pytest.raises(ZeroPivot):
+        solve_mnpdm(A, a[5])
+
+
+def test_config1_full_bitexact(cuda):
+    d = W.td_dominant(1024, 1024, seed=0)
+    x_ref, st, _ = D.ntdm(*d)
+    rep = solve_ntdm(TriMatrix.from_diagonals(*d[:3]), d[3])
+    assert np.array_equal(host(rep.x), x_ref)
+    assert np.array_equal(host(rep.residual_inf), D.residual_inf_tri(*d[:3], x_ref, d[3]))
+
+
+@pytest.mark.parametrize("sparse", [False, True])
+def test_config2_slice_bitexact(cuda, sparse):
+    p = W.pd_dominant(256, 4096, seed=1, sparse_outer=sparse)
+    A = PentaMatrix.from_diagonals(*p[:5])
+    x_n, *_ = D.npdm(*p)
+    x_m, _, _, nz = D.mnpdm(*p)
+    assert np.array_equal(host(solve_npdm(A, p[5]).x), x_n)
+    rep = solve_mnpdm(A, p[5])
+    assert np.array_equal(host(rep.x), x_m)
+    assert np.array_equal(host(rep.ops.total), np.array([sum(D.ops_mnpdm(4096, int(z)).values()) for z in nz]))
+
+
+def test_empty_batch_and_dimension_errors(cuda):
+    from paper_1804_09666_b200 import DimensionMismatch, InvalidInput
+    t = TriMatrix.from_diagonals(np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 3)))
+    rep = solve_ntdm(t, np.zeros((0, 4)))
+    assert rep.x.shape == (0, 4)
+    with pytest.raises(DimensionMismatch):
+        solve_ntdm(TriMatrix.from_diagonals([1.0], [2.0, 2.0], [1.0]), [1.0, 2.0, 3.0])
+    with pytest.raises(InvalidInput):
+        PentaMatrix.from_diagonals([], [1.0], [1.0, 2.0], [1.0], [])
