@@ -134,19 +134,24 @@ def gen_inputs(wl, rank):
     return W.pd_dominant(wl["batch"], wl["n"], sparse_outer=wl.get("sparse", False), rng=rng)
 
 
-def rowaligned_interleaved(arrs, kind):
-    """Reference-length (B, L) host arrays -> row-aligned interleaved (n, B)
-    host arrays: the C ABI's BX_LAYOUT_INTERLEAVED storage."""
+def rowaligned(arrs, kind, layout):
+    """Reference-length (B, L) host arrays -> row-aligned host arrays in the C
+    ABI storage: interleaved (n, B) or system-major (B, n)."""
     offs = (-1, 0, 1) if kind == "tri" else (-2, -1, 0, 1, 2)
     main = arrs[len(offs) // 2]
     bsz, n = main.shape
     out = []
     for a, off in zip(arrs[:len(offs)], offs):
-        r = np.zeros((n, bsz))
         first = -off if off < 0 else 0
-        r[first:first + a.shape[1]] = a.T
+        if layout == "interleaved":
+            r = np.zeros((n, bsz))
+            r[first:first + a.shape[1]] = a.T
+        else:
+            r = np.zeros((bsz, n))
+            r[:, first:first + a.shape[1]] = a
         out.append(r)
-    out.append(np.ascontiguousarray(arrs[len(offs)].T))
+    rhs = arrs[len(offs)]
+    out.append(np.ascontiguousarray(rhs.T if layout == "interleaved" else rhs))
     return out
 
 
@@ -224,15 +229,17 @@ def run_ours(args, wl):
     algo = {"sequential": _lib.ALGO_SEQUENTIAL, "partitioned": _lib.ALGO_PARTITIONED}[args.algo]
 
     arrs = gen_inputs(wl, rank)
-    host = rowaligned_interleaved(arrs, kind)                 # C-ABI layout, host
+    lay = _lib.LAYOUT_INTERLEAVED if args.layout == "interleaved" else _lib.LAYOUT_SYSTEM_MAJOR
+    host = rowaligned(arrs, kind, args.layout)                # C-ABI layout, host
+    ld = bsz if args.layout == "interleaved" else n
     dev_in = [torch.from_numpy(h).to(dev) for h in host]
-    x = torch.empty((n, bsz), dtype=torch.float64, device=dev)
+    x = torch.empty(host[-1].shape, dtype=torch.float64, device=dev)
     status = torch.empty(bsz, dtype=torch.int32, device=dev)
     index = torch.empty(bsz, dtype=torch.int32, device=dev)
     nz = torch.empty(bsz, dtype=torch.int64, device=dev)
     L = _lib.lib()
     solver = wl["solver"]
-    nbytes = L.bx_workspace_bytes(_lib.SOLVER[solver], bsz, n, _lib.LAYOUT_INTERLEAVED, algo)
+    nbytes = L.bx_workspace_bytes(_lib.SOLVER[solver], bsz, n, lay, algo)
     wsb = workspace(nbytes, dev)
     stream = torch.cuda.current_stream()
 
@@ -240,13 +247,13 @@ def run_ours(args, wl):
         s = stream.cuda_stream
         if solver == "ntdm":
             rc = L.bx_ntdm_f64(*(ptr(t) for t in ins), ptr(out), ptr(status), ptr(index), bsz, n,
-                               bsz, _lib.LAYOUT_INTERLEAVED, algo, ptr(wsb), wsb.numel(), s)
+                               ld, lay, algo, ptr(wsb), wsb.numel(), s)
         elif solver == "npdm":
             rc = L.bx_npdm_f64(*(ptr(t) for t in ins), ptr(out), ptr(status), ptr(index), bsz, n,
-                               bsz, _lib.LAYOUT_INTERLEAVED, algo, ptr(wsb), wsb.numel(), s)
+                               ld, lay, algo, ptr(wsb), wsb.numel(), s)
         else:
             rc = L.bx_mnpdm_f64(*(ptr(t) for t in ins), ptr(out), ptr(status), ptr(index), ptr(nz),
-                                bsz, n, bsz, _lib.LAYOUT_INTERLEAVED, algo, ptr(wsb), wsb.numel(), s)
+                                bsz, n, ld, lay, algo, ptr(wsb), wsb.numel(), s)
         _lib.check(rc, solver)
 
     # ---- correctness gate on this rank's data (sampled systems vs oracle) ----
@@ -296,7 +303,7 @@ def run_ours(args, wl):
 
     # ---- end-to-end through the C ABI with pinned host buffers ----
     pinned = [torch.from_numpy(h).pin_memory() for h in host]
-    x_host = torch.empty((n, bsz), dtype=torch.float64).pin_memory()
+    x_host = torch.empty(host[-1].shape, dtype=torch.float64).pin_memory()
     dev_e2e = [torch.empty_like(t) for t in dev_in]
     x_e2e = torch.empty_like(x)
 
@@ -348,7 +355,7 @@ def run_ours(args, wl):
         "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl["desc"], "solver": solver, "algo": args.algo,
-                   "batch_per_gpu": bsz, "n": n, "layout": "interleaved row-aligned",
+                   "batch_per_gpu": bsz, "n": n, "layout": f"{args.layout} row-aligned",
                    "l2": f"inputs {alg_bytes/1e9:.2f} GB per step > 126 MB L2, no flush",
                    "parallelism": f"dp{ws_world} (system-index sharding)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -376,11 +383,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="npdm", choices=sorted(WORKLOADS))
-    ap.add_argument("--algo", default="sequential", choices=["sequential", "partitioned"])
+    ap.add_argument("--algo", default="partitioned", choices=["sequential", "partitioned"])
+    ap.add_argument("--layout", default=None, choices=["interleaved", "system"],
+                    help="C-ABI storage (default: system-major for partitioned, interleaved for sequential)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.layout is None:
+        args.layout = "system" if args.algo == "partitioned" else "interleaved"
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference(args, wl)

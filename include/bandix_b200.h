@@ -56,6 +56,7 @@ extern "C" {
 #define BX_STATUS_DIVERGED 4        /* Diverged                    errors.py:62-70 */
 #define BX_STATUS_ZERO_DIAG 5       /* ZeroDiagonal(index)         errors.py:73-78 */
 #define BX_STATUS_WINDOW_OVERFLOW 6 /* fp64 symbolic window exceeded (no reference twin) */
+#define BX_STATUS_NOT_GRID 7        /* wavefront SIP given a system whose +-1 couplings cross grid rows */
 
 /* layouts */
 #define BX_LAYOUT_INTERLEAVED 0
@@ -117,6 +118,46 @@ int bx_residual_inf_f64(int32_t bandwidth, const double *sub2, const double *sub
                         const double *main, const double *sup1, const double *sup2,
                         const double *x, const double *rhs, double *res_inf, int64_t batch,
                         int64_t n, int64_t ld, int32_t layout, void *stream);
+
+/* ---- ILU(0) / SIP -------------------------------------------------------- */
+/* Stride-m five-point band: subm[i] = A[i,i-m], sub1[i] = A[i,i-1], main[i],
+ * sup1[i] = A[i,i+1], supm[i] = A[i,i+m] (row-aligned, n rows each).  m = 2
+ * is the reference's pentadiagonal (offsets -2..+2) bit-for-bit; m >= 3 is
+ * the grid generalisation and admits Stone's alpha.  */
+
+/* Pattern-restricted ILU(0) and defect K = L U - A.  Replaces ilu0_penta
+ * (iterative.py:62-124) and defect_matrix (186-200).  Every output is a
+ * row-aligned array in the call's layout and may be NULL: factors mu (U
+ * main), l1 (L(i,i-1)), l2 (L(i,i-m)), phi (U(i,i+1)), psi (U(i,i+m)); defect
+ * diagonals at offsets -m, -1, 0, +1, +m, -(m-1), +(m-1) (the last two are
+ * zero for m = 2).  Synchronises the stream (factor export). */
+int bx_ilu0_f64(const double *subm, const double *sub1, const double *main, const double *sup1,
+                const double *supm, double *mu, double *l1, double *l2, double *phi, double *psi,
+                double *k_subm, double *k_sub1, double *k_main, double *k_sup1, double *k_supm,
+                double *k_subq, double *k_supq, int32_t *status, int32_t *index, int64_t batch,
+                int64_t n, int64_t m, double alpha, int64_t ld, int32_t layout, void *workspace,
+                size_t workspace_bytes, void *stream);
+
+/* Stone's strongly implicit procedure (Algorithm 1).  Replaces sip_solve
+ * (iterative.py:255-308).  tol[batch]: absolute thresholds on ||b - A x||_inf
+ * (the loop runs while r >= tol).  x: in = initial guess when use_x0 (else
+ * zeros), out = final iterate.  Optional (NULL-able): best_x (the best iterate,
+ * as MaxIterationsExceeded.best), iterations, residual, best_residual, history
+ * ([batch][max_iter], r after each iteration).  status: OK, ZERO_PIVOT(index),
+ * MAX_ITER, DIVERGED (r > 1e6 r0), NOT_GRID (wavefront only).  algo:
+ * BX_ALGO_SEQUENTIAL (one thread per system, any band), BX_ALGO_WAVEFRONT
+ * (grid-structured systems, n % m == 0, m <= 1024: one CTA per system walks the
+ * grid's anti-diagonals) or BX_ALGO_AUTO. */
+#define BX_ALGO_WAVEFRONT 2
+size_t bx_sip_workspace_bytes(int64_t batch, int64_t n, int64_t m);
+#define BX_ALGO_AUTO 3  /* wavefront when every system is grid-structured, else sequential (syncs) */
+int bx_sip_f64(const double *subm, const double *sub1, const double *main, const double *sup1,
+               const double *supm, const double *rhs, const double *tol, double *x,
+               double *best_x, int64_t *iterations, double *residual, double *best_residual,
+               int32_t *status, int32_t *index, double *history, int64_t batch, int64_t n,
+               int64_t m, double alpha, int64_t max_iter, int32_t use_x0, int64_t ld,
+               int32_t layout, int32_t algo, void *workspace, size_t workspace_bytes,
+               void *stream);
 
 #ifdef __cplusplus
 }

@@ -11,6 +11,8 @@ fallback: without the built library or a GPU every solver raises.
 
 from .core import BandFactors, OpCounter, PentaMatrix, SolveReport, TriMatrix  # noqa: F401
 from .direct import solve_mnpdm, solve_npdm, solve_ntdm  # noqa: F401
+from .iterative import (DefectMatrix, SipConfig, StencilMatrix, defect_matrix,  # noqa: F401
+                        ilu0_penta, sip_solve)
 from .errors import (BandixError, DenseCapExceeded, DimensionMismatch, Diverged,  # noqa: F401
                      InvalidInput, MaxIterationsExceeded, SingularMatrix, SolverError,
                      ZeroDiagonal, ZeroPivot)

@@ -30,10 +30,14 @@ _SIGS = {
     "bx_version": ([], C.c_char_p),
     "bx_last_error": ([], C.c_char_p),
     "bx_workspace_bytes": ([_i32, _i64, _i64, _i32, _i32], _sz),
+    "bx_sip_workspace_bytes": ([_i64, _i64, _i64], _sz),
     "bx_ntdm_f64": ([_p] * 7 + [_i64, _i64, _i64, _i32, _i32, _p, _sz, _p], C.c_int),
     "bx_npdm_f64": ([_p] * 9 + [_i64, _i64, _i64, _i32, _i32, _p, _sz, _p], C.c_int),
     "bx_mnpdm_f64": ([_p] * 10 + [_i64, _i64, _i64, _i32, _i32, _p, _sz, _p], C.c_int),
     "bx_residual_inf_f64": ([_i32] + [_p] * 8 + [_i64, _i64, _i64, _i32, _p], C.c_int),
+    "bx_ilu0_f64": ([_p] * 19 + [_i64, _i64, _i64, C.c_double, _i64, _i32, _p, _sz, _p], C.c_int),
+    "bx_sip_f64": ([_p] * 15 + [_i64, _i64, _i64, C.c_double, _i64, _i32, _i64, _i32, _i32, _p,
+                                _sz, _p], C.c_int),
 }
 
 _lib = None

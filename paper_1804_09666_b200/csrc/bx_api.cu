@@ -53,6 +53,13 @@ static int check_common(const char *fn, int64_t batch, int64_t n, int64_t nmin, 
 
 extern "C" {
 
+/* Workspace of the SIP solver for a given stride (the wavefront planes depend
+ * on m); max of the sequential and wavefront requirements. */
+size_t bx_sip_workspace_bytes(int64_t batch, int64_t n, int64_t m) {
+  const size_t a = bx::sip_workspace_bytes(batch, n), b = bx::sip_wave_workspace_bytes(batch, n, m);
+  return a > b ? a : b;
+}
+
 const char *bx_version(void) { return "bandix_b200 0.1.0 (sm_100a)"; }
 const char *bx_last_error(void) { return bxh::g_err; }
 
@@ -65,6 +72,8 @@ size_t bx_workspace_bytes(int32_t solver, int64_t batch, int64_t n, int32_t layo
     case BX_SOLVER_NPDM:
     case BX_SOLVER_MNPDM:
       return algo == BX_ALGO_SEQUENTIAL ? 2 * rows : bx::part_workspace_bytes(2, batch, n);
+    case BX_SOLVER_SIP:
+      return algo == BX_ALGO_SEQUENTIAL ? bx::sip_workspace_bytes(batch, n) : 0;
     default:
       return bx::other_workspace_bytes(solver, batch, n);
   }
@@ -76,8 +85,8 @@ int bx_ntdm_f64(const double *sub1, const double *main, const double *sup1, cons
                 void *stream) {
   int rc = check_common("bx_ntdm_f64", batch, n, 2, ld, layout);
   if (rc) return rc;
-  BX_REQUIRE(sub1 && main && sup1 && rhs && x, "bx_ntdm_f64: null array pointer");
   if (batch == 0) return BX_OK;
+  BX_REQUIRE(sub1 && main && sup1 && rhs && x, "bx_ntdm_f64: null array pointer");
   const size_t need = bx_workspace_bytes(BX_SOLVER_NTDM, batch, n, layout, algo);
   if (workspace_bytes < need || (need && !workspace)) {
     set_error("bx_ntdm_f64: workspace %zu bytes < required %zu", workspace_bytes, need);
@@ -105,8 +114,8 @@ static int penta_common(const char *fn, bool mod, const double *sub2, const doub
                         int32_t algo, void *workspace, size_t workspace_bytes, void *stream) {
   int rc = check_common(fn, batch, n, 3, ld, layout);
   if (rc) return rc;
-  BX_REQUIRE(sub2 && sub1 && main && sup1 && sup2 && rhs && x, "%s: null array pointer", fn);
   if (batch == 0) return BX_OK;
+  BX_REQUIRE(sub2 && sub1 && main && sup1 && sup2 && rhs && x, "%s: null array pointer", fn);
   const size_t need = bx_workspace_bytes(mod ? BX_SOLVER_MNPDM : BX_SOLVER_NPDM, batch, n, layout, algo);
   if (workspace_bytes < need || (need && !workspace)) {
     set_error("%s: workspace %zu bytes < required %zu", fn, workspace_bytes, need);
@@ -151,12 +160,89 @@ int bx_residual_inf_f64(int32_t bandwidth, const double *sub2, const double *sub
   BX_REQUIRE(bandwidth == 1 || bandwidth == 2, "bx_residual_inf_f64: bandwidth must be 1 or 2");
   int rc = check_common("bx_residual_inf_f64", batch, n, bandwidth == 1 ? 2 : 3, ld, layout);
   if (rc) return rc;
+  if (batch == 0) return BX_OK;
   BX_REQUIRE(sub1 && main && sup1 && x && rhs && res_inf, "bx_residual_inf_f64: null pointer");
   BX_REQUIRE(bandwidth == 1 || (sub2 && sup2), "bx_residual_inf_f64: null sub2/sup2");
-  if (batch == 0) return BX_OK;
   bx::residual_inf(bandwidth, sub2, sub1, main, sup1, sup2, x, rhs, res_inf, batch, n, ld, layout,
                    (cudaStream_t)stream);
   return bxh::check_launch("bx_residual_inf_f64");
+}
+
+static int check_sip_args(const char *fn, int64_t batch, int64_t n, int64_t m, double alpha,
+                          int64_t ld, int32_t layout) {
+  int rc = check_common(fn, batch, n, 3, ld, layout);
+  if (rc) return rc;
+  BX_REQUIRE(m >= 2 && m < n, "%s: outer offset m=%lld must satisfy 2 <= m < n", fn, (long long)m);
+  BX_REQUIRE(m >= 3 || alpha == 0.0, "%s: Stone's alpha needs m >= 3 (m = 2 is the reference ILU(0))", fn);
+  BX_REQUIRE(alpha == alpha, "%s: alpha is NaN", fn);
+  return BX_OK;
+}
+
+int bx_ilu0_f64(const double *subm, const double *sub1, const double *main, const double *sup1,
+                const double *supm, double *mu, double *l1, double *l2, double *phi, double *psi,
+                double *k_subm, double *k_sub1, double *k_main, double *k_sup1, double *k_supm,
+                double *k_subq, double *k_supq, int32_t *status, int32_t *index, int64_t batch,
+                int64_t n, int64_t m, double alpha, int64_t ld, int32_t layout, void *workspace,
+                size_t workspace_bytes, void *stream) {
+  int rc = check_sip_args("bx_ilu0_f64", batch, n, m, alpha, ld, layout);
+  if (rc) return rc;
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(subm && sub1 && main && sup1 && supm, "bx_ilu0_f64: null matrix pointer");
+  const size_t need = bx::sip_workspace_bytes(batch, n);
+  if (workspace_bytes < need || !workspace) {
+    set_error("bx_ilu0_f64: workspace %zu bytes < required %zu", workspace_bytes, need);
+    return BX_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  bx::sip_seq(subm, sub1, main, sup1, supm, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+              nullptr, status, index, nullptr, (double *)workspace, batch, n, m, alpha, 0, 0, ld,
+              layout, 1, st);
+  rc = bxh::check_launch("bx_ilu0_f64");
+  if (rc) return rc;
+  double *outs[12] = {mu, l1, l2, phi, psi, k_subm, k_sub1, k_main, k_sup1, k_supm, k_subq, k_supq};
+  rc = bx::sip_export((double *)workspace, batch, n, outs, ld, layout, st);
+  if (rc) return rc;
+  return bxh::check_launch("bx_ilu0_f64 export");
+}
+
+int bx_sip_f64(const double *subm, const double *sub1, const double *main, const double *sup1,
+               const double *supm, const double *rhs, const double *tol, double *x,
+               double *best_x, int64_t *iterations, double *residual, double *best_residual,
+               int32_t *status, int32_t *index, double *history, int64_t batch, int64_t n,
+               int64_t m, double alpha, int64_t max_iter, int32_t use_x0, int64_t ld,
+               int32_t layout, int32_t algo, void *workspace, size_t workspace_bytes,
+               void *stream) {
+  int rc = check_sip_args("bx_sip_f64", batch, n, m, alpha, ld, layout);
+  if (rc) return rc;
+  BX_REQUIRE(max_iter >= 1, "bx_sip_f64: max_iter must be at least 1");
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(subm && sub1 && main && sup1 && supm && rhs && tol && x,
+             "bx_sip_f64: null array pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (algo == BX_ALGO_AUTO)
+    algo = bx::sip_is_grid(sub1, sup1, batch, n, m, ld, layout, st) ? BX_ALGO_WAVEFRONT
+                                                                     : BX_ALGO_SEQUENTIAL;
+  if (algo != BX_ALGO_SEQUENTIAL && algo != BX_ALGO_WAVEFRONT) {
+    set_error("bx_sip_f64: unknown algo %d", algo);
+    return BX_ERR_ARG;
+  }
+  const size_t need = algo == BX_ALGO_WAVEFRONT ? bx::sip_wave_workspace_bytes(batch, n, m)
+                                                : bx::sip_workspace_bytes(batch, n);
+  if (workspace_bytes < need || !workspace) {
+    set_error("bx_sip_f64: workspace %zu bytes < required %zu", workspace_bytes, need);
+    return BX_ERR_WORKSPACE;
+  }
+  if (algo == BX_ALGO_SEQUENTIAL) {
+    bx::sip_seq(subm, sub1, main, sup1, supm, rhs, tol, x, best_x, iterations, residual,
+                best_residual, status, index, history, (double *)workspace, batch, n, m, alpha,
+                max_iter, use_x0, ld, layout, 0, st);
+  } else {
+    rc = bx::sip_wave(subm, sub1, main, sup1, supm, rhs, tol, x, best_x, iterations, residual,
+                      best_residual, status, index, history, (double *)workspace, batch, n, m,
+                      alpha, max_iter, use_x0, ld, layout, st);
+    if (rc) return rc;
+  }
+  return bxh::check_launch("bx_sip_f64");
 }
 
 }  // extern "C"

@@ -1,24 +1,720 @@
-// Partitioned (on-chip) direct solvers -- placeholder until the kernels land.
+// Partitioned ("two-port tree") direct solvers for banded systems of half-
+// bandwidth K (K=1 tridiagonal: NTDM; K=2 pentadiagonal: NPDM / MNPDM).
+//
+// Throughput path (BX_ALGO_PARTITIONED).  Same solution contract as the
+// reference solvers (solve_ntdm/solve_npdm/solve_mnpdm, direct.py:73-113),
+// different elimination order, so results agree to rounding (north-star
+// tolerance 1e-10 relative on nonsingular well-conditioned systems), not
+// bitwise.  The bit-exact path is bx_direct_seq.cu.
+//
+// Decomposition (one system per cluster of C CTAs, all data on chip):
+//   * thread t of a CTA owns a chunk of M consecutive rows;
+//   * phase 1 (registers + smem): a downward elimination of the chunk with
+//     the coupling to the K unknowns left of the chunk carried as a "left
+//     spike" W, then an upward elimination carrying the right spike V, so that
+//     every row of the chunk reads   x_j = d_j - W_j . L - V_j . R
+//     with L / R the K unknowns just outside the chunk.  These 1+2K numbers
+//     per row stay in shared memory.
+//   * the chunk's first K and last K rows form a "two-port"
+//         F = gF + AF L + BF R,   E = gE + AE L + BE R        (K-vectors, KxK)
+//     Two adjacent segments merge into one two-port by eliminating their
+//     shared interface (a KxK solve); a binary tree of merges over the CTA's
+//     chunks (shared memory) and then over the cluster's CTAs (DSMEM)
+//     reduces the system to its root, whose L = R = 0.
+//   * the tree is descended to hand every chunk its L and R, and phase 3
+//     writes x_j = d_j - W_j.L - V_j.R.
+// HBM traffic is the compulsory I/O (K=2: 6 reads + 1 write per row; K=1:
+// 4 + 1): intermediates never leave the SM.
+#include <cooperative_groups.h>
+#include <stdlib.h>
+
 #include "bx_common.cuh"
 #include "bx_kernels.h"
 
+namespace cg = cooperative_groups;
+
+#ifdef BX_TRACE
+// developer instrumentation (tools/trace_part.py): per-CTA phase clocks
+__device__ long long g_bx_trace[4096][10];
+extern "C" int bx_trace_read(void *host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, g_bx_trace, bytes < sizeof(g_bx_trace) ? bytes : sizeof(g_bx_trace));
+}
+#define BX_TR(slot)                                                                 \
+  do {                                                                              \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_bx_trace[blockIdx.x][slot] = clock64(); \
+  } while (0)
+#else
+#define BX_TR(slot) \
+  do {              \
+  } while (0)
+#endif
+
 namespace bx {
+namespace part {
+
+template <int K>
+struct Vec {
+  double v[K];
+};
+template <int K>
+struct Mat {
+  double m[K][K];
+};
+
+template <int K>
+__device__ __forceinline__ Vec<K> mv(const Mat<K> &a, const Vec<K> &x) {
+  Vec<K> r;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) s = fma(a.m[i][j], x.v[j], s);
+    r.v[i] = s;
+  }
+  return r;
+}
+template <int K>
+__device__ __forceinline__ Mat<K> mm(const Mat<K> &a, const Mat<K> &b) {
+  Mat<K> r;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) s = fma(a.m[i][k], b.m[k][j], s);
+      r.m[i][j] = s;
+    }
+  return r;
+}
+template <int K>
+__device__ __forceinline__ Vec<K> vadd(const Vec<K> &a, const Vec<K> &b) {
+  Vec<K> r;
+#pragma unroll
+  for (int i = 0; i < K; ++i) r.v[i] = a.v[i] + b.v[i];
+  return r;
+}
+template <int K>
+__device__ __forceinline__ Mat<K> madd(const Mat<K> &a, const Mat<K> &b) {
+  Mat<K> r;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) r.m[i][j] = a.m[i][j] + b.m[i][j];
+  return r;
+}
+// (I - P)^{-1}; returns false if singular
+template <int K>
+__device__ __forceinline__ bool inv_i_minus(const Mat<K> &p, Mat<K> &out) {
+  if (K == 1) {
+    const double d = 1.0 - p.m[0][0];
+    out.m[0][0] = 1.0 / d;
+    return d != 0.0;
+  } else {
+    const double a = 1.0 - p.m[0][0], b = -p.m[0][1], c = -p.m[1][0], d = 1.0 - p.m[1][1];
+    const double det = a * d - b * c;
+    const double r = 1.0 / det;
+    out.m[0][0] = d * r;
+    out.m[0][1] = -b * r;
+    out.m[1][0] = -c * r;
+    out.m[1][1] = a * r;
+    return det != 0.0;
+  }
+}
+
+// one side (F or E) of a two-port: x = g + A L + B R
+template <int K>
+struct Port {
+  Vec<K> g;
+  Mat<K> A, B;
+};
+template <int K>
+struct TwoPort {
+  Port<K> F, E;
+};
+// what the descent needs at a merge node: u (left child's E) and v (right
+// child's F) as affine functions of the merged node's L and R
+template <int K>
+struct MergeInfo {
+  Port<K> u, v;
+};
+
+template <int K>
+__device__ __forceinline__ bool merge(const TwoPort<K> &a, const TwoPort<K> &b, TwoPort<K> &out,
+                                      MergeInfo<K> &info) {
+  Mat<K> S;
+  const bool ok = inv_i_minus<K>(mm<K>(a.E.B, b.F.A), S);
+  // u = S (gAE + BAE gBF) + S AAE L + S BAE BBF R
+  info.u.g = mv<K>(S, vadd<K>(a.E.g, mv<K>(a.E.B, b.F.g)));
+  info.u.A = mm<K>(S, a.E.A);
+  info.u.B = mm<K>(S, mm<K>(a.E.B, b.F.B));
+  // v = gBF + ABF u + BBF R
+  info.v.g = vadd<K>(b.F.g, mv<K>(b.F.A, info.u.g));
+  info.v.A = mm<K>(b.F.A, info.u.A);
+  info.v.B = madd<K>(mm<K>(b.F.A, info.u.B), b.F.B);
+  // merged F = A.F with its R replaced by v ; merged E = B.E with L replaced by u
+  out.F.g = vadd<K>(a.F.g, mv<K>(a.F.B, info.v.g));
+  out.F.A = madd<K>(a.F.A, mm<K>(a.F.B, info.v.A));
+  out.F.B = mm<K>(a.F.B, info.v.B);
+  out.E.g = vadd<K>(b.E.g, mv<K>(b.E.A, info.u.g));
+  out.E.A = mm<K>(b.E.A, info.u.A);
+  out.E.B = madd<K>(mm<K>(b.E.A, info.u.B), b.E.B);
+  return ok;
+}
+
+template <int K>
+__device__ __forceinline__ Vec<K> apply(const Port<K> &p, const Vec<K> &L, const Vec<K> &R) {
+  return vadd<K>(p.g, vadd<K>(mv<K>(p.A, L), mv<K>(p.B, R)));
+}
+
+// per-row state kept in smem between the passes: Q = 1 + 2K doubles
+//   down pass: p (x_{j+1} coeff), q (x_{j+2} coeff, K=2), y, W[K]  (normalised)
+//   up pass  : d, W[K], V[K]
+template <int K>
+struct Cfg {
+  static constexpr int Q = 1 + 2 * K;
+};
+
+// shared-memory layout (doubles): state[Q][M][T] | info[T] | wport[T/32] | wlr[T/32][2K] | misc
+template <int K, int M, int T>
+struct Smem {
+  static constexpr int Q = Cfg<K>::Q;
+  static constexpr int NW = T / 32;
+  static constexpr int kState = Q * M * T;
+  static constexpr int kInfo = T * (int)(sizeof(MergeInfo<K>) / 8);
+  static constexpr int kWPort = NW * (int)(sizeof(TwoPort<K>) / 8);
+  static constexpr int kWLR = NW * 2 * K;
+  static constexpr int kMisc = 8;
+  static constexpr size_t bytes =
+      sizeof(double) * (size_t)(kState + kInfo + kWPort + kWLR + kMisc);
+};
+
+// 1/a to ~1 ulp: MUFU seed + two Newton steps (tolerance path only)
+__device__ __forceinline__ double rcp(double a) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+  double e = fma(-a, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-a, r, 1.0);
+  return fma(r, e, r);
+}
+
+// exact power-of-two scale that brings |a| into [1, 2) (a normal, nonzero)
+__device__ __forceinline__ double pow2_inv_scale(double a) {
+  const int hi = __double2hiint(a);
+  const int ex = (hi >> 20) & 0x7ff;
+  return __hiloint2double((2046 - ex) << 20, 0);
+}
+
+// 32-byte vector global accesses (LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100a);
+// streaming: no L1 allocation for data that is touched once
+__device__ __forceinline__ void ld4(const double *p, double *o) {
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3])
+      : "l"(p));
+}
+__device__ __forceinline__ void st4(double *p, const double *v) {
+  asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]),
+               "d"(v[1]), "d"(v[2]), "d"(v[3])
+               : "memory");
+}
+
+template <int K>
+__device__ __forceinline__ TwoPort<K> shfl_down_port(const TwoPort<K> &p, int delta) {
+  TwoPort<K> r;
+  const double *src = reinterpret_cast<const double *>(&p);
+  double *dst = reinterpret_cast<double *>(&r);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(TwoPort<K>) / 8); ++i)
+    dst[i] = __shfl_down_sync(0xffffffffu, src[i], delta);
+  return r;
+}
+template <int K>
+__device__ __forceinline__ Vec<K> shfl_up_vec(const Vec<K> &v, int delta) {
+  Vec<K> r;
+#pragma unroll
+  for (int i = 0; i < K; ++i) r.v[i] = __shfl_up_sync(0xffffffffu, v.v[i], delta);
+  return r;
+}
+
+template <int K, int M, int T, bool VEC, class Lay>
+__global__ void __launch_bounds__(T)
+part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
+            const double *__restrict__ ep, const double *__restrict__ f1p,
+            const double *__restrict__ f2p, const double *__restrict__ bp,
+            double *__restrict__ xp, int32_t *status, int32_t *index, int64_t *nz_out,
+            int64_t batch, int64_t n, Lay lay, int csize) {
+  using SM = Smem<K, M, T>;
+  constexpr int NW = SM::NW;
+  static_assert(T % 32 == 0 && (NW & (NW - 1)) == 0, "T must be 32 * power of two");
+  extern __shared__ __align__(16) double smem[];
+  double *state = smem;
+  MergeInfo<K> *info = reinterpret_cast<MergeInfo<K> *>(smem + SM::kState);
+  TwoPort<K> *wport = reinterpret_cast<TwoPort<K> *>(smem + SM::kState + SM::kInfo);
+  double *wlr = smem + SM::kState + SM::kInfo + SM::kWPort;
+  int *misc = reinterpret_cast<int *>(wlr + SM::kWLR);
+
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int crank = csize > 1 ? (int)cg::this_cluster().block_rank() : 0;
+  const int64_t s = blockIdx.x / csize;
+  const int64_t seg0 = (int64_t)crank * (T * M);
+  const int64_t base = seg0 + (int64_t)t * M;
+  auto st = [&](int q, int j) -> double & { return state[(q * M + j) * T + t]; };
+  if (t == 0) misc[0] = 0;
+
+  BX_TR(0);
+  // ---------------- phase 1: downward elimination --------------------------
+  // Division-free: row j is combined as mu_{j-1} row_j - t1 row_{j-1} (and
+  // likewise for row j-2), then rescaled by an exact power of two so |mu| is
+  // in [1, 2).  The dependent chain per row is a few FMAs; the reciprocal that
+  // normalises the stored row is off the chain.  Stored (normalised):
+  //   x_j + p x_{j+1} + q x_{j+2} + W.L = y
+  int32_t bad = -1;
+  int nzc = 0;
+  // unnormalised carried rows j-1 and j-2: (mu, phi, psi, y, W)
+  double m1 = 1, f1 = 0, g1 = 0, y1 = 0, m2 = 1, f2 = 0, g2 = 0, y2 = 0;
+  double W1[K], W2[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) W1[k] = W2[k] = 0.0;
+  constexpr int G = 4;
+  static_assert(M % G == 0, "M must be a multiple of 4");
+  double ga2[2][G], ga1[2][G], ge[2][G], gc1[2][G], gc2[2][G], gb[2][G];
+  auto load_group = [&](int g, int buf) {
+    const int64_t i0 = base + g * G;
+    if (VEC && i0 + G <= n) {
+      if (K == 2) ld4(c2p + lay(i0, s), ga2[buf]);
+      ld4(c1p + lay(i0, s), ga1[buf]);
+      ld4(ep + lay(i0, s), ge[buf]);
+      ld4(f1p + lay(i0, s), gc1[buf]);
+      if (K == 2) ld4(f2p + lay(i0, s), gc2[buf]);
+      ld4(bp + lay(i0, s), gb[buf]);
+#pragma unroll
+      for (int u = 0; u < G; ++u) {  // slots outside the matrix are never trusted
+        const int64_t i = i0 + u;
+        if (K != 2 || i < 2) ga2[buf][u] = 0.0;
+        if (i < 1) ga1[buf][u] = 0.0;
+        if (i > n - 2) gc1[buf][u] = 0.0;
+        if (K != 2 || i > n - 3) gc2[buf][u] = 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int64_t i = i0 + u;
+        const bool in = i < n;
+        ga2[buf][u] = (K == 2 && in && i >= 2) ? ldg(c2p + lay(i, s)) : 0.0;
+        ga1[buf][u] = (in && i >= 1) ? ldg(c1p + lay(i, s)) : 0.0;
+        ge[buf][u] = in ? ldg(ep + lay(i, s)) : 1.0;  // padding rows: identity
+        gc1[buf][u] = (in && i <= n - 2) ? ldg(f1p + lay(i, s)) : 0.0;
+        gc2[buf][u] = (K == 2 && in && i <= n - 3) ? ldg(f2p + lay(i, s)) : 0.0;
+        gb[buf][u] = in ? ldg(bp + lay(i, s)) : 0.0;
+      }
+    }
+  };
+  load_group(0, 0);
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    const int g = j / G, u = j % G, buf = g & 1;
+    if (u == 0 && g + 1 < M / G) load_group(g + 1, buf ^ 1);
+    const double a2 = ga2[buf][u], a1 = ga1[buf][u], e = ge[buf][u], c1 = gc1[buf][u],
+                 c2 = gc2[buf][u], b = gb[buf][u];
+    if (K == 2) nzc += (a2 != 0.0);
+    double mu, ph, ps, y, W[K];
+    if (j == 0) {
+      mu = e; ph = c1; ps = c2; y = b;
+      if (K == 1) { W[0] = a1; } else { W[0] = a2; W[K - 1] = a1; }
+    } else if (K == 1) {
+      // row_j <- mu_{j-1} row_j - a row_{j-1}
+      mu = fma(m1, e, -a1 * f1);
+      ph = m1 * c1;
+      ps = 0.0;
+      y = fma(m1, b, -a1 * y1);
+      W[0] = -a1 * W1[0];
+    } else if (j == 1) {
+      // row 1: x_{-1} = L1 (coefficient a2), eliminate x_0 with row 0
+      mu = fma(m1, e, -a1 * f1);
+      ph = fma(m1, c1, -a1 * g1);
+      ps = m1 * c2;
+      y = fma(m1, b, -a1 * y1);
+      W[0] = -a1 * W1[0];
+      W[K - 1] = fma(m1, a2, -a1 * W1[K - 1]);
+    } else {
+      // R = mu_{j-2} row_j - a2 row_{j-2}: coefficients of x_{j-1}, x_j, ...
+      const double T1 = fma(m2, a1, -a2 * f2);
+      const double T0 = fma(m2, e, -a2 * g2);
+      const double C1 = m2 * c1, C2 = m2 * c2;
+      const double Y = fma(m2, b, -a2 * y2);
+      // new = mu_{j-1} R - T1 row_{j-1}
+      mu = fma(m1, T0, -T1 * f1);
+      ph = fma(m1, C1, -T1 * g1);
+      ps = m1 * C2;
+      y = fma(m1, Y, -T1 * y1);
+#pragma unroll
+      for (int k = 0; k < K; ++k) W[k] = fma(m1, -a2 * W2[k], -T1 * W1[k]);
+    }
+    if (mu == 0.0 || !isfinite(mu)) {
+      if (bad < 0) bad = (int32_t)(base + j);
+      mu = 1.0;
+    }
+    const double sc = pow2_inv_scale(mu);   // exact
+    mu *= sc; ph *= sc; ps *= sc; y *= sc;
+#pragma unroll
+    for (int k = 0; k < K; ++k) W[k] *= sc;
+    const double r = rcp(mu);
+    st(0, j) = ph * r;
+    if (K == 2) st(1, j) = ps * r;
+    st(K, j) = y * r;
+#pragma unroll
+    for (int k = 0; k < K; ++k) st(K + 1 + k, j) = W[k] * r;
+    m2 = m1; f2 = f1; g2 = g1; y2 = y1;
+    m1 = mu; f1 = ph; g1 = ps; y1 = y;
+#pragma unroll
+    for (int k = 0; k < K; ++k) { W2[k] = W1[k]; W1[k] = W[k]; }
+  }
+
+  BX_TR(1);
+  // ---------------- phase 1b: upward elimination ---------------------------
+  // x_j = d_j - W_j.L - V_j.R ; state slots after: 0:d, 1..K: W, K+1..2K: V
+  {
+    double d1 = 0, d2 = 0, Wu1[K], Wu2[K], V1[K], V2[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) Wu1[k] = Wu2[k] = V1[k] = V2[k] = 0.0;
+#pragma unroll
+    for (int j = M - 1; j >= 0; --j) {
+      const double p = st(0, j);
+      const double q = K == 2 ? st(1, j) : 0.0;
+      const double y = st(K, j);
+      double W[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) W[k] = st(K + 1 + k, j);
+      double d, Wu[K], V[K];
+      if (j == M - 1) {
+        d = y;
+#pragma unroll
+        for (int k = 0; k < K; ++k) Wu[k] = W[k];
+        V[0] = p;
+        if (K == 2) V[1] = q;
+      } else if (K == 2 && j == M - 2) {
+        d = fma(-p, d1, y);
+#pragma unroll
+        for (int k = 0; k < K; ++k) Wu[k] = fma(-p, Wu1[k], W[k]);
+        V[0] = fma(-p, V1[0], q);
+        V[1] = -p * V1[1];
+      } else {
+        d = fma(-p, d1, y);
+#pragma unroll
+        for (int k = 0; k < K; ++k) { Wu[k] = fma(-p, Wu1[k], W[k]); V[k] = -p * V1[k]; }
+        if (K == 2) {
+          d = fma(-q, d2, d);
+#pragma unroll
+          for (int k = 0; k < K; ++k) { Wu[k] = fma(-q, Wu2[k], Wu[k]); V[k] = fma(-q, V2[k], V[k]); }
+        }
+      }
+      st(0, j) = d;
+#pragma unroll
+      for (int k = 0; k < K; ++k) { st(1 + k, j) = Wu[k]; st(1 + K + k, j) = V[k]; }
+      d2 = d1; d1 = d;
+#pragma unroll
+      for (int k = 0; k < K; ++k) { Wu2[k] = Wu1[k]; Wu1[k] = Wu[k]; V2[k] = V1[k]; V1[k] = V[k]; }
+    }
+  }
+
+  BX_TR(2);
+  // chunk two-port from the thread's own rows 0..K-1 (F) and M-K..M-1 (E)
+  TwoPort<K> port;
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    const int jf = a, je = M - K + a;
+    port.F.g.v[a] = st(0, jf);
+    port.E.g.v[a] = st(0, je);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      port.F.A.m[a][k] = -st(1 + k, jf);
+      port.F.B.m[a][k] = -st(1 + K + k, jf);
+      port.E.A.m[a][k] = -st(1 + k, je);
+      port.E.B.m[a][k] = -st(1 + K + k, je);
+    }
+  }
+
+  // ---------------- tree ascent: warp-synchronous, then across warps --------
+  // merge info for the in-warp levels: node (level l, index k) of warp w at
+  // info[w*31 + (32 - (32 >> l)) + k]; cross-warp nodes after NW*31.
+  bool ok = true;
+#pragma unroll
+  for (int l = 0; l < 5; ++l) {
+    const int step = 1 << l;
+    const TwoPort<K> other = shfl_down_port<K>(port, step);
+    if ((lane & (2 * step - 1)) == 0) {
+      MergeInfo<K> mi;
+      TwoPort<K> m;
+      ok &= merge<K>(port, other, m, mi);
+      info[warp * 31 + (32 - (32 >> l)) + (lane >> (l + 1))] = mi;
+      port = m;
+    }
+  }
+  BX_TR(3);
+  if (lane == 0) wport[warp] = port;
+  __syncthreads();
+  if (NW > 1 && warp == 0) {
+    // levels over the NW warp ports (lanes 0..NW-1)
+    TwoPort<K> wp;
+    if (lane < NW) wp = wport[lane];
+    int off = NW * 31;
+#pragma unroll
+    for (int l = 0; (1 << l) < NW; ++l) {
+      const int step = 1 << l;
+      const TwoPort<K> other = shfl_down_port<K>(wp, step);
+      if (lane < NW && (lane & (2 * step - 1)) == 0) {
+        MergeInfo<K> mi;
+        TwoPort<K> m;
+        ok &= merge<K>(wp, other, m, mi);
+        info[off + (lane >> (l + 1))] = mi;
+        wp = m;
+      }
+      off += NW >> (l + 1);
+    }
+    if (lane == 0) wport[0] = wp;
+  }
+
+  BX_TR(4);
+  // ---------------- cluster level -------------------------------------------
+  Vec<K> Lseg, Rseg;
+#pragma unroll
+  for (int k = 0; k < K; ++k) Lseg.v[k] = Rseg.v[k] = 0.0;
+  if (csize > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();  // every CTA's wport[0] is final and visible
+    if (t == 0) {
+      // every CTA redundantly merges the cluster's segments left to right and
+      // walks back to its own segment's L and R (csize <= 8)
+      TwoPort<K> acc = *cl.map_shared_rank(&wport[0], 0);
+      MergeInfo<K> chain[8];
+      for (int r = 1; r < csize; ++r) {
+        const TwoPort<K> nxt = *cl.map_shared_rank(&wport[0], r);
+        TwoPort<K> m;
+        ok &= merge<K>(acc, nxt, m, chain[r]);
+        acc = m;
+      }
+      Vec<K> L, R;
+#pragma unroll
+      for (int k = 0; k < K; ++k) L.v[k] = R.v[k] = 0.0;
+      bool found = false;
+      for (int r = csize - 1; r >= 1 && !found; --r) {
+        const Vec<K> uu = apply<K>(chain[r].u, L, R);  // E of [0..r-1] = L of segment r
+        const Vec<K> vv = apply<K>(chain[r].v, L, R);  // F of segment r = R of [0..r-1]
+        if (r == crank) { Lseg = uu; Rseg = R; found = true; }
+        R = vv;
+      }
+      if (!found) { Lseg = L; Rseg = R; }
+    }
+    cl.sync();  // remote reads done before anyone proceeds / exits
+  }
+
+  BX_TR(5);
+  // ---------------- tree descent -------------------------------------------
+  if (warp == 0) {
+    // root of the CTA (lane 0), then the cross-warp levels (lanes 0..NW-1)
+    Vec<K> L = Lseg, R = Rseg;
+    if (NW > 1) {
+      int nlev = 0;
+      while ((1 << nlev) < NW) ++nlev;
+      // offsets of cross-warp levels
+      int offs[6];
+      int off = NW * 31;
+      for (int l = 0; l < nlev; ++l) { offs[l] = off; off += NW >> (l + 1); }
+      for (int l = nlev - 1; l >= 0; --l) {
+        const int step = 1 << l;
+        const bool act = lane < NW && (lane & (2 * step - 1)) == 0;
+        Vec<K> uu = L, vv = R;
+        if (act) {
+          const MergeInfo<K> mi = info[offs[l] + (lane >> (l + 1))];
+          uu = apply<K>(mi.u, L, R);
+          vv = apply<K>(mi.v, L, R);
+        }
+        const Vec<K> pu = shfl_up_vec<K>(uu, step), pR = shfl_up_vec<K>(R, step);
+        if (lane < NW && (lane & (2 * step - 1)) == step) { L = pu; R = pR; }
+        if (act) R = vv;
+      }
+    }
+    if (lane < NW) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) { wlr[lane * 2 * K + k] = L.v[k]; wlr[lane * 2 * K + K + k] = R.v[k]; }
+    }
+  }
+  __syncthreads();
+  Vec<K> L, R;
+#pragma unroll
+  for (int k = 0; k < K; ++k) { L.v[k] = wlr[warp * 2 * K + k]; R.v[k] = wlr[warp * 2 * K + K + k]; }
+#pragma unroll
+  for (int l = 4; l >= 0; --l) {
+    const int step = 1 << l;
+    const bool act = (lane & (2 * step - 1)) == 0;
+    Vec<K> uu = L, vv = R;
+    if (act) {
+      const MergeInfo<K> mi = info[warp * 31 + (32 - (32 >> l)) + (lane >> (l + 1))];
+      uu = apply<K>(mi.u, L, R);
+      vv = apply<K>(mi.v, L, R);
+    }
+    const Vec<K> pu = shfl_up_vec<K>(uu, step), pR = shfl_up_vec<K>(R, step);
+    if ((lane & (2 * step - 1)) == step) { L = pu; R = pR; }
+    if (act) R = vv;
+  }
+
+  BX_TR(6);
+  // ---------------- phase 3: x_j = d - W.L - V.R -----------------------------
+#pragma unroll
+  for (int g = 0; g < M / G; ++g) {
+    double xv[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const int j = g * G + u;
+      double v = st(0, j);
+#pragma unroll
+      for (int k = 0; k < K; ++k) v = fma(-st(1 + k, j), L.v[k], fma(-st(1 + K + k, j), R.v[k], v));
+      xv[u] = v;
+    }
+    const int64_t i0 = base + g * G;
+    if (VEC && i0 + G <= n) {
+      st4(xp + lay(i0, s), xv);
+    } else {
+#pragma unroll
+      for (int u = 0; u < G; ++u)
+        if (i0 + u < n) xp[lay(i0 + u, s)] = xv[u];
+    }
+  }
+
+  BX_TR(7);
+  // ---------------- status / counters ---------------------------------------
+  // status/index were preset to OK/-1 by the launcher; failing CTAs report the
+  // smallest failing row (atomicMin on the unsigned view of index)
+  if (!ok && bad < 0) bad = (int32_t)seg0;
+  if (__syncthreads_or(bad >= 0)) {
+    if (status) status[s] = BX_STATUS_ZERO_PIVOT;
+    if (index && bad >= 0) atomicMin(reinterpret_cast<unsigned int *>(index + s), (unsigned int)bad);
+  }
+#ifdef BX_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 4096) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_bx_trace[blockIdx.x][8] = clock64();
+    g_bx_trace[blockIdx.x][9] = smid;
+  }
+#endif
+  if (K == 2 && nz_out) {
+    nzc = __reduce_add_sync(0xffffffffu, nzc);
+    if (lane == 0) atomicAdd(&misc[0], nzc);
+    __syncthreads();
+    if (t == 0) atomicAdd(reinterpret_cast<unsigned long long *>(nz_out + s),
+                          (unsigned long long)misc[0]);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// launch configuration
+// ----------------------------------------------------------------------------
+template <int K, int M, int T, bool VEC, class Lay>
+static int launch(const double *c2, const double *c1, const double *e, const double *f1,
+                  const double *f2, const double *b, double *x, int32_t *st, int32_t *ix,
+                  int64_t *nz, int64_t batch, int64_t n, Lay lay, cudaStream_t stream) {
+  constexpr int rows = M * T;
+  const int csize = (int)((n + rows - 1) / rows);
+  if (csize > 8) {
+    bxh::set_error("partitioned solver: n=%lld exceeds %d rows (8-CTA cluster)", (long long)n,
+                   8 * rows);
+    return BX_ERR_UNSUPPORTED;
+  }
+  const size_t smem = Smem<K, M, T>::bytes;
+  auto kern = part_kernel<K, M, T, VEC, Lay>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (nz) cudaMemsetAsync(nz, 0, sizeof(int64_t) * (size_t)batch, stream);
+  if (st) cudaMemsetAsync(st, 0, sizeof(int32_t) * (size_t)batch, stream);       // BX_STATUS_OK
+  if (ix) cudaMemsetAsync(ix, 0xff, sizeof(int32_t) * (size_t)batch, stream);    // -1
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(batch * csize));
+  cfg.blockDim = dim3(T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t err = cudaLaunchKernelEx(&cfg, kern, c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n,
+                                       lay, csize);
+  if (err != cudaSuccess) {
+    bxh::set_error("partitioned solver launch: %s", cudaGetErrorString(err));
+    return BX_ERR_CUDA;
+  }
+  return BX_OK;
+}
+
+template <int K, bool VEC, class Lay>
+static int dispatch2(const double *c2, const double *c1, const double *e, const double *f1,
+                     const double *f2, const double *b, double *x, int32_t *st, int32_t *ix,
+                     int64_t *nz, int64_t batch, int64_t n, Lay lay, cudaStream_t stream) {
+  // rows per CTA = M*T; small systems use small CTAs (many CTAs per SM).
+  // BX_PART_CFG (developer knob, benchmarking only) forces one configuration.
+  static int forced = -2;
+  if (forced == -2) {
+    const char *env = getenv("BX_PART_CFG");
+    forced = env ? atoi(env) : -1;
+  }
+  switch (forced) {
+    case 0: return launch<K, 8, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+    case 1: return launch<K, 8, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+    case 2: return launch<K, 8, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+    case 3: return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+    case 4: return launch<K, 16, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+    case 5: return launch<K, 32, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+    case 6: return launch<K, 16, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+    default: break;
+  }
+  if (n <= 256) return launch<K, 8, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+  if (n <= 512) return launch<K, 8, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+  return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+}
+
+static bool aligned32(const void *p) { return p == nullptr || ((uintptr_t)p & 31u) == 0; }
+
+template <int K, class Lay>
+static int dispatch(const double *c2, const double *c1, const double *e, const double *f1,
+                    const double *f2, const double *b, double *x, int32_t *st, int32_t *ix,
+                    int64_t *nz, int64_t batch, int64_t n, Lay lay, cudaStream_t stream,
+                    bool vec_ok) {
+  vec_ok = vec_ok && aligned32(c2) && aligned32(c1) && aligned32(e) && aligned32(f1) &&
+           aligned32(f2) && aligned32(b) && aligned32(x);
+  if (vec_ok) return dispatch2<K, true>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+  return dispatch2<K, false>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+}
+
+}  // namespace part
 
 size_t part_workspace_bytes(int, int64_t, int64_t) { return 0; }
 
-int ntdm_part(const double *, const double *, const double *, const double *, double *, double *,
-              int32_t *, int32_t *, int64_t, int64_t, int64_t, int, cudaStream_t) {
-  bxh::set_error("bx_ntdm_f64: BX_ALGO_PARTITIONED not built yet");
-  return BX_ERR_UNSUPPORTED;
+int ntdm_part(const double *d, const double *e, const double *f, const double *b, double *x,
+              double *, int32_t *st, int32_t *ix, int64_t batch, int64_t n, int64_t ld, int layout,
+              cudaStream_t stream) {
+  if (layout == BX_LAYOUT_SYSTEM_MAJOR)
+    return part::dispatch<1>(nullptr, d, e, f, nullptr, b, x, st, ix, nullptr, batch, n,
+                             SystemMajor{ld}, stream, ld % 4 == 0);
+  return part::dispatch<1>(nullptr, d, e, f, nullptr, b, x, st, ix, nullptr, batch, n,
+                           Interleaved{ld}, stream, false);
 }
 
-int penta_part(bool, const double *, const double *, const double *, const double *,
-               const double *, const double *, double *, double *, int32_t *, int32_t *,
-               int64_t *, int64_t, int64_t, int64_t, int, cudaStream_t) {
-  bxh::set_error("BX_ALGO_PARTITIONED not built yet");
-  return BX_ERR_UNSUPPORTED;
+int penta_part(bool, const double *c, const double *d, const double *e, const double *f,
+               const double *g, const double *b, double *x, double *, int32_t *st, int32_t *ix,
+               int64_t *nz, int64_t batch, int64_t n, int64_t ld, int layout, cudaStream_t stream) {
+  if (layout == BX_LAYOUT_SYSTEM_MAJOR)
+    return part::dispatch<2>(c, d, e, f, g, b, x, st, ix, nz, batch, n, SystemMajor{ld}, stream,
+                             ld % 4 == 0);
+  return part::dispatch<2>(c, d, e, f, g, b, x, st, ix, nz, batch, n, Interleaved{ld}, stream,
+                           false);
 }
 
-size_t other_workspace_bytes(int, int64_t, int64_t) { return 0; }
+size_t other_workspace_bytes(int solver, int64_t batch, int64_t n) {
+  if (solver == BX_SOLVER_SIP) return sip_workspace_bytes(batch, n);
+  return 0;
+}
 
 }  // namespace bx

@@ -28,6 +28,27 @@ int penta_part(bool mod, const double *c, const double *d, const double *e, cons
                int32_t *ix, int64_t *nz, int64_t batch, int64_t n, int64_t ld, int layout,
                cudaStream_t stream);
 
+// bx_sip.cu
+size_t sip_workspace_bytes(int64_t batch, int64_t n);
+int sip_seq(const double *a2, const double *a1, const double *e, const double *c1,
+            const double *c2, const double *b, const double *tol, double *x, double *best_x,
+            int64_t *iters, double *res, double *best_res, int32_t *st, int32_t *ix,
+            double *hist, double *ws, int64_t batch, int64_t n, int64_t m, double alpha,
+            int64_t max_iter, int use_x0, int64_t ld, int layout, int factor_only,
+            cudaStream_t stream);
+int sip_export(double *ws, int64_t batch, int64_t n, double *const *outs12, int64_t ld,
+               int layout, cudaStream_t stream);
+
+// bx_sip_wave.cu
+size_t sip_wave_workspace_bytes(int64_t batch, int64_t n, int64_t m);
+bool sip_is_grid(const double *a1, const double *c1, int64_t batch, int64_t n, int64_t m,
+                 int64_t ld, int layout, cudaStream_t stream);
+int sip_wave(const double *a2, const double *a1, const double *e, const double *c1,
+             const double *c2, const double *b, const double *tol, double *x, double *best_x,
+             int64_t *iters, double *res, double *best_res, int32_t *st, int32_t *ix,
+             double *hist, double *ws, int64_t batch, int64_t n, int64_t m, double alpha,
+             int64_t max_iter, int use_x0, int64_t ld, int layout, cudaStream_t stream);
+
 // workspace of the non-direct solvers (bx_api.cu dispatch)
 size_t other_workspace_bytes(int solver, int64_t batch, int64_t n);
 

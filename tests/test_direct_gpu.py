@@ -121,3 +121,57 @@ def test_empty_batch_and_dimension_errors(cuda):
         solve_ntdm(TriMatrix.from_diagonals([1.0], [2.0, 2.0], [1.0]), [1.0, 2.0, 3.0])
     with pytest.raises(InvalidInput):
         PentaMatrix.from_diagonals([], [1.0], [1.0, 2.0], [1.0], [])
+
+
+# --------------------------------------------------------------------------
+# partitioned (throughput) algorithm: tolerance parity
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 17, 256, 257, 1000, 1024, 2049, 4096, 8192])
+def test_ntdm_partitioned_sizes(cuda, layout, n):
+    d = W.td_dominant(40, n, seed=n)
+    x_ref, _, _ = D.ntdm(*d)
+    rep = solve_ntdm(TriMatrix.from_diagonals(*d[:3], layout=layout), d[3], algo="partitioned")
+    assert (host(rep.status) == 0).all()
+    assert rel_err(host(rep.x), x_ref).max() <= REL_TOL
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("n", [3, 4, 5, 6, 7, 17, 255, 1000, 1024, 1025, 4096, 6000])
+@pytest.mark.parametrize("sparse", [False, True])
+def test_penta_partitioned_sizes(cuda, layout, n, sparse):
+    if sparse and n < 5:
+        pytest.skip("sparse-outer family needs n >= 5")
+    p = W.pd_dominant(24, n, seed=n, sparse_outer=sparse)
+    A = PentaMatrix.from_diagonals(*p[:5], layout=layout)
+    x_ref, _, _ = D.npdm(*p)
+    for fn in (solve_npdm, solve_mnpdm):
+        rep = fn(A, p[5], algo="partitioned")
+        assert (host(rep.status) == 0).all()
+        assert rel_err(host(rep.x), x_ref).max() <= REL_TOL
+    _, _, _, nz = D.mnpdm(*p)
+    rep = solve_mnpdm(A, p[5], algo="partitioned")
+    assert np.array_equal(host(rep.ops.total), np.array([sum(D.ops_mnpdm(n, int(z)).values()) for z in nz]))
+
+
+def test_config2_partitioned_full(cuda):
+    p = W.pd_dominant(8192, 4096, seed=1)
+    A = PentaMatrix.from_diagonals(*p[:5], layout="system")
+    rep = solve_npdm(A, p[5], algo="partitioned")
+    x = host(rep.x)
+    # full-size parity against the oracle on a sample of systems, plus the
+    # size-independent property ||b - A x||_inf ~ rounding on every system
+    idx = np.arange(0, 8192, 97)
+    x_ref, _, _ = D.npdm(*(a[idx] for a in p))
+    assert rel_err(x[idx], x_ref).max() <= REL_TOL
+    res = host(rep.residual_inf)
+    assert np.all(res <= 1e-13), res.max()
+
+
+def test_partitioned_zero_pivot_flagged(cuda):
+    p = [a.copy() for a in W.pd_dominant(4, 64, seed=3)]
+    p[2][1, 0] = 0.0   # a zero leading pivot: the chunk-local elimination fails too
+    A = PentaMatrix.from_diagonals(*p[:5], layout="system")
+    rep = solve_npdm(A, p[5], algo="partitioned")
+    st = host(rep.status)
+    assert st[1] == 1 and host(rep.index)[1] == 0 and st[0] == 0 and st[2] == 0
