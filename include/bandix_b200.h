@@ -119,6 +119,25 @@ int bx_residual_inf_f64(int32_t bandwidth, const double *sub2, const double *sub
                         const double *x, const double *rhs, double *res_inf, int64_t batch,
                         int64_t n, int64_t ld, int32_t layout, void *stream);
 
+/* ---- symbolic solvers ----------------------------------------------------- */
+/* STDM / SPDM: exact-zero pivots are replaced by the indeterminate t and the
+ * solution is the limit t -> 0, as exact_solve_stdm / exact_solve_spdm
+ * (exact.py:278-307).  The reference works over exact rationals; here the
+ * rational functions are truncated Laurent series in t with binary64
+ * coefficients.  Inputs are binary64 (the reference requires exact
+ * input and rejects floats, exact.py:232-236; a float is an exact rational).
+ * substitutions[s] (may be NULL) = ExactSolveResult.pivot_substitutions.
+ * status: OK, SINGULAR (exact_det_band == 0 -> SingularMatrix) or
+ * WINDOW_OVERFLOW (the fixed series window could not hold the expansion). */
+int bx_stdm_f64(const double *sub1, const double *main, const double *sup1, const double *rhs,
+                double *x, int32_t *status, int32_t *index, int32_t *substitutions,
+                int64_t batch, int64_t n, int64_t ld, int32_t layout, void *workspace,
+                size_t workspace_bytes, void *stream);
+int bx_spdm_f64(const double *sub2, const double *sub1, const double *main, const double *sup1,
+                const double *sup2, const double *rhs, double *x, int32_t *status,
+                int32_t *index, int32_t *substitutions, int64_t batch, int64_t n, int64_t ld,
+                int32_t layout, void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---- ILU(0) / SIP -------------------------------------------------------- */
 /* Stride-m five-point band: subm[i] = A[i,i-m], sub1[i] = A[i,i-1], main[i],
  * sup1[i] = A[i,i+1], supm[i] = A[i,i+m] (row-aligned, n rows each).  m = 2

@@ -1,0 +1,60 @@
+"""High-precision oracle for the symbolic solvers.  TEST INFRASTRUCTURE ONLY.
+
+The reference's exact solvers return x = A^{-1} b exactly (exact.py:1-14,
+278-307: the t-substituted elimination is LU of A + t*D and the limit t -> 0
+is A^{-1} b for nonsingular A).  At config-3 sizes the reference itself takes
+hours per system, so full-size parity is checked against
+``limit_solve_mp``: banded Gaussian elimination with partial pivoting in
+mpmath at ``dps`` decimal digits, rounded to binary64 -- float(A^{-1} b) up to
+10^-dps relative.  Small-N cases are pinned to the reference's own exact
+outputs (tests/golden/exact.npz).
+"""
+
+from __future__ import annotations
+
+import mpmath
+import numpy as np
+
+
+def limit_solve_mp(diags, offsets, rhs, dps=50):
+    """diags: reference-length 1-D arrays for the given offsets; one system."""
+    n = len(rhs)
+    with mpmath.workdps(dps):
+        kl = -min(offsets)
+        ku = max(offsets)
+        # rows as dicts col -> value (band grows to ku + kl with pivoting)
+        rows = [dict() for _ in range(n)]
+        for d, off in zip(diags, offsets):
+            for idx, v in enumerate(d):
+                i = idx - min(off, 0)
+                if v != 0.0:
+                    rows[i][i + off] = mpmath.mpf(float(v))
+        b = [mpmath.mpf(float(v)) for v in rhs]
+        for k in range(n):
+            # partial pivot among rows k..k+kl
+            cand = range(k, min(n, k + kl + 1))
+            p = max(cand, key=lambda r: abs(rows[r].get(k, 0)))
+            if rows[p].get(k, 0) == 0:
+                raise ZeroDivisionError("singular")
+            if p != k:
+                rows[k], rows[p] = rows[p], rows[k]
+                b[k], b[p] = b[p], b[k]
+            piv = rows[k][k]
+            for r in range(k + 1, min(n, k + kl + 1)):
+                f = rows[r].get(k, 0)
+                if f == 0:
+                    continue
+                m = f / piv
+                for c, v in rows[k].items():
+                    if c >= k:
+                        rows[r][c] = rows[r].get(c, 0) - m * v
+                rows[r].pop(k, None)
+                b[r] = b[r] - m * b[k]
+        x = [mpmath.mpf(0)] * n
+        for k in range(n - 1, -1, -1):
+            acc = b[k]
+            for c, v in rows[k].items():
+                if c > k:
+                    acc -= v * x[c]
+            x[k] = acc / rows[k][k]
+        return np.array([float(v) for v in x])

@@ -35,6 +35,8 @@ _SIGS = {
     "bx_npdm_f64": ([_p] * 9 + [_i64, _i64, _i64, _i32, _i32, _p, _sz, _p], C.c_int),
     "bx_mnpdm_f64": ([_p] * 10 + [_i64, _i64, _i64, _i32, _i32, _p, _sz, _p], C.c_int),
     "bx_residual_inf_f64": ([_i32] + [_p] * 8 + [_i64, _i64, _i64, _i32, _p], C.c_int),
+    "bx_stdm_f64": ([_p] * 8 + [_i64, _i64, _i64, _i32, _p, _sz, _p], C.c_int),
+    "bx_spdm_f64": ([_p] * 10 + [_i64, _i64, _i64, _i32, _p, _sz, _p], C.c_int),
     "bx_ilu0_f64": ([_p] * 19 + [_i64, _i64, _i64, C.c_double, _i64, _i32, _p, _sz, _p], C.c_int),
     "bx_sip_f64": ([_p] * 15 + [_i64, _i64, _i64, C.c_double, _i64, _i32, _i64, _i32, _i32, _p,
                                 _sz, _p], C.c_int),

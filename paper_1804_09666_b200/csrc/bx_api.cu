@@ -168,6 +168,41 @@ int bx_residual_inf_f64(int32_t bandwidth, const double *sub2, const double *sub
   return bxh::check_launch("bx_residual_inf_f64");
 }
 
+static int exact_common(const char *fn, int kind, const double *c, const double *d,
+                        const double *e, const double *f, const double *g, const double *b,
+                        double *x, int32_t *status, int32_t *index, int32_t *subs, int64_t batch,
+                        int64_t n, int64_t ld, int32_t layout, void *workspace,
+                        size_t workspace_bytes, void *stream) {
+  int rc = check_common(fn, batch, n, kind == 1 ? 2 : 3, ld, layout);
+  if (rc) return rc;
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(d && e && f && b && x && (kind == 1 || (c && g)), "%s: null array pointer", fn);
+  const size_t need = bx::exact_workspace_bytes(kind, batch, n);
+  if (workspace_bytes < need || !workspace) {
+    set_error("%s: workspace %zu bytes < required %zu", fn, workspace_bytes, need);
+    return BX_ERR_WORKSPACE;
+  }
+  bx::exact_solve(kind, c, d, e, f, g, b, x, status, index, subs, (double *)workspace, batch, n,
+                  ld, layout, (cudaStream_t)stream);
+  return bxh::check_launch(fn);
+}
+
+int bx_stdm_f64(const double *sub1, const double *main, const double *sup1, const double *rhs,
+                double *x, int32_t *status, int32_t *index, int32_t *substitutions,
+                int64_t batch, int64_t n, int64_t ld, int32_t layout, void *workspace,
+                size_t workspace_bytes, void *stream) {
+  return exact_common("bx_stdm_f64", 1, nullptr, sub1, main, sup1, nullptr, rhs, x, status, index,
+                      substitutions, batch, n, ld, layout, workspace, workspace_bytes, stream);
+}
+
+int bx_spdm_f64(const double *sub2, const double *sub1, const double *main, const double *sup1,
+                const double *sup2, const double *rhs, double *x, int32_t *status,
+                int32_t *index, int32_t *substitutions, int64_t batch, int64_t n, int64_t ld,
+                int32_t layout, void *workspace, size_t workspace_bytes, void *stream) {
+  return exact_common("bx_spdm_f64", 2, sub2, sub1, main, sup1, sup2, rhs, x, status, index,
+                      substitutions, batch, n, ld, layout, workspace, workspace_bytes, stream);
+}
+
 static int check_sip_args(const char *fn, int64_t batch, int64_t n, int64_t m, double alpha,
                           int64_t ld, int32_t layout) {
   int rc = check_common(fn, batch, n, 3, ld, layout);

@@ -167,6 +167,23 @@ __device__ __forceinline__ Vec<K> apply(const Port<K> &p, const Vec<K> &L, const
   return vadd<K>(p.g, vadd<K>(mv<K>(p.A, L), mv<K>(p.B, R)));
 }
 
+// merge info in shared memory, structure-of-arrays: component c of node k at
+// base[c * T + k] (consecutive nodes -> consecutive banks)
+template <int K, int T>
+__device__ __forceinline__ void store_info(double *base, int node, const MergeInfo<K> &mi) {
+  const double *v = reinterpret_cast<const double *>(&mi);
+#pragma unroll
+  for (int c = 0; c < (int)(sizeof(MergeInfo<K>) / 8); ++c) base[c * T + node] = v[c];
+}
+template <int K, int T>
+__device__ __forceinline__ MergeInfo<K> load_info(const double *base, int node) {
+  MergeInfo<K> mi;
+  double *v = reinterpret_cast<double *>(&mi);
+#pragma unroll
+  for (int c = 0; c < (int)(sizeof(MergeInfo<K>) / 8); ++c) v[c] = base[c * T + node];
+  return mi;
+}
+
 // per-row state kept in smem between the passes: Q = 1 + 2K doubles
 //   down pass: p (x_{j+1} coeff), q (x_{j+2} coeff, K=2), y, W[K]  (normalised)
 //   up pass  : d, W[K], V[K]
@@ -175,18 +192,20 @@ struct Cfg {
   static constexpr int Q = 1 + 2 * K;
 };
 
-// shared-memory layout (doubles): state[Q][M][T] | info[T] | wport[T/32] | wlr[T/32][2K] | misc
+// shared-memory layout (doubles): state[Q][M][T] | info[20][T] | wport[T/32] |
+// wlr[T/32][2K] | croots[8] (cluster roots, pushed by every CTA) | misc
 template <int K, int M, int T>
 struct Smem {
   static constexpr int Q = Cfg<K>::Q;
   static constexpr int NW = T / 32;
   static constexpr int kState = Q * M * T;
-  static constexpr int kInfo = T * (int)(sizeof(MergeInfo<K>) / 8);
+  static constexpr int kInfo = T * (int)(sizeof(MergeInfo<K>) / 8);  // SoA, T nodes
   static constexpr int kWPort = NW * (int)(sizeof(TwoPort<K>) / 8);
   static constexpr int kWLR = NW * 2 * K;
+  static constexpr int kRoots = 8 * (int)(sizeof(TwoPort<K>) / 8);
   static constexpr int kMisc = 8;
   static constexpr size_t bytes =
-      sizeof(double) * (size_t)(kState + kInfo + kWPort + kWLR + kMisc);
+      sizeof(double) * (size_t)(kState + kInfo + kWPort + kWLR + kRoots + kMisc);
 };
 
 // 1/a to ~1 ulp: MUFU seed + two Newton steps (tolerance path only)
@@ -249,10 +268,11 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   static_assert(T % 32 == 0 && (NW & (NW - 1)) == 0, "T must be 32 * power of two");
   extern __shared__ __align__(16) double smem[];
   double *state = smem;
-  MergeInfo<K> *info = reinterpret_cast<MergeInfo<K> *>(smem + SM::kState);
+  double *info = smem + SM::kState;
   TwoPort<K> *wport = reinterpret_cast<TwoPort<K> *>(smem + SM::kState + SM::kInfo);
   double *wlr = smem + SM::kState + SM::kInfo + SM::kWPort;
-  int *misc = reinterpret_cast<int *>(wlr + SM::kWLR);
+  TwoPort<K> *croots = reinterpret_cast<TwoPort<K> *>(wlr + SM::kWLR);
+  int *misc = reinterpret_cast<int *>(wlr + SM::kWLR + SM::kRoots);
 
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int crank = csize > 1 ? (int)cg::this_cluster().block_rank() : 0;
@@ -261,6 +281,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   const int64_t base = seg0 + (int64_t)t * M;
   auto st = [&](int q, int j) -> double & { return state[(q * M + j) * T + t]; };
   if (t == 0) misc[0] = 0;
+  if (csize > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
   BX_TR(0);
   // ---------------- phase 1: downward elimination --------------------------
@@ -447,7 +468,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
       MergeInfo<K> mi;
       TwoPort<K> m;
       ok &= merge<K>(port, other, m, mi);
-      info[warp * 31 + (32 - (32 >> l)) + (lane >> (l + 1))] = mi;
+      store_info<K, T>(info, warp * 31 + (32 - (32 >> l)) + (lane >> (l + 1)), mi);
       port = m;
     }
   }
@@ -467,7 +488,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
         MergeInfo<K> mi;
         TwoPort<K> m;
         ok &= merge<K>(wp, other, m, mi);
-        info[off + (lane >> (l + 1))] = mi;
+        store_info<K, T>(info, off + (lane >> (l + 1)), mi);
         wp = m;
       }
       off += NW >> (l + 1);
@@ -482,22 +503,26 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   for (int k = 0; k < K; ++k) Lseg.v[k] = Rseg.v[k] = 0.0;
   if (csize > 1) {
     cg::cluster_group cl = cg::this_cluster();
-    cl.sync();  // every CTA's wport[0] is final and visible
+    // every CTA pushes its segment root into slot [crank] of every CTA of the
+    // cluster (DSMEM stores), then one cluster barrier; afterwards all reads
+    // are local, so no second barrier is needed before exit
+    __syncthreads();  // wport[0] (written by warp 0) visible to the pushing lanes
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // peers started (arrive at entry)
+    if (t < csize) *cl.map_shared_rank(&croots[crank], t) = wport[0];
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (t == 0) {
-      // every CTA redundantly merges the cluster's segments left to right and
-      // walks back to its own segment's L and R (csize <= 8)
-      TwoPort<K> acc = *cl.map_shared_rank(&wport[0], 0);
+      TwoPort<K> acc = croots[0];
       MergeInfo<K> chain[8];
       for (int r = 1; r < csize; ++r) {
-        const TwoPort<K> nxt = *cl.map_shared_rank(&wport[0], r);
         TwoPort<K> m;
-        ok &= merge<K>(acc, nxt, m, chain[r]);
+        ok &= merge<K>(acc, croots[r], m, chain[r]);
         acc = m;
       }
       Vec<K> L, R;
 #pragma unroll
       for (int k = 0; k < K; ++k) L.v[k] = R.v[k] = 0.0;
       bool found = false;
+      // node r merges [0..r-1] (left) with segment r (right)
       for (int r = csize - 1; r >= 1 && !found; --r) {
         const Vec<K> uu = apply<K>(chain[r].u, L, R);  // E of [0..r-1] = L of segment r
         const Vec<K> vv = apply<K>(chain[r].v, L, R);  // F of segment r = R of [0..r-1]
@@ -506,7 +531,6 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
       }
       if (!found) { Lseg = L; Rseg = R; }
     }
-    cl.sync();  // remote reads done before anyone proceeds / exits
   }
 
   BX_TR(5);
@@ -526,7 +550,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
         const bool act = lane < NW && (lane & (2 * step - 1)) == 0;
         Vec<K> uu = L, vv = R;
         if (act) {
-          const MergeInfo<K> mi = info[offs[l] + (lane >> (l + 1))];
+          const MergeInfo<K> mi = load_info<K, T>(info, offs[l] + (lane >> (l + 1)));
           uu = apply<K>(mi.u, L, R);
           vv = apply<K>(mi.v, L, R);
         }
@@ -550,7 +574,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     const bool act = (lane & (2 * step - 1)) == 0;
     Vec<K> uu = L, vv = R;
     if (act) {
-      const MergeInfo<K> mi = info[warp * 31 + (32 - (32 >> l)) + (lane >> (l + 1))];
+      const MergeInfo<K> mi = load_info<K, T>(info, warp * 31 + (32 - (32 >> l)) + (lane >> (l + 1)));
       uu = apply<K>(mi.u, L, R);
       vv = apply<K>(mi.v, L, R);
     }
@@ -672,7 +696,8 @@ static int dispatch2(const double *c2, const double *c1, const double *e, const 
   }
   if (n <= 256) return launch<K, 8, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
   if (n <= 512) return launch<K, 8, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
-  return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+  if (n <= 1024) return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+  return launch<K, 16, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
 }
 
 static bool aligned32(const void *p) { return p == nullptr || ((uintptr_t)p & 31u) == 0; }
@@ -714,6 +739,8 @@ int penta_part(bool, const double *c, const double *d, const double *e, const do
 
 size_t other_workspace_bytes(int solver, int64_t batch, int64_t n) {
   if (solver == BX_SOLVER_SIP) return sip_workspace_bytes(batch, n);
+  if (solver == BX_SOLVER_STDM) return exact_workspace_bytes(1, batch, n);
+  if (solver == BX_SOLVER_SPDM) return exact_workspace_bytes(2, batch, n);
   return 0;
 }
 

@@ -49,6 +49,13 @@ int sip_wave(const double *a2, const double *a1, const double *e, const double *
              double *hist, double *ws, int64_t batch, int64_t n, int64_t m, double alpha,
              int64_t max_iter, int use_x0, int64_t ld, int layout, cudaStream_t stream);
 
+// bx_exact.cu (kind 1 = STDM, 2 = SPDM)
+size_t exact_workspace_bytes(int kind, int64_t batch, int64_t n);
+int exact_solve(int kind, const double *c, const double *d, const double *e, const double *f,
+                const double *g, const double *b, double *x, int32_t *st, int32_t *ix,
+                int32_t *subs, double *ws, int64_t batch, int64_t n, int64_t ld, int layout,
+                cudaStream_t stream);
+
 // workspace of the non-direct solvers (bx_api.cu dispatch)
 size_t other_workspace_bytes(int solver, int64_t batch, int64_t n);
 

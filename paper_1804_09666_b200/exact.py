@@ -1,0 +1,93 @@
+"""Symbolic solvers SPDM / STDM -- the reference's ``bandix.exact`` entry
+points (exact.py:278-307) over the CUDA C ABI.
+
+Zero pivots are replaced by the indeterminate t and the solution is
+evaluated in the limit t -> 0, as in the reference; the rational functions of
+t are carried as truncated Laurent series with binary64 coefficients
+(DESIGN.md "symbolic solvers").  Conventions that differ from the reference,
+by design:
+
+* inputs are binary64 (a float is an exact rational; the reference demands
+  Fraction input and raises InvalidInput for floats, exact.py:232-236) and
+  x is returned in binary64 -- the correctly-rounded exact answer up to the
+  conditioning of the system, not a tuple of Fractions;
+* batched calls report SingularMatrix / window overflow per system in
+  ``status`` instead of raising.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Any
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import PentaMatrix, TriMatrix, _as_batch, ptr, stream_handle, vector_from_layout, \
+    vector_to_layout, workspace
+from .errors import InvalidInput, STATUS_OK, exception_for
+
+
+@dataclass
+class ExactSolveResult:
+    """Solution plus the number of zero pivots replaced by t (exact.py:213-218)."""
+
+    x: Any
+    pivot_substitutions: Any
+    status: Any = None
+    index: Any = None
+
+
+def _rhs(a, b):
+    bb, _ = _as_batch(b, "rhs")
+    if bb.shape[1] != a.n:
+        raise InvalidInput(f"rhs length {bb.shape[1]} does not match n={a.n}")
+    if bb.shape[0] != a.batch:
+        raise InvalidInput(f"rhs batch {bb.shape[0]} != {a.batch}")
+    return vector_to_layout(bb, a.n, a.layout, a.device)
+
+
+def _solve(kind, a, b):
+    b_store = _rhs(a, b)
+    x = a.new_vector()
+    dev = a.device
+    status = torch.empty(a.batch, dtype=torch.int32, device=dev)
+    index = torch.empty(a.batch, dtype=torch.int32, device=dev)
+    subs = torch.empty(a.batch, dtype=torch.int32, device=dev)
+    solver = "stdm" if kind == 1 else "spdm"
+    nbytes = _lib.lib().bx_workspace_bytes(_lib.SOLVER[solver], a.batch, a.n, a.layout, 0)
+    ws = workspace(nbytes, dev)
+    if kind == 1:
+        d, e, f = a.rowaligned()
+        _lib.call("bx_stdm_f64", ptr(d), ptr(e), ptr(f), ptr(b_store), ptr(x), ptr(status),
+                  ptr(index), ptr(subs), a.batch, a.n, a.ld, a.layout, ptr(ws), ws.numel(),
+                  stream_handle())
+    else:
+        c, d, e, f, g = a.rowaligned()
+        _lib.call("bx_spdm_f64", ptr(c), ptr(d), ptr(e), ptr(f), ptr(g), ptr(b_store), ptr(x),
+                  ptr(status), ptr(index), ptr(subs), a.batch, a.n, a.ld, a.layout, ptr(ws),
+                  ws.numel(), stream_handle())
+    xv = vector_from_layout(x, a.layout)
+    if a.single:
+        st = int(status[0])
+        if st != STATUS_OK:
+            raise exception_for(st, int(index[0]))
+        x1 = xv[0].cpu().numpy()
+        x1.setflags(write=False)
+        return ExactSolveResult(x1, int(subs[0]), status.cpu().numpy(), index.cpu().numpy())
+    return ExactSolveResult(xv, subs, status, index)
+
+
+def exact_solve_stdm(t: TriMatrix, b) -> ExactSolveResult:
+    """Symbolic tridiagonal solve (exact.py:296-307)."""
+    if not isinstance(t, TriMatrix):
+        raise TypeError("expected a TriMatrix")
+    return _solve(1, t, b)
+
+
+def exact_solve_spdm(a: PentaMatrix, b) -> ExactSolveResult:
+    """Symbolic pentadiagonal solve (exact.py:278-293)."""
+    if not isinstance(a, PentaMatrix):
+        raise TypeError("expected a PentaMatrix")
+    return _solve(2, a, b)
