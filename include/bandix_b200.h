@@ -178,6 +178,36 @@ int bx_sip_f64(const double *subm, const double *sub1, const double *main, const
                int32_t layout, int32_t algo, void *workspace, size_t workspace_bytes,
                void *stream);
 
+/* ---- Hotelling-Bodewig ----------------------------------------------------- */
+/* Dense Newton-Schulz inversion X <- X (2I - M X) from X0 = diag(1/m_ii) of the
+ * ILU(0)/Stone factors L (unit lower) and U (upper) of every system, stopping
+ * when ||I - M X||_inf < tol[s] (hb_invert_dense, inverse.py:94-119, on
+ * dense_lower_factor / dense_upper_factor, 72-87).  X X P runs on the FP64
+ * tensor cores (mma.sync ... f64, DMMA) over the triangle only.  x_lower /
+ * x_upper (may be NULL): [batch][n][n] row-major.  inv_iterations /
+ * inv_residual: [2*batch] (L of system s at s, U at batch+s).  status[s]: OK,
+ * ZERO_PIVOT (ILU), ZERO_DIAG(index) or MAX_ITER (index -2: the inversion).
+ * Host-driven iteration: synchronises the stream. */
+size_t bx_hb_workspace_bytes(int64_t batch, int64_t n);
+int bx_hb_invert_f64(const double *subm, const double *sub1, const double *main,
+                     const double *sup1, const double *supm, const double *tol, double *x_lower,
+                     double *x_upper, int64_t *inv_iterations, double *inv_residual,
+                     int32_t *status, int32_t *index, int64_t batch, int64_t n, int64_t m,
+                     double alpha, int64_t max_iter, int64_t ld, int32_t layout, void *workspace,
+                     size_t workspace_bytes, void *stream);
+
+/* SIP with the substitutions replaced by the HB inverses (sip_hb_solve,
+ * mode="dense", inverse.py:205-302): same contract as bx_sip_f64 plus the
+ * inversion counters.  The inversion tolerance is tol[s], as in the reference
+ * (inverse.py:235-236); max_inv_iter = 200 there.  Synchronises the stream. */
+int bx_sip_hb_f64(const double *subm, const double *sub1, const double *main, const double *sup1,
+                  const double *supm, const double *rhs, const double *tol, double *x,
+                  double *best_x, int64_t *iterations, double *residual, double *best_residual,
+                  int32_t *status, int32_t *index, double *history, int64_t *inv_iterations,
+                  double *inv_residual, int64_t batch, int64_t n, int64_t m, double alpha,
+                  int64_t max_iter, int64_t max_inv_iter, int32_t use_x0, int64_t ld,
+                  int32_t layout, void *workspace, size_t workspace_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

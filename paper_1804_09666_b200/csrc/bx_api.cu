@@ -280,4 +280,54 @@ int bx_sip_f64(const double *subm, const double *sub1, const double *main, const
   return bxh::check_launch("bx_sip_f64");
 }
 
+size_t bx_hb_workspace_bytes(int64_t batch, int64_t n) {
+  return bx::hb_total_workspace_bytes(batch, n);
+}
+
+int bx_hb_invert_f64(const double *subm, const double *sub1, const double *main,
+                     const double *sup1, const double *supm, const double *tol, double *x_lower,
+                     double *x_upper, int64_t *inv_iterations, double *inv_residual,
+                     int32_t *status, int32_t *index, int64_t batch, int64_t n, int64_t m,
+                     double alpha, int64_t max_iter, int64_t ld, int32_t layout, void *workspace,
+                     size_t workspace_bytes, void *stream) {
+  int rc = check_sip_args("bx_hb_invert_f64", batch, n, m, alpha, ld, layout);
+  if (rc) return rc;
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(subm && sub1 && main && sup1 && supm && tol, "bx_hb_invert_f64: null pointer");
+  BX_REQUIRE(max_iter >= 0, "bx_hb_invert_f64: max_iter must be >= 0");
+  const size_t need = bx::hb_total_workspace_bytes(batch, n);
+  if (workspace_bytes < need || !workspace) {
+    set_error("bx_hb_invert_f64: workspace %zu bytes < required %zu", workspace_bytes, need);
+    return BX_ERR_WORKSPACE;
+  }
+  return bx::sip_hb(subm, sub1, main, sup1, supm, nullptr, tol, nullptr, nullptr, nullptr, nullptr,
+                    nullptr, status, index, nullptr, inv_iterations, inv_residual, batch, n, m,
+                    alpha, 0, max_iter, 0, ld, layout, workspace, (cudaStream_t)stream, true,
+                    x_lower, x_upper);
+}
+
+int bx_sip_hb_f64(const double *subm, const double *sub1, const double *main, const double *sup1,
+                  const double *supm, const double *rhs, const double *tol, double *x,
+                  double *best_x, int64_t *iterations, double *residual, double *best_residual,
+                  int32_t *status, int32_t *index, double *history, int64_t *inv_iterations,
+                  double *inv_residual, int64_t batch, int64_t n, int64_t m, double alpha,
+                  int64_t max_iter, int64_t max_inv_iter, int32_t use_x0, int64_t ld,
+                  int32_t layout, void *workspace, size_t workspace_bytes, void *stream) {
+  int rc = check_sip_args("bx_sip_hb_f64", batch, n, m, alpha, ld, layout);
+  if (rc) return rc;
+  BX_REQUIRE(max_iter >= 1, "bx_sip_hb_f64: max_iter must be at least 1");
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(subm && sub1 && main && sup1 && supm && rhs && tol && x,
+             "bx_sip_hb_f64: null array pointer");
+  const size_t need = bx::hb_total_workspace_bytes(batch, n);
+  if (workspace_bytes < need || !workspace) {
+    set_error("bx_sip_hb_f64: workspace %zu bytes < required %zu", workspace_bytes, need);
+    return BX_ERR_WORKSPACE;
+  }
+  return bx::sip_hb(subm, sub1, main, sup1, supm, rhs, tol, x, best_x, iterations, residual,
+                    best_residual, status, index, history, inv_iterations, inv_residual, batch, n,
+                    m, alpha, max_iter, max_inv_iter, use_x0, ld, layout, workspace,
+                    (cudaStream_t)stream, false, nullptr, nullptr);
+}
+
 }  // extern "C"

@@ -1,0 +1,373 @@
+// Host drivers of the Hotelling-Bodewig inversion and of SIP-HB
+// (inverse.py:94-119, 205-302).  Both iterate on the host with one small
+// device->host read per iteration (the per-factor / per-system residuals),
+// exactly mirroring the reference's loop control; all arithmetic is on the
+// GPU (bx_hb.cu, bx_sip.cu).  These entry points synchronise the stream.
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <vector>
+
+#include "bx_common.cuh"
+#include "bx_kernels.h"
+
+namespace bx {
+namespace hbh {
+
+// SIP factor planes (bx_sip.cu layout): MU, L1, L2, PHI, PSI, KM, K1N, K0, K1P, KP, KQN, KQP, ...
+enum { MU = 0, L1, L2, PHI, PSI, KM, K1N, K0, K1P, KP, KQN, KQP };
+
+// A (caller layout) and b -> interleaved planes [n][batch]
+template <class Lay>
+__global__ void to_planes_kernel(const double *a2, const double *a1, const double *e,
+                                 const double *c1, const double *c2, const double *b,
+                                 const double *x0, double *out, int64_t batch, int64_t n, Lay lay,
+                                 int use_x0) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= batch * n) return;
+  const int64_t i = idx / batch, s = idx % batch;
+  const int64_t pl = batch * n;
+  out[0 * pl + idx] = a2[lay(i, s)];
+  out[1 * pl + idx] = a1[lay(i, s)];
+  out[2 * pl + idx] = e[lay(i, s)];
+  out[3 * pl + idx] = c1[lay(i, s)];
+  out[4 * pl + idx] = c2[lay(i, s)];
+  out[5 * pl + idx] = b[lay(i, s)];
+  out[6 * pl + idx] = use_x0 ? x0[lay(i, s)] : 0.0;
+}
+
+template <class Lay>
+__global__ void from_plane_kernel(const double *in, double *out, int64_t batch, int64_t n, Lay lay) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= batch * n) return;
+  const int64_t i = idx / batch, s = idx % batch;
+  out[lay(i, s)] = in[idx];
+}
+
+// acc from 0: main, -1, +1, -m, +m [, -(m-1), +(m-1)] (iterative.py:213-221)
+__device__ __forceinline__ double sweep_at(const double *d0, const double *dn1, const double *dp1,
+                                           const double *dnm, const double *dpm, const double *dnq,
+                                           const double *dpq, const double *x, int64_t i,
+                                           int64_t s, int64_t batch, int64_t n, int64_t m) {
+  auto X = [&](int64_t r) { return x[r * batch + s]; };
+  auto D = [&](const double *d) { return d[i * batch + s]; };
+  double acc = __dadd_rn(0.0, __dmul_rn(D(d0), X(i)));
+  if (i >= 1) acc = __dadd_rn(acc, __dmul_rn(D(dn1), X(i - 1)));
+  if (i <= n - 2) acc = __dadd_rn(acc, __dmul_rn(D(dp1), X(i + 1)));
+  if (i >= m) acc = __dadd_rn(acc, __dmul_rn(D(dnm), X(i - m)));
+  if (i + m <= n - 1) acc = __dadd_rn(acc, __dmul_rn(D(dpm), X(i + m)));
+  if (dnq) {
+    const int64_t q = m - 1;
+    if (i >= q) acc = __dadd_rn(acc, __dmul_rn(D(dnq), X(i - q)));
+    if (i + q <= n - 1) acc = __dadd_rn(acc, __dmul_rn(D(dpq), X(i + q)));
+  }
+  return acc;
+}
+
+// v = K x + b   (active systems only)
+__global__ void kx_plus_b_kernel(const double *fac, const double *b, const double *x, double *v,
+                                 const int *act, int nact, int64_t batch, int64_t n, int64_t m) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)nact * n) return;
+  const int64_t s = act[idx % nact], i = idx / nact;
+  const int64_t pl = batch * n;
+  const double *P = fac;
+  const double kx = sweep_at(P + K0 * pl, P + K1N * pl, P + K1P * pl, P + KM * pl, P + KP * pl,
+                             m != 2 ? P + KQN * pl : nullptr, m != 2 ? P + KQP * pl : nullptr, x,
+                             i, s, batch, n, m);
+  v[i * batch + s] = __dadd_rn(kx, b[i * batch + s]);
+}
+
+// r_s = max_i |b - A x| (NaN propagates: its bit pattern orders above +inf)
+__global__ void residual_bits_kernel(const double *A, const double *x, const int *act, int nact,
+                                     unsigned long long *rbits, int64_t batch, int64_t n,
+                                     int64_t m) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)nact * n) return;
+  const int64_t s = act[idx % nact], i = idx / nact;
+  const int64_t pl = batch * n;
+  const double ax = sweep_at(A + 2 * pl, A + 1 * pl, A + 3 * pl, A + 0 * pl, A + 4 * pl, nullptr,
+                             nullptr, x, i, s, batch, n, m);
+  double r = fabs(__dsub_rn(A[5 * pl + i * batch + s], ax));
+  if (r != r) r = __longlong_as_double(0x7ff8000000000000LL);
+  atomicMax(rbits + s, (unsigned long long)__double_as_longlong(r));
+}
+
+__global__ void copy_systems_kernel(const double *src, double *dst, const int *act, int nact,
+                                    int64_t batch, int64_t n) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)nact * n) return;
+  const int64_t s = act[idx % nact], i = idx / nact;
+  dst[i * batch + s] = src[i * batch + s];
+}
+
+inline unsigned blocks(int64_t work, int threads = 256) { return (unsigned)((work + threads - 1) / threads); }
+
+inline double bits2d(unsigned long long b) {
+  double d;
+  memcpy(&d, &b, sizeof d);
+  return d;
+}
+
+}  // namespace hbh
+
+// workspace: SIP planes | A planes (7) | vectors v, y, x, xn (4) | ints | dense X, Xn, P
+size_t hb_total_workspace_bytes(int64_t batch, int64_t n) {
+  return sip_workspace_bytes(batch, n) + sizeof(double) * 11 * (size_t)batch * (size_t)n +
+         sizeof(int) * 8 * (size_t)(2 * batch) + sizeof(unsigned long long) * (size_t)(2 * batch) +
+         hb_dense_bytes(batch, n) + 1024;
+}
+
+struct HbWs {
+  double *fac, *A, *v, *y, *x, *xb, *Xa, *Xb, *P;
+  int *act, *parity, *zd;
+  unsigned long long *rbits;
+};
+
+static HbWs carve(void *ws, int64_t batch, int64_t n) {
+  char *p = (char *)ws;
+  HbWs w;
+  const size_t vec = sizeof(double) * (size_t)batch * (size_t)n;
+  w.fac = (double *)p; p += sip_workspace_bytes(batch, n);
+  w.A = (double *)p; p += 7 * vec;
+  w.v = (double *)p; p += vec;
+  w.y = (double *)p; p += vec;
+  w.x = (double *)p; p += vec;
+  w.xb = (double *)p; p += vec;
+  const int64_t np_ = hb_padded(n);
+  const size_t dense = sizeof(double) * (size_t)(2 * batch) * (size_t)np_ * (size_t)np_;
+  p = (char *)(((uintptr_t)p + 255) & ~(uintptr_t)255);
+  w.Xa = (double *)p; p += dense;
+  w.Xb = (double *)p; p += dense;
+  w.P = (double *)p; p += dense;
+  w.act = (int *)p; p += sizeof(int) * 2 * batch;
+  w.parity = (int *)p; p += sizeof(int) * 2 * batch;
+  w.zd = (int *)p; p += sizeof(int) * 2 * batch;
+  p = (char *)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+  w.rbits = (unsigned long long *)p;
+  return w;
+}
+
+// Invert the 2*batch factors; inv_iters/inv_res/inv_status: [2*batch] host arrays.
+static int hb_invert_all(HbWs &w, const double *tol_host, int64_t batch, int64_t n, int64_t m,
+                         int64_t max_iter, int64_t *inv_iters, double *inv_res, int *inv_status,
+                         int *zero_row, cudaStream_t st) {
+  const int64_t pl = batch * n;
+  const int F = (int)(2 * batch);
+  std::vector<int> parity(F, 0), act, zd(F, 0x7fffffff);
+  cudaMemcpyAsync(w.zd, zd.data(), sizeof(int) * F, cudaMemcpyHostToDevice, st);
+  hb_init(w.Xa, w.fac + hbh::MU * pl, n, batch, w.zd, st);
+  cudaMemcpyAsync(zd.data(), w.zd, sizeof(int) * F, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  for (int f = 0; f < F; ++f) {
+    inv_iters[f] = 0;
+    inv_res[f] = NAN;
+    zero_row[f] = zd[f] == 0x7fffffff ? -1 : zd[f];
+    inv_status[f] = zd[f] == 0x7fffffff ? -1 : BX_STATUS_ZERO_DIAG;  // -1: running
+    if (inv_status[f] < 0) act.push_back(f);
+  }
+  cudaMemcpyAsync(w.parity, parity.data(), sizeof(int) * F, cudaMemcpyHostToDevice, st);
+  std::vector<unsigned long long> bits(F);
+  for (int64_t it = 0; it <= max_iter && !act.empty(); ++it) {
+    const int na = (int)act.size();
+    cudaMemcpyAsync(w.act, act.data(), sizeof(int) * na, cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(w.rbits, 0, sizeof(unsigned long long) * F, st);
+    hb_residual(w.Xa, w.Xb, w.parity, w.P, w.fac + hbh::L1 * pl, w.fac + hbh::L2 * pl,
+                w.fac + hbh::MU * pl, w.fac + hbh::PHI * pl, w.fac + hbh::PSI * pl, w.act, na,
+                w.rbits, n, m, batch, st);
+    cudaMemcpyAsync(bits.data(), w.rbits, sizeof(unsigned long long) * F, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    std::vector<int> next;
+    for (int f : act) {
+      const double r = hbh::bits2d(bits[f]);
+      inv_res[f] = r;
+      inv_iters[f] = it;
+      const double tl = tol_host[f % batch];
+      if (r < tl) {
+        inv_status[f] = BX_STATUS_OK;
+      } else if (it == max_iter) {
+        inv_status[f] = BX_STATUS_MAX_ITER;
+      } else {
+        next.push_back(f);
+      }
+    }
+    if (next.empty()) break;
+    const int nn = (int)next.size();
+    cudaMemcpyAsync(w.act, next.data(), sizeof(int) * nn, cudaMemcpyHostToDevice, st);
+    hb_gemm(w.Xa, w.Xb, w.parity, w.P, w.act, nn, n, batch, st);
+    for (int f : next) parity[f] ^= 1;
+    cudaMemcpyAsync(w.parity, parity.data(), sizeof(int) * F, cudaMemcpyHostToDevice, st);
+    act.swap(next);
+  }
+  cudaStreamSynchronize(st);
+  return bxh::check_launch("hotelling-bodewig");
+}
+
+template <class Lay>
+static int sip_hb_impl(const double *a2, const double *a1, const double *e, const double *c1,
+                       const double *c2, const double *b, const double *tol, double *x,
+                       double *best_x, int64_t *iterations, double *residual,
+                       double *best_residual, int32_t *status, int32_t *index, double *history,
+                       int64_t *inv_iterations, double *inv_residual, int64_t batch, int64_t n,
+                       int64_t m, double alpha, int64_t max_iter, int64_t max_inv_iter,
+                       int use_x0, Lay lay, int64_t ld, int layout, void *workspace,
+                       cudaStream_t st, bool invert_only, double *xl_out, double *xu_out) {
+  HbWs w = carve(workspace, batch, n);
+  const int64_t pl = batch * n;
+  const int F = (int)(2 * batch);
+  // ILU(0)/Stone factors and defect (bx_sip.cu, factor-only pass)
+  std::vector<int32_t> fst(batch), fix(batch);
+  int32_t *dst = (int32_t *)w.act, *dix = (int32_t *)w.zd;  // reuse int scratch
+  sip_seq(a2, a1, e, c1, c2, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, dst,
+          dix, nullptr, w.fac, batch, n, m, alpha, 0, 0, ld, layout, 1, st);
+  cudaMemcpyAsync(fst.data(), dst, sizeof(int32_t) * batch, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(fix.data(), dix, sizeof(int32_t) * batch, cudaMemcpyDeviceToHost, st);
+  std::vector<double> tolh(batch);
+  cudaMemcpyAsync(tolh.data(), tol, sizeof(double) * batch, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  // inversion (systems whose ILU failed still invert garbage; they are reported as ZERO_PIVOT)
+  std::vector<int64_t> ii(F);
+  std::vector<double> ir(F);
+  std::vector<int> ist(F), zr(F);
+  int rc = hb_invert_all(w, tolh.data(), batch, n, m, max_inv_iter, ii.data(), ir.data(),
+                         ist.data(), zr.data(), st);
+  if (rc) return rc;
+  if (inv_iterations) cudaMemcpyAsync(inv_iterations, ii.data(), sizeof(int64_t) * F, cudaMemcpyHostToDevice, st);
+  if (inv_residual) cudaMemcpyAsync(inv_residual, ir.data(), sizeof(double) * F, cudaMemcpyHostToDevice, st);
+  std::vector<int32_t> sst(batch, BX_STATUS_OK), six(batch, -1);
+  std::vector<int> run;
+  for (int64_t s = 0; s < batch; ++s) {
+    if (fst[s] != BX_STATUS_OK) { sst[s] = fst[s]; six[s] = fix[s]; continue; }
+    const int fl = (int)s, fu = (int)(batch + s);
+    if (ist[fl] == BX_STATUS_ZERO_DIAG || ist[fu] == BX_STATUS_ZERO_DIAG) {
+      sst[s] = BX_STATUS_ZERO_DIAG;
+      six[s] = ist[fl] == BX_STATUS_ZERO_DIAG ? zr[fl] : zr[fu];
+      continue;
+    }
+    if (ist[fl] == BX_STATUS_MAX_ITER || ist[fu] == BX_STATUS_MAX_ITER) {
+      sst[s] = BX_STATUS_MAX_ITER;  // hb_invert_dense raised MaxIterationsExceeded
+      six[s] = -2;                  // marks "inversion", not the outer SIP
+      continue;
+    }
+    run.push_back((int)s);
+  }
+  if (xl_out || xu_out) {
+    // export the dense inverses (row-major [batch][n][n], real part only)
+    std::vector<int> par(F);
+    // parity lives on device; recompute on host from iteration counts
+    for (int f = 0; f < F; ++f) par[f] = (int)(ii[f] & 1);
+    const int64_t np_ = hb_padded(n);
+    for (int64_t s = 0; s < batch; ++s)
+      for (int side = 0; side < 2; ++side) {
+        double *out = side ? xu_out : xl_out;
+        if (!out) continue;
+        const int f = side ? (int)(batch + s) : (int)s;
+        const double *src = (par[f] ? w.Xb : w.Xa) + (size_t)f * np_ * np_;
+        cudaMemcpy2DAsync(out + (size_t)s * n * n, sizeof(double) * n, src, sizeof(double) * np_,
+                          sizeof(double) * n, n, cudaMemcpyDeviceToDevice, st);
+      }
+  }
+  if (invert_only) {
+    if (status) cudaMemcpyAsync(status, sst.data(), sizeof(int32_t) * batch, cudaMemcpyHostToDevice, st);
+    if (index) cudaMemcpyAsync(index, six.data(), sizeof(int32_t) * batch, cudaMemcpyHostToDevice, st);
+    cudaStreamSynchronize(st);
+    return bxh::check_launch("bx_hb_invert_f64");
+  }
+  // the parity array on the device is final; SIP-HB iteration (inverse.py:274-298)
+  hbh::to_planes_kernel<<<hbh::blocks(pl), 256, 0, st>>>(a2, a1, e, c1, c2, b, x, w.A, batch, n,
+                                                          lay, use_x0);
+  double *xcur = w.A + 6 * pl;  // x lives in the 7th A plane
+  std::vector<unsigned long long> bits(batch);
+  std::vector<double> r(batch, NAN), r0(batch, NAN), best(batch, NAN);
+  std::vector<int64_t> k(batch, 0);
+  std::vector<std::vector<double>> hist(history ? batch : 0);
+  auto eval = [&](const std::vector<int> &act) {
+    const int na = (int)act.size();
+    cudaMemcpyAsync(w.act, act.data(), sizeof(int) * na, cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(w.rbits, 0, sizeof(unsigned long long) * batch, st);
+    hbh::residual_bits_kernel<<<hbh::blocks((int64_t)na * n), 256, 0, st>>>(w.A, xcur, w.act, na,
+                                                                              w.rbits, batch, n, m);
+    cudaMemcpyAsync(bits.data(), w.rbits, sizeof(unsigned long long) * batch,
+                    cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+  };
+  if (!run.empty()) {
+    eval(run);
+    for (int s : run) r0[s] = best[s] = r[s] = hbh::bits2d(bits[s]);
+    // best iterate starts as x0
+    const int na = (int)run.size();
+    hbh::copy_systems_kernel<<<hbh::blocks((int64_t)na * n), 256, 0, st>>>(xcur, w.xb, w.act, na,
+                                                                             batch, n);
+  }
+  std::vector<int> act;
+  for (int s : run)
+    if (r[s] >= tolh[s]) act.push_back(s);
+  while (!act.empty()) {
+    std::vector<int> go;
+    for (int s : act) {
+      if (k[s] >= max_iter) sst[s] = BX_STATUS_MAX_ITER;
+      else go.push_back(s);
+    }
+    if (go.empty()) break;
+    const int na = (int)go.size();
+    cudaMemcpyAsync(w.act, go.data(), sizeof(int) * na, cudaMemcpyHostToDevice, st);
+    hbh::kx_plus_b_kernel<<<hbh::blocks((int64_t)na * n), 256, 0, st>>>(w.fac, w.A + 5 * pl, xcur,
+                                                                          w.v, w.act, na, batch, n, m);
+    hb_apply(w.Xa, w.Xb, w.parity, w.v, w.y, w.act, na, n, batch, 0, st);
+    hb_apply(w.Xa, w.Xb, w.parity, w.y, xcur, w.act, na, n, batch, 1, st);
+    eval(go);
+    std::vector<int> improved, next;
+    for (int s : go) {
+      r[s] = hbh::bits2d(bits[s]);
+      k[s] += 1;
+      if (history) hist[s].push_back(r[s]);
+      if (r[s] < best[s]) { best[s] = r[s]; improved.push_back(s); }
+      if (r0[s] > 0 && r[s] > 1e6 * r0[s]) { sst[s] = BX_STATUS_DIVERGED; continue; }
+      if (r[s] >= tolh[s]) next.push_back(s);
+    }
+    if (!improved.empty()) {
+      const int ni = (int)improved.size();
+      cudaMemcpyAsync(w.act, improved.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st);
+      hbh::copy_systems_kernel<<<hbh::blocks((int64_t)ni * n), 256, 0, st>>>(xcur, w.xb, w.act, ni,
+                                                                               batch, n);
+    }
+    act.swap(next);
+  }
+  // outputs
+  hbh::from_plane_kernel<<<hbh::blocks(pl), 256, 0, st>>>(xcur, x, batch, n, lay);
+  if (best_x) hbh::from_plane_kernel<<<hbh::blocks(pl), 256, 0, st>>>(w.xb, best_x, batch, n, lay);
+  if (iterations) cudaMemcpyAsync(iterations, k.data(), sizeof(int64_t) * batch, cudaMemcpyHostToDevice, st);
+  if (residual) cudaMemcpyAsync(residual, r.data(), sizeof(double) * batch, cudaMemcpyHostToDevice, st);
+  if (best_residual) cudaMemcpyAsync(best_residual, best.data(), sizeof(double) * batch, cudaMemcpyHostToDevice, st);
+  if (status) cudaMemcpyAsync(status, sst.data(), sizeof(int32_t) * batch, cudaMemcpyHostToDevice, st);
+  if (index) cudaMemcpyAsync(index, six.data(), sizeof(int32_t) * batch, cudaMemcpyHostToDevice, st);
+  if (history) {
+    std::vector<double> h((size_t)batch * max_iter, NAN);
+    for (int64_t s = 0; s < batch; ++s)
+      for (size_t j = 0; j < hist[s].size(); ++j) h[(size_t)s * max_iter + j] = hist[s][j];
+    cudaMemcpyAsync(history, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, st);
+  }
+  cudaStreamSynchronize(st);
+  return bxh::check_launch("bx_sip_hb_f64");
+}
+
+int sip_hb(const double *a2, const double *a1, const double *e, const double *c1,
+           const double *c2, const double *b, const double *tol, double *x, double *best_x,
+           int64_t *iterations, double *residual, double *best_residual, int32_t *status,
+           int32_t *index, double *history, int64_t *inv_iterations, double *inv_residual,
+           int64_t batch, int64_t n, int64_t m, double alpha, int64_t max_iter,
+           int64_t max_inv_iter, int use_x0, int64_t ld, int layout, void *workspace,
+           cudaStream_t st, bool invert_only, double *xl, double *xu) {
+  if (layout == BX_LAYOUT_INTERLEAVED)
+    return sip_hb_impl(a2, a1, e, c1, c2, b, tol, x, best_x, iterations, residual, best_residual,
+                       status, index, history, inv_iterations, inv_residual, batch, n, m, alpha,
+                       max_iter, max_inv_iter, use_x0, Interleaved{ld}, ld, layout, workspace, st,
+                       invert_only, xl, xu);
+  return sip_hb_impl(a2, a1, e, c1, c2, b, tol, x, best_x, iterations, residual, best_residual,
+                     status, index, history, inv_iterations, inv_residual, batch, n, m, alpha,
+                     max_iter, max_inv_iter, use_x0, SystemMajor{ld}, ld, layout, workspace, st,
+                     invert_only, xl, xu);
+}
+
+}  // namespace bx

@@ -56,6 +56,28 @@ int exact_solve(int kind, const double *c, const double *d, const double *e, con
                 int32_t *subs, double *ws, int64_t batch, int64_t n, int64_t ld, int layout,
                 cudaStream_t stream);
 
+// bx_hb.cu / bx_hb_host.cu
+size_t hb_dense_bytes(int64_t batch, int64_t n);
+int64_t hb_padded(int64_t n);
+int hb_gemm(double *Xa, double *Xb, const int *parity, const double *P, const int *active_list,
+            int nactive, int64_t n, int64_t batch, cudaStream_t stream);
+int hb_residual(const double *Xa, const double *Xb, const int *parity, double *P, const double *l1,
+                const double *l2, const double *mu, const double *phi, const double *psi,
+                const int *active_list, int nactive, unsigned long long *rbits, int64_t n,
+                int64_t m, int64_t batch, cudaStream_t stream);
+int hb_init(double *X, const double *mu, int64_t n, int64_t batch, int32_t *zero_diag,
+            cudaStream_t stream);
+int hb_apply(const double *Xa, const double *Xb, const int *parity, const double *v, double *y,
+             const int *act, int nact, int64_t n, int64_t batch, int upper, cudaStream_t stream);
+size_t hb_total_workspace_bytes(int64_t batch, int64_t n);
+int sip_hb(const double *a2, const double *a1, const double *e, const double *c1,
+           const double *c2, const double *b, const double *tol, double *x, double *best_x,
+           int64_t *iterations, double *residual, double *best_residual, int32_t *status,
+           int32_t *index, double *history, int64_t *inv_iterations, double *inv_residual,
+           int64_t batch, int64_t n, int64_t m, double alpha, int64_t max_iter,
+           int64_t max_inv_iter, int use_x0, int64_t ld, int layout, void *workspace,
+           cudaStream_t st, bool invert_only, double *xl, double *xu);
+
 // workspace of the non-direct solvers (bx_api.cu dispatch)
 size_t other_workspace_bytes(int solver, int64_t batch, int64_t n);
 

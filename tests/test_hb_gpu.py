@@ -1,0 +1,73 @@
+"""GPU parity of the Hotelling-Bodewig inversion (DMMA) and SIP-HB against the
+reference's own outputs (golden) and the numpy/BLAS restatement.  The
+reference's HB products go through BLAS, so parity is iteration counts +
+tolerance, not bits."""
+
+import numpy as np
+import pytest
+
+from oracle import inverse as H
+from oracle import iterative as I
+from paper_1804_09666_b200 import (DenseCapExceeded, PentaMatrix, SipConfig, StencilMatrix,
+                                   hb_invert_factors, sip_hb_solve)
+from paper_1804_09666_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+PD = ("sub2", "sub1", "main", "sup1", "sup2", "rhs")
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.mark.parametrize("layout", ["interleaved", "system"])
+def test_sip_hb_golden(cuda, golden, layout):
+    g = golden("inverse")
+    a = [g[f"hb_{k}"] for k in PD]
+    A = PentaMatrix.from_diagonals(*a[:5], layout=layout)
+    rep = sip_hb_solve(A, a[5], SipConfig(tolerance=g["hb_tol"], max_iterations=500))
+    assert (host(rep.status) == 0).all()
+    assert np.array_equal(host(rep.iterations), g["hb_k"])
+    assert np.array_equal(host(rep.inv_iterations)[:, 0], g["hb_linv_iters"])
+    assert np.array_equal(host(rep.inv_iterations)[:, 1], g["hb_uinv_iters"])
+    x = host(rep.x)
+    assert np.abs(x - g["hb_x"]).max() <= 1e-11 * np.abs(g["hb_x"]).max()
+    assert np.all(host(rep.residual_inf) < g["hb_tol"])
+
+
+@pytest.mark.parametrize("m,rows,alpha", [(2, 128, 0.0), (16, 24, 0.5), (32, 64, 0.5)])
+def test_hb_inverses_match_restatement(cuda, m, rows, alpha):
+    n = m * rows
+    p = W.five_point(3, n, m, seed=8)
+    tol = W.sip_tolerance(p[5])
+    A = StencilMatrix.from_diagonals(*p[:5], m=m)
+    xl, xu, its, res, st, _ = hb_invert_factors(A, tol, alpha=alpha)
+    f, _, _ = I.ilu0(*p[:5], m=m, alpha=alpha)
+    lo, up = H.dense_lower(f), H.dense_upper(f)
+    for s in range(3):
+        ref_l = H.hb_invert_dense(lo[s], tol[s])
+        ref_u = H.hb_invert_dense(up[s], tol[s])
+        assert host(its)[s, 0] == ref_l[1] and host(its)[s, 1] == ref_u[1]
+        assert np.abs(host(xl)[s] - ref_l[0]).max() <= 1e-12 * np.abs(ref_l[0]).max()
+        assert np.abs(host(xu)[s] - ref_u[0]).max() <= 1e-12 * np.abs(ref_u[0]).max()
+        assert host(res)[s, 0] < tol[s] and host(res)[s, 1] < tol[s]
+
+
+def test_sip_hb_stencil_matches_sip(cuda):
+    """SIP-HB and SIP reach the same iterate count and solution (probe P9)."""
+    m, n = 32, 2048
+    p = W.five_point(8, n, m, seed=3)
+    tol = W.sip_tolerance(p[5])
+    A = StencilMatrix.from_diagonals(*p[:5], m=m)
+    from paper_1804_09666_b200 import sip_solve
+    r1 = sip_solve(A, p[5], SipConfig(tolerance=tol, max_iterations=500, alpha=0.5))
+    r2 = sip_hb_solve(A, p[5], SipConfig(tolerance=tol, max_iterations=500, alpha=0.5))
+    assert (host(r2.status) == 0).all()
+    assert np.all(np.abs(host(r1.iterations) - host(r2.iterations)) <= 1)
+    assert np.abs(host(r1.x) - host(r2.x)).max() <= 1e-7 * np.abs(host(r1.x)).max()
+
+
+def test_dense_cap(cuda):
+    p = W.five_point(1, 64, 2)
+    with pytest.raises(DenseCapExceeded):
+        sip_hb_solve(PentaMatrix.from_diagonals(*p[:5]), p[5], dense_cap=32)
