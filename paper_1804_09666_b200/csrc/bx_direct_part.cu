@@ -331,6 +331,19 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
       }
     }
   };
+  if (VEC && t < (K == 2 ? 6 : 4)) {
+    // warm L2 with this CTA's whole segment of one array per thread (TMA bulk
+    // prefetch, no registers): the per-group loads below then see L2, not
+    // HBM, latency.  Bytes are still fetched from HBM exactly once.
+    const double *arr[6] = {bp, ep, c1p, f1p, c2p, f2p};
+    const int64_t rows = min((int64_t)(T * M), n - seg0) & ~(int64_t)1;
+    if (rows > 0) {
+      const double *src = arr[t] + lay(seg0, s);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src),
+                   "r"((unsigned)(rows * sizeof(double)))
+                   : "memory");
+    }
+  }
   load_group(0, 0);
 #pragma unroll
   for (int j = 0; j < M; ++j) {
@@ -460,7 +473,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   // merge info for the in-warp levels: node (level l, index k) of warp w at
   // info[w*31 + (32 - (32 >> l)) + k]; cross-warp nodes after NW*31.
   bool ok = true;
-#pragma unroll
+#pragma unroll 1
   for (int l = 0; l < 5; ++l) {
     const int step = 1 << l;
     const TwoPort<K> other = shfl_down_port<K>(port, step);
@@ -568,7 +581,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   Vec<K> L, R;
 #pragma unroll
   for (int k = 0; k < K; ++k) { L.v[k] = wlr[warp * 2 * K + k]; R.v[k] = wlr[warp * 2 * K + K + k]; }
-#pragma unroll
+#pragma unroll 1
   for (int l = 4; l >= 0; --l) {
     const int step = 1 << l;
     const bool act = (lane & (2 * step - 1)) == 0;

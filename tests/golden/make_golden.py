@@ -226,9 +226,9 @@ def golden_exact():
         xs[s] = [float(v) for v in r.x]; subs[s] = r.pivot_substitutions
     out.update(stdm0_sub1=q[0], stdm0_main=q[1], stdm0_sup1=q[2], stdm0_rhs=q[3], stdm0_x=xs,
                stdm0_subs=subs)
-    # exact determinant sign/zero gate on a singular 3x3 (rows 0 and 2 equal)
+    # exact determinant zero gate on a singular 3x3 (rows 0 and 1 equal)
     F = Fraction
-    t = core.TriMatrix.from_diagonals([F(1), F(1)], [F(1), F(1), F(1)], [F(1), F(1)])
+    t = core.TriMatrix.from_diagonals([F(1), F(1)], [F(1), F(1), F(1)], [F(1), F(0)])
     out.update(det_singular=np.float64(float(exact.exact_det_band(t))))
     _save("exact", **out)
 

@@ -55,7 +55,7 @@ def test_single_system_contract(cuda, golden):
     t = TriMatrix.from_diagonals(g["stdm_sub1"][0], g["stdm_main"][0], g["stdm_sup1"][0])
     r = exact_solve_stdm(t, g["stdm_rhs"][0])
     assert isinstance(r.x, np.ndarray) and r.pivot_substitutions == g["stdm_subs"][0]
-    sing = TriMatrix.from_diagonals([1.0, 1.0], [1.0, 1.0, 1.0], [1.0, 1.0])
+    sing = TriMatrix.from_diagonals([1.0, 1.0], [1.0, 1.0, 1.0], [1.0, 0.0])
     assert g["det_singular"] == 0.0
     with pytest.raises(SingularMatrix):
         exact_solve_stdm(sing, [1.0, 2.0, 3.0])

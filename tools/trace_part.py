@@ -49,7 +49,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 buf = np.zeros((4096, 10), dtype=np.int64)
 L.bx_trace_read(buf.ctypes.data, buf.nbytes)
-names = ["down", "up", "port", "warp-asc", "xwarp-asc", "cluster", "descent", "phase3", "status"]
+names = ["down", "up", "port+warp-asc", "xwarp-asc", "cluster", "descent", "phase3", "status"]
 d = np.diff(buf[:, :9], axis=1)
 ok = buf[:, 0] > 0
 print(f"K={k} n={n} B={batch} cfg={os.environ.get('BX_PART_CFG', 'auto')} CTAs traced={ok.sum()}")
