@@ -119,6 +119,13 @@ int bx_residual_inf_f64(int32_t bandwidth, const double *sub2, const double *sub
                         const double *x, const double *rhs, double *res_inf, int64_t batch,
                         int64_t n, int64_t ld, int32_t layout, void *stream);
 
+/* dst[b][c][r] = src[b][r][c] (r < rows, c < cols): converts between the
+ * interleaved and system-major storages (and feeds the ADI y-sweep the
+ * x-sweep output).  Strides in elements; smem-tiled, both sides coalesced. */
+int bx_transpose_f64(const double *src, double *dst, int64_t rows, int64_t cols, int64_t ld_src,
+                     int64_t ld_dst, int64_t nbatch, int64_t batch_stride_src,
+                     int64_t batch_stride_dst, void *stream);
+
 /* ---- symbolic solvers ----------------------------------------------------- */
 /* STDM / SPDM: exact-zero pivots are replaced by the indeterminate t and the
  * solution is the limit t -> 0, as exact_solve_stdm / exact_solve_spdm

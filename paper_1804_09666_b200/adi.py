@@ -1,0 +1,84 @@
+"""One ADI time step of a 2-D parabolic problem (BASELINE.json config 5):
+N tridiagonal systems along x, then N along y whose right-hand sides are the
+x-sweep output (the paper's "N SLAEs d times per time step", PAPER.md:64-67;
+the reference itself has no ADI driver).
+
+Storage: the grid u[y][x] (x fastest).  The x-sweep systems are the rows
+y (system-major for the C ABI); the y-sweep systems are the columns x, so
+the x-sweep output is transposed once on the GPU (bx_transpose_f64) into
+system-major [x][y] and the y-sweep result comes back as u[x][y].
+
+Multi-GPU (strong scaling): rank r owns grid rows [r*ny/G, (r+1)*ny/G) for the
+x-sweep and grid columns [r*nx/G, (r+1)*nx/G) for the y-sweep; the one
+exchange between the sweeps is an all-to-all of the transposed x-sweep output
+(NCCL over NVLink on the GPU path).  The solver, the transpose and the
+process group are injected so the exchange logic is tested with gloo on CPU.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+
+class CudaBackend:
+    """Partitioned NTDM (system-major) + smem-tiled transpose, via the C ABI."""
+
+    def __init__(self, device):
+        self.device = device
+
+    def tri_solve(self, sub1, main, sup1, rhs, out):
+        from .core import ptr, stream_handle
+        B, n = main.shape
+        status = torch.empty(B, dtype=torch.int32, device=self.device)
+        _lib.call("bx_ntdm_f64", ptr(sub1), ptr(main), ptr(sup1), ptr(rhs), ptr(out), ptr(status),
+                  None, B, n, main.stride(0), _lib.LAYOUT_SYSTEM_MAJOR, _lib.ALGO_PARTITIONED,
+                  None, 0, stream_handle())
+        return status
+
+    def transpose(self, src, dst):
+        from .core import ptr, stream_handle
+        r, c = src.shape
+        _lib.call("bx_transpose_f64", ptr(src), ptr(dst), r, c, src.stride(0), dst.stride(0), 1, 0, 0,
+                  stream_handle())
+
+
+class ADIStep:
+    """x-sweep -> (exchange) -> y-sweep for one rank.
+
+    xs: (sub1, main, sup1) row-aligned, shape (ny_local, nx): this rank's rows.
+    ys: (sub1, main, sup1) row-aligned, shape (nx_local, ny): this rank's columns.
+    """
+
+    def __init__(self, xs, ys, group=None, backend=None):
+        self.xs, self.ys = xs, ys
+        self.group = group
+        self.world = torch.distributed.get_world_size(group) if group is not None else 1
+        self.nyl, self.nx = xs[1].shape
+        self.nxl, self.ny = ys[1].shape
+        if self.nyl * self.world != self.ny or self.nxl * self.world != self.nx:
+            raise ValueError("grid must split evenly over the ranks")
+        dev = xs[1].device
+        self.backend = backend or CudaBackend(dev)
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.X = torch.empty((self.nyl, self.nx), **f64)
+        self.XT = torch.empty((self.nx, self.nyl), **f64)
+        self.Y = torch.empty((self.nxl, self.ny), **f64) if self.world > 1 else None
+        self.recv = torch.empty((self.world, self.nxl, self.nyl), **f64) if self.world > 1 else None
+        self.U = torch.empty((self.nxl, self.ny), **f64)
+
+    def __call__(self, rhs):
+        be = self.backend
+        st_x = be.tri_solve(*self.xs, rhs, self.X)            # x-sweep
+        be.transpose(self.X, self.XT)                          # [x][y_local]
+        if self.world == 1:
+            y_in = self.XT
+        else:
+            # block r of XT (columns owned by rank r) goes to rank r
+            torch.distributed.all_to_all_single(self.recv.view(-1), self.XT.view(-1),
+                                                group=self.group)
+            self.Y.view(self.nxl, self.world, self.nyl).copy_(self.recv.transpose(0, 1))
+            y_in = self.Y
+        st_y = be.tri_solve(*self.ys, y_in, self.U)            # y-sweep
+        return self.U, st_x, st_y

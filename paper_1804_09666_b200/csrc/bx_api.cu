@@ -280,6 +280,19 @@ int bx_sip_f64(const double *subm, const double *sub1, const double *main, const
   return bxh::check_launch("bx_sip_f64");
 }
 
+int bx_transpose_f64(const double *src, double *dst, int64_t rows, int64_t cols, int64_t ld_src,
+                     int64_t ld_dst, int64_t nbatch, int64_t batch_stride_src,
+                     int64_t batch_stride_dst, void *stream) {
+  BX_REQUIRE(rows >= 0 && cols >= 0 && nbatch >= 0, "bx_transpose_f64: negative extent");
+  if (rows == 0 || cols == 0 || nbatch == 0) return BX_OK;
+  BX_REQUIRE(src && dst, "bx_transpose_f64: null pointer");
+  BX_REQUIRE(ld_src >= cols && ld_dst >= rows, "bx_transpose_f64: leading dimension too small");
+  BX_REQUIRE(rows / 32 < 65535 && nbatch < 65535, "bx_transpose_f64: extent too large");
+  bx::transpose(src, dst, rows, cols, ld_src, ld_dst, nbatch, batch_stride_src, batch_stride_dst,
+                (cudaStream_t)stream);
+  return bxh::check_launch("bx_transpose_f64");
+}
+
 size_t bx_hb_workspace_bytes(int64_t batch, int64_t n) {
   return bx::hb_total_workspace_bytes(batch, n);
 }

@@ -181,6 +181,12 @@ __global__ void hb_residual_kernel(const double *__restrict__ Xa, const double *
   }
   double rsum = 0.0;
   const int64_t j0 = lower ? 0 : i, j1 = lower ? i + 1 : n;
+  // the GEMM reads whole 64x64 diagonal tiles of P: keep their other triangle zero
+  {
+    const int64_t t0 = i & ~(int64_t)(TM - 1), t1 = t0 + TM;
+    const int64_t z0 = lower ? i + 1 : t0, z1 = lower ? t1 : i;
+    for (int64_t j = z0 + threadIdx.x; j < z1; j += blockDim.x) p[i * n + j] = 0.0;
+  }
   for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
     double v = c0 * x[i * n + j];
     if (c1 != 0.0) v = fma(c1, x[k1 * n + j], v);

@@ -78,6 +78,10 @@ int sip_hb(const double *a2, const double *a1, const double *e, const double *c1
            int64_t max_inv_iter, int use_x0, int64_t ld, int layout, void *workspace,
            cudaStream_t st, bool invert_only, double *xl, double *xu);
 
+// bx_layout.cu
+int transpose(const double *src, double *dst, int64_t rows, int64_t cols, int64_t lds,
+              int64_t ldd, int64_t nbatch, int64_t bss, int64_t bsd, cudaStream_t stream);
+
 // workspace of the non-direct solvers (bx_api.cu dispatch)
 size_t other_workspace_bytes(int solver, int64_t batch, int64_t n);
 
