@@ -140,7 +140,7 @@ struct MergeInfo {
 };
 
 template <int K>
-__device__ __forceinline__ bool merge(const TwoPort<K> &a, const TwoPort<K> &b, TwoPort<K> &out,
+__device__ __noinline__ bool merge(const TwoPort<K> &a, const TwoPort<K> &b, TwoPort<K> &out,
                                       MergeInfo<K> &info) {
   Mat<K> S;
   const bool ok = inv_i_minus<K>(mm<K>(a.E.B, b.F.A), S);
@@ -299,35 +299,37 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   for (int k = 0; k < K; ++k) W1[k] = W2[k] = 0.0;
   constexpr int G = 4;
   static_assert(M % G == 0, "M must be a multiple of 4");
-  double ga2[2][G], ga1[2][G], ge[2][G], gc1[2][G], gc2[2][G], gb[2][G];
-  auto load_group = [&](int g, int buf) {
+  double ca2[G], ca1[G], ce[G], cc1[G], cc2[G], cb[G];  // group being eliminated
+  double na2[G], na1[G], ne[G], nc1[G], nc2[G], nb[G];  // group in flight
+  auto load_group = [&](int g, double (&A2)[G], double (&A1)[G], double (&E)[G], double (&C1)[G],
+                        double (&C2)[G], double (&Bv)[G]) {
     const int64_t i0 = base + g * G;
     if (VEC && i0 + G <= n) {
-      if (K == 2) ld4(c2p + lay(i0, s), ga2[buf]);
-      ld4(c1p + lay(i0, s), ga1[buf]);
-      ld4(ep + lay(i0, s), ge[buf]);
-      ld4(f1p + lay(i0, s), gc1[buf]);
-      if (K == 2) ld4(f2p + lay(i0, s), gc2[buf]);
-      ld4(bp + lay(i0, s), gb[buf]);
+      if (K == 2) ld4(c2p + lay(i0, s), A2);
+      ld4(c1p + lay(i0, s), A1);
+      ld4(ep + lay(i0, s), E);
+      ld4(f1p + lay(i0, s), C1);
+      if (K == 2) ld4(f2p + lay(i0, s), C2);
+      ld4(bp + lay(i0, s), Bv);
 #pragma unroll
       for (int u = 0; u < G; ++u) {  // slots outside the matrix are never trusted
         const int64_t i = i0 + u;
-        if (K != 2 || i < 2) ga2[buf][u] = 0.0;
-        if (i < 1) ga1[buf][u] = 0.0;
-        if (i > n - 2) gc1[buf][u] = 0.0;
-        if (K != 2 || i > n - 3) gc2[buf][u] = 0.0;
+        if (K != 2 || i < 2) A2[u] = 0.0;
+        if (i < 1) A1[u] = 0.0;
+        if (i > n - 2) C1[u] = 0.0;
+        if (K != 2 || i > n - 3) C2[u] = 0.0;
       }
     } else {
 #pragma unroll
       for (int u = 0; u < G; ++u) {
         const int64_t i = i0 + u;
         const bool in = i < n;
-        ga2[buf][u] = (K == 2 && in && i >= 2) ? ldg(c2p + lay(i, s)) : 0.0;
-        ga1[buf][u] = (in && i >= 1) ? ldg(c1p + lay(i, s)) : 0.0;
-        ge[buf][u] = in ? ldg(ep + lay(i, s)) : 1.0;  // padding rows: identity
-        gc1[buf][u] = (in && i <= n - 2) ? ldg(f1p + lay(i, s)) : 0.0;
-        gc2[buf][u] = (K == 2 && in && i <= n - 3) ? ldg(f2p + lay(i, s)) : 0.0;
-        gb[buf][u] = in ? ldg(bp + lay(i, s)) : 0.0;
+        A2[u] = (K == 2 && in && i >= 2) ? ldg(c2p + lay(i, s)) : 0.0;
+        A1[u] = (in && i >= 1) ? ldg(c1p + lay(i, s)) : 0.0;
+        E[u] = in ? ldg(ep + lay(i, s)) : 1.0;  // padding rows: identity
+        C1[u] = (in && i <= n - 2) ? ldg(f1p + lay(i, s)) : 0.0;
+        C2[u] = (K == 2 && in && i <= n - 3) ? ldg(f2p + lay(i, s)) : 0.0;
+        Bv[u] = in ? ldg(bp + lay(i, s)) : 0.0;
       }
     }
   };
@@ -344,13 +346,14 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
                    : "memory");
     }
   }
-  load_group(0, 0);
+  load_group(0, ca2, ca1, ce, cc1, cc2, cb);
+#pragma unroll 1
+  for (int g = 0; g < M / G; ++g) {
+    if (g + 1 < M / G) load_group(g + 1, na2, na1, ne, nc1, nc2, nb);
 #pragma unroll
-  for (int j = 0; j < M; ++j) {
-    const int g = j / G, u = j % G, buf = g & 1;
-    if (u == 0 && g + 1 < M / G) load_group(g + 1, buf ^ 1);
-    const double a2 = ga2[buf][u], a1 = ga1[buf][u], e = ge[buf][u], c1 = gc1[buf][u],
-                 c2 = gc2[buf][u], b = gb[buf][u];
+    for (int u = 0; u < G; ++u) {
+    const int j = g * G + u;
+    const double a2 = ca2[u], a1 = ca1[u], e = ce[u], c1 = cc1[u], c2 = cc2[u], b = cb[u];
     if (K == 2) nzc += (a2 != 0.0);
     double mu, ph, ps, y, W[K];
     if (j == 0) {
@@ -403,6 +406,11 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     m1 = mu; f1 = ph; g1 = ps; y1 = y;
 #pragma unroll
     for (int k = 0; k < K; ++k) { W2[k] = W1[k]; W1[k] = W[k]; }
+    }
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      ca2[u] = na2[u]; ca1[u] = na1[u]; ce[u] = ne[u]; cc1[u] = nc1[u]; cc2[u] = nc2[u]; cb[u] = nb[u];
+    }
   }
 
   BX_TR(1);
@@ -412,7 +420,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     double d1 = 0, d2 = 0, Wu1[K], Wu2[K], V1[K], V2[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) Wu1[k] = Wu2[k] = V1[k] = V2[k] = 0.0;
-#pragma unroll
+#pragma unroll 1
     for (int j = M - 1; j >= 0; --j) {
       const double p = st(0, j);
       const double q = K == 2 ? st(1, j) : 0.0;
@@ -493,7 +501,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     TwoPort<K> wp;
     if (lane < NW) wp = wport[lane];
     int off = NW * 31;
-#pragma unroll
+#pragma unroll 1
     for (int l = 0; (1 << l) < NW; ++l) {
       const int step = 1 << l;
       const TwoPort<K> other = shfl_down_port<K>(wp, step);
@@ -598,7 +606,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
 
   BX_TR(6);
   // ---------------- phase 3: x_j = d - W.L - V.R -----------------------------
-#pragma unroll
+#pragma unroll 1
   for (int g = 0; g < M / G; ++g) {
     double xv[G];
 #pragma unroll
