@@ -7,25 +7,25 @@
 
 Default workload: config 2 (BASELINE.json configs[1]) NPDM, B=8192 systems of
 order N=4096 per GPU, float64, seed 1 -- the configuration the headline metric
-is quoted on.  A step = one batched solve of the whole batch.  Weak scaling:
-every rank solves its own B systems (seeded per rank); no collective on the
-path.  Rank 0 prints ONE JSON line.
+is quoted on.  Other workloads (one JSON line each): mnpdm (config 2 sparse
+outer), ntdm (config 1), ntdm8k (one config-5 sweep), sip (config 4:
+512x512 grid, alpha 0.5, wavefront kernel).
 
-value     systems/s over all ranks, inputs resident in HBM (device-timed,
-          CUDA events, max over ranks); inputs (1.88 GB) exceed the 126 MB L2
-          so no flush is needed between steps.
-e2e       the same metric through the public C ABI call with pinned HOST
-          buffers: H2D of the step's diagonals + rhs and D2H of x inside the
-          timed region.
-roofline  dominant kernel: algorithmic bytes (56 B/row PD, 40 B/row TD:
-          diagonals + rhs read, x written) per launch / mean launch time,
-          against MEASURED_PEAKS.json hbm_gbs.
+A step = one batched solve of the whole batch on every rank (weak scaling:
+each rank its own seeded batch, no collective on the path).  Rank 0 prints
+ONE JSON line.
+
+value     the metric over all ranks, inputs resident in HBM (device-timed with
+          CUDA events, max over ranks); inputs exceed the 126 MB L2 (config.l2).
+e2e       the same metric through the C ABI with pinned HOST buffers: H2D of
+          the step's matrix + rhs and D2H of x inside the timed region.
+roofline  dominant kernel: algorithmic bytes per launch / mean launch time
+          (CUDA events on the launching stream) vs MEASURED_PEAKS.json hbm_gbs.
 cpu_baseline  the C restatement of the reference (oracle/c, OpenMP, all host
           threads) on a bounded sample of the same workload, rank 0, N=1.
 
 --impl reference times that CPU restatement (the reference is pure Python and
-is not compiled; the oracle port is its faithful CPU implementation) on this
-arm's config and metric.
+is not compiled; the oracle port is its faithful CPU implementation).
 """
 
 from __future__ import annotations
@@ -44,32 +44,16 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-WORKLOADS = {
-    # name: (kind, batch, n, generator)
-    "npdm": dict(kind="penta", solver="npdm", batch=8192, n=4096, cfg=1,
-                 desc="config 2 NPDM: B=8192 pentadiagonal DD systems, N=4096, seed 1"),
-    "mnpdm": dict(kind="penta", solver="mnpdm", batch=8192, n=4096, cfg=1, sparse=True,
-                  desc="config 2 MNPDM: B=8192, N=4096, sparse outer diagonals (nz(sub2)=2), seed 1"),
-    "ntdm": dict(kind="tri", solver="ntdm", batch=1024, n=1024, cfg=0,
-                 desc="config 1 NTDM: B=1024 tridiagonal DD systems, N=1024, seed 0"),
-    "ntdm8k": dict(kind="tri", solver="ntdm", batch=8192, n=8192, cfg=4,
-                   desc="config 5 sweep: B=8192 tridiagonal DD systems, N=8192, seed 0"),
-}
-
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 def load_peaks():
-    p = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
-        with open(p) as f:
-            d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
@@ -82,9 +66,7 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap,power.draw")
 
     def __init__(self, gpu_index):
-        self.gpu = gpu_index
-        self.rows = []
-        self.proc = None
+        self.gpu, self.rows, self.proc = gpu_index, [], None
 
     def start(self):
         try:
@@ -92,8 +74,7 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
         return self
@@ -124,254 +105,395 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
-def gen_inputs(wl, rank):
-    from paper_1804_09666_b200 import workloads as W
-
-    seed = [wl["cfg"], rank] if rank else wl["cfg"]   # rank 0 = the config's own seed
-    rng = np.random.default_rng(seed)
-    if wl["kind"] == "tri":
-        return W.td_dominant(wl["batch"], wl["n"], rng=rng)
-    return W.pd_dominant(wl["batch"], wl["n"], sparse_outer=wl.get("sparse", False), rng=rng)
-
-
-def rowaligned(arrs, kind, layout):
-    """Reference-length (B, L) host arrays -> row-aligned host arrays in the C
-    ABI storage: interleaved (n, B) or system-major (B, n)."""
-    offs = (-1, 0, 1) if kind == "tri" else (-2, -1, 0, 1, 2)
-    main = arrs[len(offs) // 2]
+def rowaligned(arrs, offsets, layout):
+    """Reference-length (B, L) host arrays + rhs -> row-aligned host arrays in
+    the C ABI storage: interleaved (n, B) or system-major (B, n)."""
+    main = arrs[offsets.index(0)]
     bsz, n = main.shape
     out = []
-    for a, off in zip(arrs[:len(offs)], offs):
+    for a, off in zip(arrs[:len(offsets)], offsets):
         first = -off if off < 0 else 0
         if layout == "interleaved":
-            r = np.zeros((n, bsz))
-            r[first:first + a.shape[1]] = a.T
+            r = np.zeros((n, bsz)); r[first:first + a.shape[1]] = a.T
         else:
-            r = np.zeros((bsz, n))
-            r[:, first:first + a.shape[1]] = a
+            r = np.zeros((bsz, n)); r[:, first:first + a.shape[1]] = a
         out.append(r)
-    rhs = arrs[len(offs)]
+    rhs = arrs[len(offsets)]
     out.append(np.ascontiguousarray(rhs.T if layout == "interleaved" else rhs))
     return out
 
 
-def cpu_port_rate(wl, arrs, sample, threads=None):
-    """Time the C restatement of the reference on `sample` systems; returns
-    (systems/s, seconds, threads)."""
-    from oracle import cport
+DIRECT = {  # name: (solver, batch, n, config index, sparse outer, description)
+    "npdm": ("npdm", 8192, 4096, 1, False,
+             "config 2 NPDM: B=8192 pentadiagonal DD systems, N=4096, seed 1"),
+    "mnpdm": ("mnpdm", 8192, 4096, 1, True,
+              "config 2 MNPDM: B=8192, N=4096, sparse outer diagonals (nz(sub2)=2), seed 1"),
+    "ntdm": ("ntdm", 1024, 1024, 0, False,
+             "config 1 NTDM: B=1024 tridiagonal DD systems, N=1024, seed 0"),
+    "ntdm8k": ("ntdm", 8192, 8192, 4, False,
+               "config 5 sweep: B=8192 tridiagonal DD systems, N=8192"),
+}
 
-    kind = wl["kind"]
+
+def direct_inputs(name, rank=0):
+    from paper_1804_09666_b200 import workloads as W
+    solver, bsz, n, cfg, sparse, _ = DIRECT[name]
+    rng = np.random.default_rng([cfg, rank] if rank else cfg)
+    if solver == "ntdm":
+        return W.td_dominant(bsz, n, rng=rng)
+    return W.pd_dominant(bsz, n, sparse_outer=sparse, rng=rng)
+
+
+def cpu_direct_rate(solver, arrs, sample):
+    """Time the C restatement on `sample` systems: (systems/s, seconds, threads)."""
+    from oracle import cport
     sl = [a[:sample] for a in arrs]
-    if kind == "tri":
+    if solver == "ntdm":
         d, e, f = cport.rowaligned_tri(*sl[:3])
         b = np.ascontiguousarray(sl[3])
         cport.ntdm(d[:8], e[:8], f[:8], b[:8])
-        t0 = time.perf_counter()
-        cport.ntdm(d, e, f, b)
-        dt = time.perf_counter() - t0
+        t0 = time.perf_counter(); cport.ntdm(d, e, f, b); dt = time.perf_counter() - t0
     else:
-        r = cport.rowaligned_penta(*sl[:5])
-        b = np.ascontiguousarray(sl[5])
-        mod = 1 if wl["solver"] == "mnpdm" else 0
+        r = cport.rowaligned_penta(*sl[:5]); b = np.ascontiguousarray(sl[5])
+        mod = 1 if solver == "mnpdm" else 0
         cport.penta(mod, *(x[:8] for x in r), b[:8])
-        t0 = time.perf_counter()
-        cport.penta(mod, *r, b)
-        dt = time.perf_counter() - t0
+        t0 = time.perf_counter(); cport.penta(mod, *r, b); dt = time.perf_counter() - t0
     return sample / dt, dt, cport.threads()
 
 
-def run_reference(args, wl):
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+class Direct:
+    metric, unit, scaling = "systems_solved_per_s", "systems/s", "weak"
+    launches_per_step = 1
+
+    def __init__(self, args, rank, dev, name):
+        import torch
+        from paper_1804_09666_b200 import _lib
+        from paper_1804_09666_b200.core import workspace
+        self.args = args
+        solver, batch, n, cfg, sparse, desc = DIRECT[name]
+        self.solver, self.batch, self.n = solver, batch, n
+        self.kind = "tri" if solver == "ntdm" else "penta"
+        self.arrs = direct_inputs(name, rank)
+        offsets = (-1, 0, 1) if self.kind == "tri" else (-2, -1, 0, 1, 2)
+        self.lay = _lib.LAYOUT_INTERLEAVED if args.layout == "interleaved" else _lib.LAYOUT_SYSTEM_MAJOR
+        self.algo = {"sequential": _lib.ALGO_SEQUENTIAL, "partitioned": _lib.ALGO_PARTITIONED}[args.algo]
+        self.host = rowaligned(self.arrs, offsets, args.layout)
+        self.ld = batch if args.layout == "interleaved" else n
+        self.d_in = [torch.from_numpy(h).to(dev) for h in self.host]
+        self.x = torch.empty(self.host[-1].shape, dtype=torch.float64, device=dev)
+        self.status = torch.empty(batch, dtype=torch.int32, device=dev)
+        self.index = torch.empty(batch, dtype=torch.int32, device=dev)
+        self.nz = torch.empty(batch, dtype=torch.int64, device=dev)
+        L = _lib.lib()
+        self.ws = workspace(L.bx_workspace_bytes(_lib.SOLVER[solver], batch, n, self.lay, self.algo), dev)
+        self.bytes_per_row = 40 if self.kind == "tri" else 56
+        self.units = batch
+        self.config = {"workload": desc, "solver": solver, "algo": args.algo, "batch_per_gpu": batch,
+                       "n": n, "layout": f"{args.layout} row-aligned",
+                       "l2": f"inputs {self.bytes_per_row * batch * n / 1e9:.2f} GB per step > 126 MB L2, no flush"}
+
+    def solve(self, ins, out):
+        import torch
+        from paper_1804_09666_b200 import _lib
+        from paper_1804_09666_b200.core import ptr
+        L, s = _lib.lib(), torch.cuda.current_stream().cuda_stream
+        tail = (self.batch, self.n, self.ld, self.lay, self.algo, ptr(self.ws), self.ws.numel(), s)
+        if self.solver == "ntdm":
+            rc = L.bx_ntdm_f64(*(ptr(t) for t in ins), ptr(out), ptr(self.status), ptr(self.index), *tail)
+        elif self.solver == "npdm":
+            rc = L.bx_npdm_f64(*(ptr(t) for t in ins), ptr(out), ptr(self.status), ptr(self.index), *tail)
+        else:
+            rc = L.bx_mnpdm_f64(*(ptr(t) for t in ins), ptr(out), ptr(self.status), ptr(self.index),
+                                ptr(self.nz), *tail)
+        _lib.check(rc, self.solver)
+
+    def step(self):
+        self.solve(self.d_in, self.x)
+
+    def check(self):
+        """Sampled parity gate against the C restatement of the reference."""
+        from oracle import cport
+        idx = np.arange(0, self.batch, max(1, self.batch // 16))
+        sl = [a[idx] for a in self.arrs]
+        if self.kind == "tri":
+            ref, _, _ = cport.ntdm(*cport.rowaligned_tri(*sl[:3]), np.ascontiguousarray(sl[3]))
+        else:
+            ref, _, _, _ = cport.penta(1 if self.solver == "mnpdm" else 0,
+                                       *cport.rowaligned_penta(*sl[:5]), np.ascontiguousarray(sl[5]))
+        x = self.x.cpu().numpy()
+        x = x.T if self.args.layout == "interleaved" else x
+        err = float(np.max(np.abs(x[idx] - ref) / np.max(np.abs(ref), axis=1, keepdims=True)))
+        assert int((self.status != 0).sum()) == 0, "unexpected zero pivot"
+        assert err <= 1e-10, f"parity gate failed: {err}"
+        return err
+
+    def e2e_prepare(self):
+        import torch
+        self.pinned = [torch.from_numpy(h).pin_memory() for h in self.host]
+        self.x_host = torch.empty(self.host[-1].shape, dtype=torch.float64).pin_memory()
+        self.d_e2e = [torch.empty_like(t) for t in self.d_in]
+        self.x_e2e = torch.empty_like(self.x)
+        self.h2d = sum(h.nbytes for h in self.host)
+        self.d2h = self.x_host.numel() * 8
+
+    def e2e_step(self):
+        for h, d in zip(self.pinned, self.d_e2e):
+            d.copy_(h, non_blocking=True)
+        self.solve(self.d_e2e, self.x_e2e)
+        self.x_host.copy_(self.x_e2e, non_blocking=True)
+
+    def roofline(self, mean_launch, peak):
+        alg = self.bytes_per_row * self.batch * self.n
+        ach = alg / mean_launch / 1e9
+        return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": None, "kernel": f"bx {self.solver} ({self.args.algo})",
+                "algorithmic_bytes_per_launch": alg, "bytes_per_row": self.bytes_per_row}
+
+    def cpu_baseline(self, budget_s=5.0):
+        rate0, _, _ = cpu_direct_rate(self.solver, self.arrs, min(self.batch, 128))
+        sample = int(min(self.batch, max(64, rate0 * budget_s)))
+        tot_s, tot_n, passes = 0.0, 0, 0
+        while tot_s < budget_s and passes < 20:
+            rate, dt, thr = cpu_direct_rate(self.solver, self.arrs, sample)
+            tot_s += dt; tot_n += sample; passes += 1
+        return {"value": tot_n / tot_s, "unit": self.unit, "cores": thr, "kind": "port",
+                "sample": f"{passes} pass(es) over {sample} of {self.batch} systems ({tot_s:.1f} s), "
+                          f"C restatement of the reference (oracle/c/bx_oracle.c), OpenMP {thr} threads"}
+
+
+SIP_CFG = dict(batch=64, n=262144, m=512, alpha=0.5, cfg=3)
+
+
+class Sip:
+    metric, unit, scaling = "sip_system_iterations_per_s", "system-iterations/s", "weak"
+    launches_per_step = 1
+
+    def __init__(self, args, rank, dev):
+        import torch
+        from paper_1804_09666_b200 import _lib, workloads as W
+        from paper_1804_09666_b200.core import workspace
+        c = SIP_CFG
+        self.batch, self.n, self.m, self.alpha = c["batch"], c["n"], c["m"], c["alpha"]
+        rng = np.random.default_rng([c["cfg"], rank] if rank else c["cfg"])
+        self.arrs = W.five_point(self.batch, self.n, self.m, rng=rng)
+        self.tol = W.sip_tolerance(self.arrs[5])
+        m = self.m
+        self.host = rowaligned(self.arrs, (-m, -1, 0, 1, m), "system")
+        self.d_in = [torch.from_numpy(h).to(dev) for h in self.host]
+        self.d_tol = torch.from_numpy(self.tol).to(dev)
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.x = torch.empty((self.batch, self.n), **f64)
+        self.iters = torch.empty(self.batch, dtype=torch.int64, device=dev)
+        self.res = torch.empty(self.batch, **f64)
+        self.status = torch.empty(self.batch, dtype=torch.int32, device=dev)
+        self.ws = workspace(_lib.lib().bx_sip_workspace_bytes(self.batch, self.n, m), dev)
+        desc = (f"config 4 SIP: B={self.batch} five-point systems, {self.n // m}x{m} grid "
+                f"(N={self.n}, offsets +-1, +-{m}), Stone alpha={self.alpha}, rel. tol 1e-8, "
+                f"<=500 iterations, seed {c['cfg']}; a step = one full sip_solve (ILU(0) + all iterations)")
+        self.config = {"workload": desc, "solver": "sip", "algo": "wavefront",
+                       "batch_per_gpu": self.batch, "n": self.n, "m": m, "alpha": self.alpha,
+                       "l2": "every iteration streams the 22 skewed planes (5.9 GB) > 126 MB L2"}
+
+    def solve(self, ins, x):
+        import torch
+        from paper_1804_09666_b200 import _lib
+        from paper_1804_09666_b200.core import ptr
+        _lib.call("bx_sip_f64", *(ptr(t) for t in ins[:5]), ptr(ins[5]), ptr(self.d_tol), ptr(x),
+                  None, ptr(self.iters), ptr(self.res), None, ptr(self.status), None, None,
+                  self.batch, self.n, self.m, self.alpha, 500, 0, self.n, _lib.LAYOUT_SYSTEM_MAJOR,
+                  2, ptr(self.ws), self.ws.numel(), torch.cuda.current_stream().cuda_stream)
+
+    def step(self):
+        self.solve(self.d_in, self.x)
+
+    def check(self):
+        from oracle import cport
+        assert int((self.status != 0).sum()) == 0
+        self.total_iters = int(self.iters.sum())
+        self.units = self.total_iters
+        idx = np.arange(0, self.batch, max(1, self.batch // 4))
+        ref = cport.sip(*cport.rowaligned_penta(*(a[idx] for a in self.arrs[:5]), m=self.m),
+                        self.arrs[5][idx], self.tol[idx], m=self.m, alpha=self.alpha)
+        assert np.array_equal(self.iters.cpu().numpy()[idx], ref["iterations"])
+        assert np.array_equal(self.x.cpu().numpy()[idx], ref["x"]), "SIP parity gate"
+        return 0.0
+
+    def e2e_prepare(self):
+        import torch
+        self.pinned = [torch.from_numpy(h).pin_memory() for h in self.host]
+        self.x_host = torch.empty((self.batch, self.n), dtype=torch.float64).pin_memory()
+        self.d_e2e = [torch.empty_like(t) for t in self.d_in]
+        self.x_e2e = torch.empty_like(self.x)
+        self.h2d = sum(h.nbytes for h in self.host)
+        self.d2h = self.x_host.numel() * 8
+
+    def e2e_step(self):
+        for h, d in zip(self.pinned, self.d_e2e):
+            d.copy_(h, non_blocking=True)
+        self.solve(self.d_e2e, self.x_e2e)
+        self.x_host.copy_(self.x_e2e, non_blocking=True)
+
+    def roofline(self, mean_launch, peak):
+        alg = 104 * self.n * self.total_iters   # SURVEY 8d: 104 B per row-iteration
+        ach = alg / mean_launch / 1e9
+        return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": None, "kernel": "bx sip_wave (setup + all iterations, one launch)",
+                "algorithmic_bytes_per_launch": alg, "bytes_per_row_iteration": 104,
+                "note": "Algorithm 1 verbatim streams ~184 B/row-iteration (K, factors, y, A, b, x)"}
+
+    def cpu_baseline(self, budget_s=5.0):
+        from oracle import cport
+        sample = 8
+        a = [x[:sample] for x in self.arrs]
+        r = cport.rowaligned_penta(*a[:5], m=self.m)
+        t0 = time.perf_counter()
+        out = cport.sip(*r, a[5], self.tol[:sample], m=self.m, alpha=self.alpha)
+        dt = time.perf_counter() - t0
+        its = int(out["iterations"].sum())
+        return {"value": its / dt, "unit": self.unit, "cores": cport.threads(), "kind": "port",
+                "sample": f"{sample} of {self.batch} systems ({its} system-iterations incl. ILU setup, "
+                          f"{dt:.1f} s), C restatement (oracle/c/bx_oracle.c), OpenMP {cport.threads()} threads"}
+
+
+WORKLOADS = sorted(list(DIRECT) + ["sip"])
+
+
+def cpu_reference_arm(args):
     """--impl reference: the CPU restatement on the host cores, rank 0 only."""
-    ws, rank, _ = dist_env()
+    world, rank, _ = dist_env()
     if rank != 0:
         return
-    arrs = gen_inputs(wl, 0)
-    bsz = wl["batch"]
-    # bounded sample per step: aim ~1-3 s of CPU work per step
-    rate0, _, _ = cpu_port_rate(wl, arrs, min(bsz, 256))
-    sample = int(min(bsz, max(64, rate0 * 1.5)))
-    for _ in range(args.warmup):
-        cpu_port_rate(wl, arrs, min(sample, 64))
+    from oracle import cport
     times = []
-    for _ in range(args.steps):
-        rate, dt, thr = cpu_port_rate(wl, arrs, sample)
-        times.append(dt)
-    tot = sum(times)
-    value = sample * len(times) / tot
-    line = {
-        "impl": "reference", "metric": "systems_solved_per_s", "value": value,
-        "unit": "systems/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "sample_systems_per_step": sample},
-        "cpu_baseline": {"value": value, "unit": "systems/s", "cores": thr, "kind": "port",
-                         "sample": f"{sample} of {bsz} systems per step, C restatement "
-                                   f"(oracle/c/bx_oracle.c, OpenMP {thr} threads)"},
-        "e2e": {"value": value, "unit": "systems/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
+    if args.workload in DIRECT:
+        solver, bsz, n, cfg, sparse, desc = DIRECT[args.workload]
+        arrs = direct_inputs(args.workload)
+        metric, unit = "systems_solved_per_s", "systems/s"
+        rate0, _, _ = cpu_direct_rate(solver, arrs, min(bsz, 256))
+        sample = int(min(bsz, max(64, rate0 * 1.5)))          # ~1.5 s of CPU work per step
+        for _ in range(args.warmup):
+            cpu_direct_rate(solver, arrs, min(sample, 64))
+        for _ in range(args.steps):
+            _, dt, thr = cpu_direct_rate(solver, arrs, sample)
+            times.append(dt)
+        value = sample * len(times) / sum(times)
+        samp = f"{sample} of {bsz} systems per step"
+    else:
+        from paper_1804_09666_b200 import workloads as W
+        c = SIP_CFG
+        metric, unit = "sip_system_iterations_per_s", "system-iterations/s"
+        arrs = W.five_point(4, c["n"], c["m"], rng=np.random.default_rng(c["cfg"]))
+        tol = W.sip_tolerance(arrs[5])
+        r = cport.rowaligned_penta(*arrs[:5], m=c["m"])
+        its = 0
+        for k in range(1 + args.steps):
+            t0 = time.perf_counter()
+            out = cport.sip(*r, arrs[5], tol, m=c["m"], alpha=c["alpha"])
+            if k >= 1:
+                times.append(time.perf_counter() - t0)
+                its += int(out["iterations"].sum())
+        value = its / sum(times)
+        thr = cport.threads()
+        desc, samp = "config 4 SIP", "4 of 64 systems per step (full sip_solve each)"
+    line = {"impl": "reference", "metric": metric, "value": value, "unit": unit,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "sample": samp},
+            "cpu_baseline": {"value": value, "unit": unit, "cores": thr, "kind": "port",
+                             "sample": f"{samp}, C restatement (oracle/c/bx_oracle.c), OpenMP {thr} threads"},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
-def run_ours(args, wl):
+def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1804_09666_b200 import PentaMatrix, TriMatrix, _lib
-    from paper_1804_09666_b200.core import ptr, workspace
-
-    ws_world, rank, local = dist_env()
-    if ws_world > 1:
+    world, rank, local = dist_env()
+    if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    kind, bsz, n = wl["kind"], wl["batch"], wl["n"]
-    algo = {"sequential": _lib.ALGO_SEQUENTIAL, "partitioned": _lib.ALGO_PARTITIONED}[args.algo]
-
-    arrs = gen_inputs(wl, rank)
-    lay = _lib.LAYOUT_INTERLEAVED if args.layout == "interleaved" else _lib.LAYOUT_SYSTEM_MAJOR
-    host = rowaligned(arrs, kind, args.layout)                # C-ABI layout, host
-    ld = bsz if args.layout == "interleaved" else n
-    dev_in = [torch.from_numpy(h).to(dev) for h in host]
-    x = torch.empty(host[-1].shape, dtype=torch.float64, device=dev)
-    status = torch.empty(bsz, dtype=torch.int32, device=dev)
-    index = torch.empty(bsz, dtype=torch.int32, device=dev)
-    nz = torch.empty(bsz, dtype=torch.int64, device=dev)
-    L = _lib.lib()
-    solver = wl["solver"]
-    nbytes = L.bx_workspace_bytes(_lib.SOLVER[solver], bsz, n, lay, algo)
-    wsb = workspace(nbytes, dev)
-    stream = torch.cuda.current_stream()
-
-    def solve(ins, out):
-        s = stream.cuda_stream
-        if solver == "ntdm":
-            rc = L.bx_ntdm_f64(*(ptr(t) for t in ins), ptr(out), ptr(status), ptr(index), bsz, n,
-                               ld, lay, algo, ptr(wsb), wsb.numel(), s)
-        elif solver == "npdm":
-            rc = L.bx_npdm_f64(*(ptr(t) for t in ins), ptr(out), ptr(status), ptr(index), bsz, n,
-                               ld, lay, algo, ptr(wsb), wsb.numel(), s)
-        else:
-            rc = L.bx_mnpdm_f64(*(ptr(t) for t in ins), ptr(out), ptr(status), ptr(index), ptr(nz),
-                                bsz, n, ld, lay, algo, ptr(wsb), wsb.numel(), s)
-        _lib.check(rc, solver)
-
-    # ---- correctness gate on this rank's data (sampled systems vs oracle) ----
-    solve(dev_in, x)
-    torch.cuda.synchronize()
-    assert int((status != 0).sum()) == 0, "unexpected zero pivot"
+    wl = Sip(args, rank, dev) if args.workload == "sip" else Direct(args, rank, dev, args.workload)
 
     def barrier():
-        if ws_world > 1:
+        if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(v):
-        if ws_world > 1:
+        if world > 1:
             t = torch.tensor([v], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             return float(t.item())
         return v
 
-    # ---- device-resident timed region ----
+    wl.step()                      # correctness gate: sampled systems vs the C restatement
+    torch.cuda.synchronize()
+    gate_err = wl.check()
+
     for _ in range(args.warmup):
-        solve(dev_in, x)
+        wl.step()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     sampler = ClockSampler(local).start() if rank == 0 else None
-    time.sleep(0.3 if sampler else 0)
+    if sampler:
+        time.sleep(0.3)
     barrier()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
     for k in range(args.steps):
         ev[k][0].record()
-        solve(dev_in, x)
+        wl.step()
         ev[k][1].record()
-    t_end.record()
+    t1.record()
     barrier()
     clocks = sampler.stop() if sampler else None
-    elapsed = max_over_ranks(t_start.elapsed_time(t_end) / 1e3)
-    launch_s = [a.elapsed_time(b) / 1e3 for a, b in ev]
-    mean_launch = statistics.mean(launch_s)
-    value = bsz * ws_world * args.steps / elapsed
-
-    bytes_per_row = 40 if kind == "tri" else 56
-    alg_bytes = bytes_per_row * bsz * n
+    elapsed = max_over_ranks(t0.elapsed_time(t1) / 1e3)
+    mean_launch = statistics.mean(a.elapsed_time(b) / 1e3 for a, b in ev)
+    value = wl.units * world * args.steps / elapsed
     peak, peak_src = load_peaks()
-    achieved = alg_bytes / mean_launch / 1e9
+    roof = wl.roofline(mean_launch, peak)
+    roof.update(mean_launch_ms=1e3 * mean_launch, peak_source=peak_src)
 
-    # ---- end-to-end through the C ABI with pinned host buffers ----
-    pinned = [torch.from_numpy(h).pin_memory() for h in host]
-    x_host = torch.empty(host[-1].shape, dtype=torch.float64).pin_memory()
-    dev_e2e = [torch.empty_like(t) for t in dev_in]
-    x_e2e = torch.empty_like(x)
-
-    def e2e_step():
-        for hsrc, ddst in zip(pinned, dev_e2e):
-            ddst.copy_(hsrc, non_blocking=True)
-        solve(dev_e2e, x_e2e)
-        x_host.copy_(x_e2e, non_blocking=True)
-
+    wl.e2e_prepare()
     for _ in range(max(1, min(args.warmup, 2))):
-        e2e_step()
+        wl.e2e_step()
     barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_steps = max(1, min(args.steps, 5))
+    e0.record()
     for _ in range(e2e_steps):
-        e2e_step()
+        wl.e2e_step()
     e1.record()
     barrier()
     e2e_elapsed = max_over_ranks(e0.elapsed_time(e1) / 1e3)
-    assert torch.equal(x_host, x.cpu()), "e2e result differs from the resident run"
-    h2d = sum(h.nbytes for h in host)
-    d2h = x_host.numel() * 8
-
-    if rank != 0:
-        if ws_world > 1:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
+    assert torch.equal(wl.x_host, wl.x.cpu()), "e2e result differs from the resident run"
 
     cpu = None
-    if ws_world == 1 and not args.no_cpu_baseline:
-        rate0, _, _ = cpu_port_rate(wl, arrs, min(bsz, 128))
-        sample = int(min(bsz, max(64, rate0 * 5)))          # <= ~5 s per pass
-        tot_s, tot_n, passes = 0.0, 0, 0
-        while tot_s < 5.0 and passes < 20:                  # ~5-10 s of CPU work in all
-            rate, dt, thr = cpu_port_rate(wl, arrs, sample)
-            tot_s += dt
-            tot_n += sample
-            passes += 1
-        cpu = {"value": tot_n / tot_s, "unit": "systems/s", "cores": thr, "kind": "port",
-               "sample": f"{passes} pass(es) over {sample} of {bsz} systems ({tot_s:.1f} s), "
-                         f"C restatement of the reference (oracle/c/bx_oracle.c), OpenMP {thr} threads"}
-
-    line = {
-        "metric": "systems_solved_per_s", "value": value, "unit": "systems/s",
-        "n_gpus": ws_world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "solver": solver, "algo": args.algo,
-                   "batch_per_gpu": bsz, "n": n, "layout": f"{args.layout} row-aligned",
-                   "l2": f"inputs {alg_bytes/1e9:.2f} GB per step > 126 MB L2, no flush",
-                   "parallelism": f"dp{ws_world} (system-index sharding)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "kernel": f"bx {solver} ({args.algo})",
-                     "algorithmic_bytes_per_launch": alg_bytes,
-                     "mean_launch_ms": 1e3 * mean_launch, "peak_source": peak_src},
-        "cpu_baseline": cpu,
-        "e2e": {"value": bsz * ws_world * e2e_steps / e2e_elapsed, "unit": "systems/s",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "pinned host -> cudaMemcpyAsync -> bx C ABI -> D2H x"},
-        "gpu_launches": args.steps,
-        "clocks": clocks,
-    }
-    print(json.dumps(line))
-    if ws_world > 1:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = wl.cpu_baseline()
+    if rank == 0:
+        cfg = dict(wl.config)
+        cfg["parallelism"] = f"dp{world} (system-index sharding)"
+        cfg["parity_gate"] = f"sampled systems vs C restatement, max rel err {gate_err:.2e}"
+        line = {
+            "metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
+            "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": cfg, "roofline": roof, "cpu_baseline": cpu,
+            "e2e": {"value": wl.units * world * e2e_steps / e2e_elapsed, "unit": wl.unit,
+                    "h2d_bytes_per_step": wl.h2d, "d2h_bytes_per_step": wl.d2h,
+                    "path": "pinned host -> cudaMemcpyAsync -> bx C ABI -> D2H x"},
+            "gpu_launches": args.steps * wl.launches_per_step,
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
@@ -382,21 +504,19 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="npdm", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="npdm", choices=WORKLOADS)
     ap.add_argument("--algo", default="partitioned", choices=["sequential", "partitioned"])
     ap.add_argument("--layout", default=None, choices=["interleaved", "system"],
                     help="C-ABI storage (default: system-major for partitioned, interleaved for sequential)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(args.warmup, 3)
     if args.layout is None:
         args.layout = "system" if args.algo == "partitioned" else "interleaved"
-    wl = WORKLOADS[args.workload]
     if args.impl == "reference":
-        run_reference(args, wl)
+        cpu_reference_arm(args)
     else:
-        run_ours(args, wl)
+        run_ours(args)
 
 
 if __name__ == "__main__":

@@ -140,7 +140,7 @@ struct MergeInfo {
 };
 
 template <int K>
-__device__ __noinline__ bool merge(const TwoPort<K> &a, const TwoPort<K> &b, TwoPort<K> &out,
+__device__ __forceinline__ bool merge(const TwoPort<K> &a, const TwoPort<K> &b, TwoPort<K> &out,
                                       MergeInfo<K> &info) {
   Mat<K> S;
   const bool ok = inv_i_minus<K>(mm<K>(a.E.B, b.F.A), S);
@@ -420,7 +420,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     double d1 = 0, d2 = 0, Wu1[K], Wu2[K], V1[K], V2[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) Wu1[k] = Wu2[k] = V1[k] = V2[k] = 0.0;
-#pragma unroll 1
+#pragma unroll
     for (int j = M - 1; j >= 0; --j) {
       const double p = st(0, j);
       const double q = K == 2 ? st(1, j) : 0.0;
