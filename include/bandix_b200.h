@@ -172,7 +172,7 @@ int bx_ilu0_f64(const double *subm, const double *sub1, const double *main, cons
  * ([batch][max_iter], r after each iteration).  status: OK, ZERO_PIVOT(index),
  * MAX_ITER, DIVERGED (r > 1e6 r0), NOT_GRID (wavefront only).  algo:
  * BX_ALGO_SEQUENTIAL (one thread per system, any band), BX_ALGO_WAVEFRONT
- * (grid-structured systems, n % m == 0, m <= 1024: one CTA per system walks the
+ * (grid-structured systems, n % m == 0, m <= 512: one CTA per system walks the
  * grid's anti-diagonals) or BX_ALGO_AUTO. */
 #define BX_ALGO_WAVEFRONT 2
 size_t bx_sip_workspace_bytes(int64_t batch, int64_t n, int64_t m);

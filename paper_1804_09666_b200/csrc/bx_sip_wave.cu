@@ -37,31 +37,62 @@ enum Plane {
 
 struct Skew {
   double *ws;
-  int64_t batch, m, T;  // T = R + m - 1 slices
+  int64_t batch, m, T, mp;  // T = R + m - 1 slices; mp = row stride (m rounded up to even)
   __device__ __forceinline__ double *at(int p, int64_t s, int64_t t) const {
-    return ws + (((int64_t)p * batch + s) * T + t) * m;
+    return ws + (((int64_t)p * batch + s) * T + t) * mp;
   }
 };
+
+// ---- TMA bulk copies into a shared-memory ring, completion on mbarriers ----
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 
 __device__ __forceinline__ double nan_max(double a, double b) {
   if (a != a || b != b) return __longlong_as_double(0x7ff8000000000000LL);
   return a > b ? a : b;
 }
 
+constexpr int NPL = 11;  // plane rows per ring stage
+
 template <class Lay>
-__global__ void sip_wave_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
+__global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
                                 const double *__restrict__ ep, const double *__restrict__ c1p,
                                 const double *__restrict__ c2p, const double *__restrict__ bp,
                                 const double *__restrict__ tol, double *__restrict__ xout,
                                 double *__restrict__ best_x, int64_t *iters, double *res,
                                 double *best_res, int32_t *status, int32_t *index,
                                 double *history, Skew S, int64_t n, double alpha,
-                                int64_t max_iter, int use_x0, Lay lay) {
+                                int64_t max_iter, int use_x0, Lay lay, int nst) {
   extern __shared__ double sh[];
   const int64_t m = S.m, R = n / m, T = S.T;
   const int q = threadIdx.x;
   const int64_t s = blockIdx.x;
-  __shared__ int s_bad, s_notgrid, s_go, s_bestcopy, s_cur;
+  __shared__ int s_bad, s_notgrid, s_go, s_bestcopy;
   __shared__ double s_red[32];
   if (q == 0) { s_bad = 0x7fffffff; s_notgrid = 0; }
   __syncthreads();
@@ -182,25 +213,71 @@ __global__ void sip_wave_kernel(const double *__restrict__ a2p, const double *__
   double *xs = sh;          // [4][m] window of the previous iterate
   double *ys = sh + 4 * m;  // [3][m]
   double *xn = sh + 7 * m;  // [4][m] window of the new iterate
+  // ring of NST stages x NPL plane rows (padded stride mp), filled by TMA bulk copies
+  const int64_t mp = S.mp;
+  double *ring = sh + 11 * m + (11 * m & 1);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(ring + (int64_t)nst * NPL * mp);
+  auto R_ = [&](int stage, int j) { return ring + ((int64_t)stage * NPL + j) * mp; };
   auto valid_cell = [&](int64_t t) { const int64_t p = t - q; return p >= 0 && p < R; };
+  if (q == 0)
+    for (int i = 0; i < nst; ++i) mbar_init(bars + i);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // setup's plane writes -> TMA reads
+  __syncthreads();
+  unsigned g_issue = 0, g_use = 0;  // global sequence numbers of ring stages
+  // thread 0: queue the plane rows of one step into the next ring stage
+  auto issue_rows = [&](const int *planes, const int64_t *slices, int cnt, const int *slots) {
+    const int stg = (int)(g_issue % nst);
+    unsigned bytes = 0;
+    int64_t c0s[NPL], c1s[NPL];
+    for (int j = 0; j < cnt; ++j) {
+      const int64_t u = slices[j];
+      c0s[j] = c1s[j] = 0;
+      if (u < 0 || u >= T) continue;
+      const int64_t qlo = u - R + 1 > 0 ? u - R + 1 : 0, qhi = u < m - 1 ? u : m - 1;
+      if (qlo > qhi) continue;
+      c0s[j] = qlo & ~(int64_t)1;
+      c1s[j] = (qhi + 2) & ~(int64_t)1;
+      bytes += (unsigned)((c1s[j] - c0s[j]) * sizeof(double));
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect(bars + stg, bytes);
+    for (int j = 0; j < cnt; ++j)
+      if (c1s[j] > c0s[j])
+        bulk_g2s(R_(stg, slots[j]) + c0s[j], S.at(planes[j], s, slices[j]) + c0s[j],
+                 (unsigned)((c1s[j] - c0s[j]) * sizeof(double)), bars + stg);
+    ++g_issue;
+  };
+  auto wait_stage = [&]() -> int {
+    const int stg = (int)(g_use % nst);
+    mbar_wait(bars + stg, (g_use / nst) & 1);
+    ++g_use;
+    return stg;
+  };
 
-  // residual of cell (slice tt, column q) from a window w[4][m] holding slices
-  // tt-1, tt, tt+1 (core.py / iterative.py:213-221 order, acc from 0)
-  auto residual_cell = [&](const Skew &SS, const double *w, int64_t tt) -> double {
+  // residual of cell (slice tt, column q) from a window w[4][m] of x slices
+  // tt-1..tt+1 and the row's A/b values (iterative.py:213-221 order, acc from 0)
+  auto residual_from = [&](const double *w, int64_t tt, double a2, double a1, double e,
+                           double c1, double c2, double bb) -> double {
     const int64_t p = tt - q, i = p * m + q;
     auto X = [&](int64_t sl, int col) { return w[(int)(((sl % 4) + 4) % 4) * m + col]; };
-    double acc = add(0.0, mul(*(SS.at(PE, s, tt) + q), X(tt, q)));
+    double acc = add(0.0, mul(e, X(tt, q)));
     if (i >= 1) {
-      if (q >= 1) acc = add(acc, mul(*(SS.at(PA1, s, tt) + q), X(tt - 1, q - 1)));
-      else if (m == 2) acc = add(acc, mul(*(SS.at(PA1, s, tt) + q), X(tt, q + 1)));
+      if (q >= 1) acc = add(acc, mul(a1, X(tt - 1, q - 1)));
+      else if (m == 2) acc = add(acc, mul(a1, X(tt, q + 1)));
     }
     if (i <= n - 2) {
-      if (q <= m - 2) acc = add(acc, mul(*(SS.at(PC1, s, tt) + q), X(tt + 1, q + 1)));
-      else if (m == 2) acc = add(acc, mul(*(SS.at(PC1, s, tt) + q), X(tt, q - 1)));
+      if (q <= m - 2) acc = add(acc, mul(c1, X(tt + 1, q + 1)));
+      else if (m == 2) acc = add(acc, mul(c1, X(tt, q - 1)));
     }
-    if (i >= m) acc = add(acc, mul(*(SS.at(PA2, s, tt) + q), X(tt - 1, q)));
-    if (i + m <= n - 1) acc = add(acc, mul(*(SS.at(PC2, s, tt) + q), X(tt + 1, q)));
-    return fabs(sub(*(SS.at(PB, s, tt) + q), acc));
+    if (i >= m) acc = add(acc, mul(a2, X(tt - 1, q)));
+    if (i + m <= n - 1) acc = add(acc, mul(c2, X(tt + 1, q)));
+    return fabs(sub(bb, acc));
+  };
+  auto residual_cell = [&](const double *w, int64_t tt) -> double {
+    return residual_from(w, tt, *(S.at(PA2, s, tt) + q), *(S.at(PA1, s, tt) + q),
+                         *(S.at(PE, s, tt) + q), *(S.at(PC1, s, tt) + q), *(S.at(PC2, s, tt) + q),
+                         *(S.at(PB, s, tt) + q));
   };
 
   auto block_max = [&](double v) -> double {
@@ -216,13 +293,10 @@ __global__ void sip_wave_kernel(const double *__restrict__ a2p, const double *__
 
   // initial residual of x0 (iterative.py:279-283)
   double rloc = 0.0;
-  {
-    // fill the window slice by slice: slice t needs t-1, t, t+1
-    for (int64_t t = 0; t < T + 1; ++t) {
-      if (t < T) xn[(int)(t % 4) * m + q] = valid_cell(t) ? *(S.at(PXA, s, t) + q) : 0.0;
-      __syncthreads();
-      if (t >= 1 && valid_cell(t - 1)) rloc = nan_max(rloc, residual_cell(S, xn, t - 1));
-    }
+  for (int64_t t = 0; t < T + 1; ++t) {
+    if (t < T) xn[(int)(t % 4) * m + q] = valid_cell(t) ? *(S.at(PXA, s, t) + q) : 0.0;
+    __syncthreads();
+    if (t >= 1 && valid_cell(t - 1)) rloc = nan_max(rloc, residual_cell(xn, t - 1));
   }
   double r = block_max(rloc);
   const double r0 = r;
@@ -253,52 +327,77 @@ __global__ void sip_wave_kernel(const double *__restrict__ a2p, const double *__
     }
     const int xo = XP[cur], xw = XP[nxt];
     // ---- forward: newRHS = K x + b, then L y = newRHS (iterative.py:293-294)
+    // ring rows per step t: K (7), b, l1, l2 at slice t; x_old at slice t+1
+    const int fpl[NPL] = {PK0, PKN1, PKP1, PKNM, PKPM, PKNQ, PKPQ, PB, PL1, PL2, xo};
+    const int fslot[NPL] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10};
+    auto issue_fwd = [&](int64_t t) {
+      int64_t sl[NPL];
+      for (int j = 0; j < NPL - 1; ++j) sl[j] = t;
+      sl[NPL - 1] = t + 1;
+      issue_rows(fpl, sl, NPL, fslot);
+    };
+    if (q == 0)
+      for (int64_t t = 0; t < nst - 1 && t < T; ++t) issue_fwd(t);
     xs[0 * m + q] = valid_cell(0) ? *(S.at(xo, s, 0) + q) : 0.0;
     double y_u = 0.0;  // own column, previous cell
     for (int64_t t = 0; t < T; ++t) {
-      if (t + 1 < T) xs[(int)((t + 1) % 4) * m + q] = valid_cell(t + 1) ? *(S.at(xo, s, t + 1) + q) : 0.0;
+      const int stg = wait_stage();
+      if (t + 1 < T) xs[(int)((t + 1) % 4) * m + q] = valid_cell(t + 1) ? R_(stg, 10)[q] : 0.0;
       __syncthreads();
+      if (q == 0 && t + nst - 1 < T) issue_fwd(t + nst - 1);
       if (valid_cell(t)) {
         const int64_t p = t - q, i = p * m + q;
         auto X = [&](int64_t sl, int col) { return xs[(int)(((sl % 4) + 4) % 4) * m + col]; };
-        double acc = add(0.0, mul(*(S.at(PK0, s, t) + q), X(t, q)));
+        double acc = add(0.0, mul(R_(stg, 0)[q], X(t, q)));
         if (i >= 1) {
-          if (q >= 1) acc = add(acc, mul(*(S.at(PKN1, s, t) + q), X(t - 1, q - 1)));
-          else if (m == 2) acc = add(acc, mul(*(S.at(PKN1, s, t) + q), X(t, q + 1)));
+          if (q >= 1) acc = add(acc, mul(R_(stg, 1)[q], X(t - 1, q - 1)));
+          else if (m == 2) acc = add(acc, mul(R_(stg, 1)[q], X(t, q + 1)));
         }
         if (i <= n - 2) {
-          if (q <= m - 2) acc = add(acc, mul(*(S.at(PKP1, s, t) + q), X(t + 1, q + 1)));
-          else if (m == 2) acc = add(acc, mul(*(S.at(PKP1, s, t) + q), X(t, q - 1)));
+          if (q <= m - 2) acc = add(acc, mul(R_(stg, 2)[q], X(t + 1, q + 1)));
+          else if (m == 2) acc = add(acc, mul(R_(stg, 2)[q], X(t, q - 1)));
         }
-        if (i >= m) acc = add(acc, mul(*(S.at(PKNM, s, t) + q), X(t - 1, q)));
-        if (i + m <= n - 1) acc = add(acc, mul(*(S.at(PKPM, s, t) + q), X(t + 1, q)));
+        if (i >= m) acc = add(acc, mul(R_(stg, 3)[q], X(t - 1, q)));
+        if (i + m <= n - 1) acc = add(acc, mul(R_(stg, 4)[q], X(t + 1, q)));
         if (m != 2) {
-          if (i >= m - 1 && q <= m - 2 && p >= 1)
-            acc = add(acc, mul(*(S.at(PKNQ, s, t) + q), X(t, q + 1)));
-          if (i + m - 1 <= n - 1 && q >= 1)
-            acc = add(acc, mul(*(S.at(PKPQ, s, t) + q), X(t, q - 1)));
+          if (i >= m - 1 && q <= m - 2 && p >= 1) acc = add(acc, mul(R_(stg, 5)[q], X(t, q + 1)));
+          if (i + m - 1 <= n - 1 && q >= 1) acc = add(acc, mul(R_(stg, 6)[q], X(t, q - 1)));
         }
-        const double v = add(acc, *(S.at(PB, s, t) + q));
+        const double v = add(acc, R_(stg, 7)[q]);
         double y = v;
-        if (i >= 1 && q >= 1) y = sub(y, mul(*(S.at(PL1, s, t) + q), ys[(int)((t + 2) % 3) * m + q - 1]));
-        if (i >= m) y = sub(y, mul(*(S.at(PL2, s, t) + q), y_u));
+        if (i >= 1 && q >= 1) y = sub(y, mul(R_(stg, 8)[q], ys[(int)((t + 2) % 3) * m + q - 1]));
+        if (i >= m) y = sub(y, mul(R_(stg, 9)[q], y_u));
         *(S.at(PY, s, t) + q) = y;
         ys[(int)(t % 3) * m + q] = y;
         y_u = y;
       }
     }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // y rows -> TMA reads below
     __syncthreads();
     // ---- backward U x = y (iterative.py:295) + fused residual (296-297)
+    // ring rows per step (t = T-1-j): y, phi, psi, mu at t; A (5), b at t+1
+    const int bpl[10] = {PY, PPHI, PPSI, PMU, PA2, PA1, PE, PC1, PC2, PB};
+    const int bslot[10] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9};
+    auto issue_bwd = [&](int64_t t) {
+      int64_t sl[10];
+      for (int j = 0; j < 4; ++j) sl[j] = t;
+      for (int j = 4; j < 10; ++j) sl[j] = t + 1;
+      issue_rows(bpl, sl, 10, bslot);
+    };
+    if (q == 0)
+      for (int64_t j = 0; j < nst - 1 && j <= T; ++j) issue_bwd(T - 1 - j);
     double x_d = 0.0;  // own column, next cell (p+1, q)
     rloc = 0.0;
-    for (int64_t t = T - 1; t >= -1; --t) {
+    for (int64_t j = 0; j <= T; ++j) {
+      const int64_t t = T - 1 - j;
+      const int stg = wait_stage();
       if (t >= 0 && valid_cell(t)) {
         const int64_t p = t - q, i = p * m + q;
-        double v = *(S.at(PY, s, t) + q);
+        double v = R_(stg, 0)[q];
         if (i <= n - 2 && q <= m - 2)
-          v = sub(v, mul(*(S.at(PPHI, s, t) + q), xn[(int)((t + 1) % 4) * m + q + 1]));
-        if (i + m <= n - 1) v = sub(v, mul(*(S.at(PPSI, s, t) + q), x_d));
-        const double xv = dvd(v, *(S.at(PMU, s, t) + q));
+          v = sub(v, mul(R_(stg, 1)[q], xn[(int)((t + 1) % 4) * m + q + 1]));
+        if (i + m <= n - 1) v = sub(v, mul(R_(stg, 2)[q], x_d));
+        const double xv = dvd(v, R_(stg, 3)[q]);
         *(S.at(xw, s, t) + q) = xv;
         xn[(int)(t % 4) * m + q] = xv;
         x_d = xv;
@@ -306,8 +405,12 @@ __global__ void sip_wave_kernel(const double *__restrict__ a2p, const double *__
         xn[(int)(t % 4) * m + q] = 0.0;
       }
       __syncthreads();
-      if (t + 1 <= T - 1 && valid_cell(t + 1)) rloc = nan_max(rloc, residual_cell(S, xn, t + 1));
+      if (q == 0 && j + nst - 1 <= T) issue_bwd(T - 1 - (j + nst - 1));
+      if (t + 1 <= T - 1 && valid_cell(t + 1))
+        rloc = nan_max(rloc, residual_from(xn, t + 1, R_(stg, 4)[q], R_(stg, 5)[q], R_(stg, 6)[q],
+                                           R_(stg, 7)[q], R_(stg, 8)[q], R_(stg, 9)[q]));
     }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // x rows -> next forward's TMA
     r = block_max(rloc);
     cur = nxt;
     ++k;
@@ -353,7 +456,7 @@ __global__ void grid_check_kernel(const double *__restrict__ a1p, const double *
 
 bool sip_is_grid(const double *a1, const double *c1, int64_t batch, int64_t n, int64_t m,
                  int64_t ld, int layout, cudaStream_t stream) {
-  if (m < 2 || n % m != 0 || m > 1024) return false;
+  if (m < 2 || n % m != 0 || m > 512) return false;
   int *flag = nullptr;
   if (cudaMallocAsync((void **)&flag, sizeof(int), stream) != cudaSuccess) return false;
   cudaMemsetAsync(flag, 0, sizeof(int), stream);
@@ -370,10 +473,12 @@ bool sip_is_grid(const double *a1, const double *c1, int64_t batch, int64_t n, i
   return h == 0;
 }
 
+static int64_t sipw_mp(int64_t m) { return (m + 1) & ~(int64_t)1; }
+
 size_t sip_wave_workspace_bytes(int64_t batch, int64_t n, int64_t m) {
   if (m < 2 || n % m) return 0;
   const int64_t T = n / m + m - 1;
-  return sizeof(double) * (size_t)sipw::kPlanes * (size_t)batch * (size_t)T * (size_t)m;
+  return sizeof(double) * (size_t)sipw::kPlanes * (size_t)batch * (size_t)T * (size_t)sipw_mp(m) + 256;
 }
 
 int sip_wave(const double *a2, const double *a1, const double *e, const double *c1,
@@ -381,25 +486,38 @@ int sip_wave(const double *a2, const double *a1, const double *e, const double *
              int64_t *iters, double *res, double *best_res, int32_t *st, int32_t *ix,
              double *hist, double *ws, int64_t batch, int64_t n, int64_t m, double alpha,
              int64_t max_iter, int use_x0, int64_t ld, int layout, cudaStream_t stream) {
-  if (n % m != 0 || m > 1024) {
-    bxh::set_error("wavefront SIP needs n %% m == 0 and m <= 1024 (n=%lld, m=%lld)",
+  if (n % m != 0 || m > 512) {
+    bxh::set_error("wavefront SIP needs n %% m == 0 and m <= 512 (n=%lld, m=%lld)",
                    (long long)n, (long long)m);
     return BX_ERR_UNSUPPORTED;
   }
-  sipw::Skew S{ws, batch, m, n / m + m - 1};
-  const size_t smem = sizeof(double) * 11 * (size_t)m;
+  const int64_t mp = sipw_mp(m);
+  // workspace base 16-byte aligned for the TMA copies
+  double *base = (double *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  sipw::Skew S{base, batch, m, n / m + m - 1, mp};
+  // ring stages: as many as fit next to the 11 m window doubles (<= 4)
+  const size_t win = sizeof(double) * (size_t)(11 * m + 1);
+  const size_t stage = sizeof(double) * (size_t)sipw::NPL * (size_t)mp;
+  int nst = (int)((200 * 1024 - win) / stage);
+  if (nst > 4) nst = 4;
+  if (nst < 2) {
+    bxh::set_error("wavefront SIP: grid width m=%lld too large for the shared-memory ring",
+                   (long long)m);
+    return BX_ERR_UNSUPPORTED;
+  }
+  const size_t smem = win + stage * nst + sizeof(uint64_t) * nst + 16;
   if (layout == BX_LAYOUT_INTERLEAVED) {
     auto k = sipw::sip_wave_kernel<Interleaved>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)batch, (unsigned)m, smem, stream>>>(a2, a1, e, c1, c2, b, tol, x, best_x, iters,
                                                      res, best_res, st, ix, hist, S, n, alpha,
-                                                     max_iter, use_x0, Interleaved{ld});
+                                                     max_iter, use_x0, Interleaved{ld}, nst);
   } else {
     auto k = sipw::sip_wave_kernel<SystemMajor>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)batch, (unsigned)m, smem, stream>>>(a2, a1, e, c1, c2, b, tol, x, best_x, iters,
                                                      res, best_res, st, ix, hist, S, n, alpha,
-                                                     max_iter, use_x0, SystemMajor{ld});
+                                                     max_iter, use_x0, SystemMajor{ld}, nst);
   }
   return BX_OK;
 }
