@@ -225,27 +225,33 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
   asm volatile("fence.proxy.async.global;" ::: "memory");  // setup's plane writes -> TMA reads
   __syncthreads();
   unsigned g_issue = 0, g_use = 0;  // global sequence numbers of ring stages
-  // thread 0: queue the plane rows of one step into the next ring stage
+  // warp 0: queue the plane rows of one step into the next ring stage (lane j
+  // issues row j; lane 0 arms the stage's mbarrier with the total byte count)
   auto issue_rows = [&](const int *planes, const int64_t *slices, int cnt, const int *slots) {
     const int stg = (int)(g_issue % nst);
+    const int lane = q & 31;
+    const int width = m < 32 ? (int)m : 32;  // lanes present in warp 0
     unsigned bytes = 0;
-    int64_t c0s[NPL], c1s[NPL];
+    int64_t a_[NPL], b_[NPL];
     for (int j = 0; j < cnt; ++j) {
       const int64_t u = slices[j];
-      c0s[j] = c1s[j] = 0;
+      a_[j] = b_[j] = 0;
       if (u < 0 || u >= T) continue;
       const int64_t qlo = u - R + 1 > 0 ? u - R + 1 : 0, qhi = u < m - 1 ? u : m - 1;
       if (qlo > qhi) continue;
-      c0s[j] = qlo & ~(int64_t)1;
-      c1s[j] = (qhi + 2) & ~(int64_t)1;
-      bytes += (unsigned)((c1s[j] - c0s[j]) * sizeof(double));
+      a_[j] = qlo & ~(int64_t)1;
+      b_[j] = (qhi + 2) & ~(int64_t)1;
+      bytes += (unsigned)((b_[j] - a_[j]) * sizeof(double));
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect(bars + stg, bytes);
-    for (int j = 0; j < cnt; ++j)
-      if (c1s[j] > c0s[j])
-        bulk_g2s(R_(stg, slots[j]) + c0s[j], S.at(planes[j], s, slices[j]) + c0s[j],
-                 (unsigned)((c1s[j] - c0s[j]) * sizeof(double)), bars + stg);
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(bars + stg, bytes);
+    }
+    __syncwarp(width == 32 ? 0xffffffffu : ((1u << width) - 1u));
+    for (int j = lane; j < cnt; j += width)
+      if (b_[j] > a_[j])
+        bulk_g2s(R_(stg, slots[j]) + a_[j], S.at(planes[j], s, slices[j]) + a_[j],
+                 (unsigned)((b_[j] - a_[j]) * sizeof(double)), bars + stg);
     ++g_issue;
   };
   auto wait_stage = [&]() -> int {
@@ -293,10 +299,17 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
 
   // initial residual of x0 (iterative.py:279-283)
   double rloc = 0.0;
-  for (int64_t t = 0; t < T + 1; ++t) {
-    if (t < T) xn[(int)(t % 4) * m + q] = valid_cell(t) ? *(S.at(PXA, s, t) + q) : 0.0;
-    __syncthreads();
-    if (t >= 1 && valid_cell(t - 1)) rloc = nan_max(rloc, residual_cell(xn, t - 1));
+  if (!use_x0) {
+    // x0 = 0: every product of the sweep is a signed zero and 0 + (+-0) = +0,
+    // so b - A x0 == b exactly and r0 = max |b|
+    for (int64_t t = 0; t < T; ++t)
+      if (valid_cell(t)) rloc = nan_max(rloc, fabs(*(S.at(PB, s, t) + q)));
+  } else {
+    for (int64_t t = 0; t < T + 1; ++t) {
+      if (t < T) xn[(int)(t % 4) * m + q] = valid_cell(t) ? *(S.at(PXA, s, t) + q) : 0.0;
+      __syncthreads();
+      if (t >= 1 && valid_cell(t - 1)) rloc = nan_max(rloc, residual_cell(xn, t - 1));
+    }
   }
   double r = block_max(rloc);
   const double r0 = r;
@@ -336,7 +349,7 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
       sl[NPL - 1] = t + 1;
       issue_rows(fpl, sl, NPL, fslot);
     };
-    if (q == 0)
+    if (q < 32)
       for (int64_t t = 0; t < nst - 1 && t < T; ++t) issue_fwd(t);
     xs[0 * m + q] = valid_cell(0) ? *(S.at(xo, s, 0) + q) : 0.0;
     double y_u = 0.0;  // own column, previous cell
@@ -344,7 +357,7 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
       const int stg = wait_stage();
       if (t + 1 < T) xs[(int)((t + 1) % 4) * m + q] = valid_cell(t + 1) ? R_(stg, 10)[q] : 0.0;
       __syncthreads();
-      if (q == 0 && t + nst - 1 < T) issue_fwd(t + nst - 1);
+      if (q < 32 && t + nst - 1 < T) issue_fwd(t + nst - 1);
       if (valid_cell(t)) {
         const int64_t p = t - q, i = p * m + q;
         auto X = [&](int64_t sl, int col) { return xs[(int)(((sl % 4) + 4) % 4) * m + col]; };
@@ -384,7 +397,7 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
       for (int j = 4; j < 10; ++j) sl[j] = t + 1;
       issue_rows(bpl, sl, 10, bslot);
     };
-    if (q == 0)
+    if (q < 32)
       for (int64_t j = 0; j < nst - 1 && j <= T; ++j) issue_bwd(T - 1 - j);
     double x_d = 0.0;  // own column, next cell (p+1, q)
     rloc = 0.0;
@@ -405,7 +418,7 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
         xn[(int)(t % 4) * m + q] = 0.0;
       }
       __syncthreads();
-      if (q == 0 && j + nst - 1 <= T) issue_bwd(T - 1 - (j + nst - 1));
+      if (q < 32 && j + nst - 1 <= T) issue_bwd(T - 1 - (j + nst - 1));
       if (t + 1 <= T - 1 && valid_cell(t + 1))
         rloc = nan_max(rloc, residual_from(xn, t + 1, R_(stg, 4)[q], R_(stg, 5)[q], R_(stg, 6)[q],
                                            R_(stg, 7)[q], R_(stg, 8)[q], R_(stg, 9)[q]));
