@@ -188,9 +188,13 @@ __global__ void hb_residual_kernel(const double *__restrict__ Xa, const double *
     for (int64_t j = z0 + threadIdx.x; j < z1; j += blockDim.x) p[i * n + j] = 0.0;
   }
   for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    // X is triangular: entries of rows k1/k2 outside the triangle are zero by
+    // definition (and are never stored in the ping-pong buffers)
     double v = c0 * x[i * n + j];
-    if (c1 != 0.0) v = fma(c1, x[k1 * n + j], v);
-    if (c2 != 0.0) v = fma(c2, x[k2 * n + j], v);
+    const bool in1 = lower ? j <= k1 : j >= k1;
+    const bool in2 = lower ? j <= k2 : j >= k2;
+    if (c1 != 0.0 && in1) v = fma(c1, x[k1 * n + j], v);
+    if (c2 != 0.0 && in2) v = fma(c2, x[k2 * n + j], v);
     p[i * n + j] = v;
     rsum += fabs((i == j ? 1.0 : 0.0) - v);
   }
