@@ -158,6 +158,12 @@ static int hb_invert_all(HbWs &w, const double *tol_host, int64_t batch, int64_t
   std::vector<int> parity(F, 0), act, zd(F, 0x7fffffff);
   cudaMemcpyAsync(w.zd, zd.data(), sizeof(int) * F, cudaMemcpyHostToDevice, st);
   hb_init(w.Xa, w.fac + hbh::MU * pl, n, batch, w.zd, st);
+  // the GEMM only ever writes the triangle of X_next: clear the other triangle
+  // once so exported inverses (and any full-matrix read) see exact zeros
+  {
+    const int64_t np_ = hb_padded(n);
+    cudaMemsetAsync(w.Xb, 0, sizeof(double) * (size_t)F * np_ * np_, st);
+  }
   cudaMemcpyAsync(zd.data(), w.zd, sizeof(int) * F, cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
   for (int f = 0; f < F; ++f) {

@@ -224,40 +224,72 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.global;" ::: "memory");  // setup's plane writes -> TMA reads
   __syncthreads();
-  unsigned g_issue = 0, g_use = 0;  // global sequence numbers of ring stages
-  // warp 0: queue the plane rows of one step into the next ring stage (lane j
-  // issues row j; lane 0 arms the stage's mbarrier with the total byte count)
-  auto issue_rows = [&](const int *planes, const int64_t *slices, int cnt, const int *slots) {
-    const int stg = (int)(g_issue % nst);
-    const int lane = q & 31;
-    const int width = m < 32 ? (int)m : 32;  // lanes present in warp 0
-    unsigned bytes = 0;
-    int64_t a_[NPL], b_[NPL];
-    for (int j = 0; j < cnt; ++j) {
-      const int64_t u = slices[j];
-      a_[j] = b_[j] = 0;
-      if (u < 0 || u >= T) continue;
-      const int64_t qlo = u - R + 1 > 0 ? u - R + 1 : 0, qhi = u < m - 1 ? u : m - 1;
-      if (qlo > qhi) continue;
-      a_[j] = qlo & ~(int64_t)1;
-      b_[j] = (qhi + 2) & ~(int64_t)1;
-      bytes += (unsigned)((b_[j] - a_[j]) * sizeof(double));
+  // ring bookkeeping (identical in every thread): stage index + phase parity
+  int i_stg = 0, u_stg = 0;
+  unsigned u_par = 0;
+  const int lane = q & 31;
+  const int width = m < 32 ? (int)m : 32;  // lanes present in warp 0
+  const unsigned wmask = width == 32 ? 0xffffffffu : ((1u << width) - 1u);
+  // per phase, lane j of warp 0 owns plane row j: base pointer, slice offset, ring slot
+  const double *my_base = nullptr;
+  const int *rw_planes = nullptr, *rw_offs = nullptr;
+  int my_off = 0, my_cnt = 0;
+  auto set_rows = [&](const int *planes, const int *offs, int cnt) {
+    my_cnt = cnt;
+    rw_planes = planes;
+    rw_offs = offs;
+    if (lane < cnt) { my_base = S.at(planes[lane], s, 0); my_off = offs[lane]; }
+  };
+  // valid columns of slice u, widened to 16-byte alignment: [a0, a0 + nb/8)
+  auto span = [&](int u, int &a0, unsigned &nb) {
+    nb = 0;
+    a0 = 0;
+    if (u >= 0 && u < (int)T) {
+      const int qlo = u - (int)R + 1 > 0 ? u - (int)R + 1 : 0, qhi = u < (int)m - 1 ? u : (int)m - 1;
+      if (qlo <= qhi) {
+        a0 = qlo & ~1;
+        nb = (unsigned)(((qhi + 2) & ~1) - a0) * (unsigned)sizeof(double);
+      }
     }
-    if (lane == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect(bars + stg, bytes);
+  };
+  // warp 0: queue the rows of step slice tb (row j uses slice tb + off_j)
+  auto issue = [&](int tb) {
+    if (width >= my_cnt) {  // one row per lane
+      unsigned nb = 0;
+      int a0 = 0;
+      if (lane < my_cnt) span(tb + my_off, a0, nb);
+      const unsigned bytes = __reduce_add_sync(wmask, nb);
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect(bars + i_stg, bytes);
+      }
+      __syncwarp(wmask);
+      if (nb)
+        bulk_g2s(R_(i_stg, lane) + a0, my_base + (int64_t)(tb + my_off) * mp + a0, nb, bars + i_stg);
+    } else {  // narrow grids (m < rows per step): lanes loop over rows
+      unsigned bytes = 0, nb;
+      int a0;
+      for (int j = 0; j < my_cnt; ++j) {
+        span(tb + rw_offs[j], a0, nb);
+        bytes += nb;
+      }
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect(bars + i_stg, bytes);
+      }
+      __syncwarp(wmask);
+      for (int j = lane; j < my_cnt; j += width) {
+        const int u = tb + rw_offs[j];
+        span(u, a0, nb);
+        if (nb) bulk_g2s(R_(i_stg, j) + a0, S.at(rw_planes[j], s, u) + a0, nb, bars + i_stg);
+      }
     }
-    __syncwarp(width == 32 ? 0xffffffffu : ((1u << width) - 1u));
-    for (int j = lane; j < cnt; j += width)
-      if (b_[j] > a_[j])
-        bulk_g2s(R_(stg, slots[j]) + a_[j], S.at(planes[j], s, slices[j]) + a_[j],
-                 (unsigned)((b_[j] - a_[j]) * sizeof(double)), bars + stg);
-    ++g_issue;
+    i_stg = i_stg + 1 == nst ? 0 : i_stg + 1;
   };
   auto wait_stage = [&]() -> int {
-    const int stg = (int)(g_use % nst);
-    mbar_wait(bars + stg, (g_use / nst) & 1);
-    ++g_use;
+    const int stg = u_stg;
+    mbar_wait(bars + stg, u_par);
+    if (++u_stg == nst) { u_stg = 0; u_par ^= 1u; }
     return stg;
   };
 
@@ -342,22 +374,18 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
     // ---- forward: newRHS = K x + b, then L y = newRHS (iterative.py:293-294)
     // ring rows per step t: K (7), b, l1, l2 at slice t; x_old at slice t+1
     const int fpl[NPL] = {PK0, PKN1, PKP1, PKNM, PKPM, PKNQ, PKPQ, PB, PL1, PL2, xo};
-    const int fslot[NPL] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10};
-    auto issue_fwd = [&](int64_t t) {
-      int64_t sl[NPL];
-      for (int j = 0; j < NPL - 1; ++j) sl[j] = t;
-      sl[NPL - 1] = t + 1;
-      issue_rows(fpl, sl, NPL, fslot);
-    };
-    if (q < 32)
-      for (int64_t t = 0; t < nst - 1 && t < T; ++t) issue_fwd(t);
+    const int foff[NPL] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1};
+    if (q < 32) {
+      set_rows(fpl, foff, NPL);
+      for (int t = 0; t < nst - 1 && t < (int)T; ++t) issue(t);
+    }
     xs[0 * m + q] = valid_cell(0) ? *(S.at(xo, s, 0) + q) : 0.0;
     double y_u = 0.0;  // own column, previous cell
     for (int64_t t = 0; t < T; ++t) {
       const int stg = wait_stage();
       if (t + 1 < T) xs[(int)((t + 1) % 4) * m + q] = valid_cell(t + 1) ? R_(stg, 10)[q] : 0.0;
       __syncthreads();
-      if (q < 32 && t + nst - 1 < T) issue_fwd(t + nst - 1);
+      if (q < 32 && t + nst - 1 < T) issue((int)(t + nst - 1));
       if (valid_cell(t)) {
         const int64_t p = t - q, i = p * m + q;
         auto X = [&](int64_t sl, int col) { return xs[(int)(((sl % 4) + 4) % 4) * m + col]; };
@@ -390,15 +418,11 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
     // ---- backward U x = y (iterative.py:295) + fused residual (296-297)
     // ring rows per step (t = T-1-j): y, phi, psi, mu at t; A (5), b at t+1
     const int bpl[10] = {PY, PPHI, PPSI, PMU, PA2, PA1, PE, PC1, PC2, PB};
-    const int bslot[10] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9};
-    auto issue_bwd = [&](int64_t t) {
-      int64_t sl[10];
-      for (int j = 0; j < 4; ++j) sl[j] = t;
-      for (int j = 4; j < 10; ++j) sl[j] = t + 1;
-      issue_rows(bpl, sl, 10, bslot);
-    };
-    if (q < 32)
-      for (int64_t j = 0; j < nst - 1 && j <= T; ++j) issue_bwd(T - 1 - j);
+    const int boff[10] = {0, 0, 0, 0, 1, 1, 1, 1, 1, 1};
+    if (q < 32) {
+      set_rows(bpl, boff, 10);
+      for (int64_t j = 0; j < nst - 1 && j <= T; ++j) issue((int)(T - 1 - j));
+    }
     double x_d = 0.0;  // own column, next cell (p+1, q)
     rloc = 0.0;
     for (int64_t j = 0; j <= T; ++j) {
@@ -418,7 +442,7 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
         xn[(int)(t % 4) * m + q] = 0.0;
       }
       __syncthreads();
-      if (q < 32 && j + nst - 1 <= T) issue_bwd(T - 1 - (j + nst - 1));
+      if (q < 32 && j + nst - 1 <= T) issue((int)(T - 1 - (j + nst - 1)));
       if (t + 1 <= T - 1 && valid_cell(t + 1))
         rloc = nan_max(rloc, residual_from(xn, t + 1, R_(stg, 4)[q], R_(stg, 5)[q], R_(stg, 6)[q],
                                            R_(stg, 7)[q], R_(stg, 8)[q], R_(stg, 9)[q]));

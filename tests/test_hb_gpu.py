@@ -71,3 +71,22 @@ def test_dense_cap(cuda):
     p = W.five_point(1, 64, 2)
     with pytest.raises(DenseCapExceeded):
         sip_hb_solve(PentaMatrix.from_diagonals(*p[:5]), p[5], dense_cap=32)
+
+
+def test_hb_inverses_ignore_stale_workspace(cuda):
+    """A workspace full of NaN bytes (left by an earlier call) must not leak
+    into the exported inverses: the off-triangle is exactly zero."""
+    import torch
+    from paper_1804_09666_b200 import _lib
+    from paper_1804_09666_b200.core import workspace
+    m, n = 16, 384
+    p = W.five_point(2, n, m, seed=8)
+    tol = W.sip_tolerance(p[5])
+    ws = workspace(_lib.lib().bx_hb_workspace_bytes(2, n), torch.device("cuda", 0))
+    ws.fill_(0xFF)  # NaN pattern in every double
+    xl, xu, its, _, st, _ = hb_invert_factors(StencilMatrix.from_diagonals(*p[:5], m=m), tol,
+                                              alpha=0.5)
+    assert (host(st) == 0).all()
+    xl, xu = host(xl), host(xu)
+    assert np.all(np.isfinite(xl)) and np.all(np.isfinite(xu))
+    assert np.all(np.triu(xl, 1) == 0.0) and np.all(np.tril(xu, -1) == 0.0)
