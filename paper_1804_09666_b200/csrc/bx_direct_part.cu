@@ -35,13 +35,17 @@ namespace cg = cooperative_groups;
 
 #ifdef BX_TRACE
 // developer instrumentation (tools/trace_part.py): per-CTA phase clocks
-__device__ long long g_bx_trace[4096][10];
+__device__ long long g_bx_trace[4096][16];
 extern "C" int bx_trace_read(void *host, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(host, g_bx_trace, bytes < sizeof(g_bx_trace) ? bytes : sizeof(g_bx_trace));
 }
-#define BX_TR(slot)                                                                 \
-  do {                                                                              \
-    if (threadIdx.x == 0 && blockIdx.x < 4096) g_bx_trace[blockIdx.x][slot] = clock64(); \
+#ifndef BX_TRACE_BASE
+#define BX_TRACE_BASE 0
+#endif
+#define BX_TR(slot)                                                                  \
+  do {                                                                               \
+    const unsigned tb_ = blockIdx.x - BX_TRACE_BASE;                                 \
+    if (threadIdx.x == 0 && tb_ < 4096) g_bx_trace[tb_][slot] = clock64();           \
   } while (0)
 #else
 #define BX_TR(slot) \
@@ -225,6 +229,10 @@ __device__ __forceinline__ double pow2_inv_scale(double a) {
   return __hiloint2double((2046 - ex) << 20, 0);
 }
 
+__device__ __forceinline__ unsigned smem_addr(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
 // 32-byte vector global accesses (LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100a);
 // streaming: no L1 allocation for data that is touched once
 __device__ __forceinline__ void ld4(const double *p, double *o) {
@@ -280,7 +288,16 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   const int64_t seg0 = (int64_t)crank * (T * M);
   const int64_t base = seg0 + (int64_t)t * M;
   auto st = [&](int q, int j) -> double & { return state[(q * M + j) * T + t]; };
-  if (t == 0) misc[0] = 0;
+  // misc: [0] nz counter (int), [1] cluster mbarrier (8-byte slot)
+  uint64_t *cbar = reinterpret_cast<uint64_t *>(misc + 2);
+  if (t == 0) {
+    misc[0] = 0;
+    if (csize > 1) {
+      // receives the (csize - 1) peer roots pushed with st.async
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(cbar)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
   if (csize > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
   BX_TR(0);
@@ -337,10 +354,10 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     // warm L2 with this CTA's whole segment of one array per thread (TMA bulk
     // prefetch, no registers): the per-group loads below then see L2, not
     // HBM, latency.  Bytes are still fetched from HBM exactly once.
-    const double *arr[6] = {bp, ep, c1p, f1p, c2p, f2p};
+    const double *arr = t == 0 ? bp : t == 1 ? ep : t == 2 ? c1p : t == 3 ? f1p : t == 4 ? c2p : f2p;
     const int64_t rows = min((int64_t)(T * M), n - seg0) & ~(int64_t)1;
     if (rows > 0) {
-      const double *src = arr[t] + lay(seg0, s);
+      const double *src = arr + lay(seg0, s);
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src),
                    "r"((unsigned)(rows * sizeof(double)))
                    : "memory");
@@ -522,38 +539,81 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   Vec<K> Lseg, Rseg;
 #pragma unroll
   for (int k = 0; k < K; ++k) Lseg.v[k] = Rseg.v[k] = 0.0;
-  if (csize > 1) {
-    cg::cluster_group cl = cg::this_cluster();
-    // every CTA pushes its segment root into slot [crank] of every CTA of the
-    // cluster (DSMEM stores), then one cluster barrier; afterwards all reads
-    // are local, so no second barrier is needed before exit
-    __syncthreads();  // wport[0] (written by warp 0) visible to the pushing lanes
+  if (csize > 1 && warp == 0) {
+    // every CTA pushes its segment root (wport[0], written by lane 0 above)
+    // into slot [crank] of every peer with st.async, completing on the peer's
+    // mbarrier: no cluster-wide barrier, no generic-proxy fence, and warps
+    // 1..NW-1 never wait here.
+    constexpr int NR = (int)(sizeof(TwoPort<K>) / 8);
+    __syncwarp();
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // peers started (arrive at entry)
-    if (t < csize) *cl.map_shared_rank(&croots[crank], t) = wport[0];
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    if (t == 0) {
-      TwoPort<K> acc = croots[0];
-      MergeInfo<K> chain[8];
-      for (int r = 1; r < csize; ++r) {
-        TwoPort<K> m;
-        ok &= merge<K>(acc, croots[r], m, chain[r]);
-        acc = m;
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(cbar)),
+                   "r"((unsigned)((csize - 1) * NR * 8))
+                   : "memory");
+    if (lane < NR) {
+      const double v = reinterpret_cast<const double *>(wport)[lane];
+      double *slot = reinterpret_cast<double *>(&croots[crank]) + lane;
+      *slot = v;
+      const unsigned ls = smem_addr(slot), lb = smem_addr(cbar);
+      for (int r = 0; r < csize; ++r) {
+        if (r == crank) continue;
+        unsigned ra, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(ls), "r"(r));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(r));
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                     ::"r"(ra), "d"(v), "r"(rb)
+                     : "memory");
       }
-      Vec<K> L, R;
-#pragma unroll
-      for (int k = 0; k < K; ++k) L.v[k] = R.v[k] = 0.0;
-      bool found = false;
-      // node r merges [0..r-1] (left) with segment r (right)
-      for (int r = csize - 1; r >= 1 && !found; --r) {
-        const Vec<K> uu = apply<K>(chain[r].u, L, R);  // E of [0..r-1] = L of segment r
-        const Vec<K> vv = apply<K>(chain[r].v, L, R);  // F of segment r = R of [0..r-1]
-        if (r == crank) { Lseg = uu; Rseg = R; found = true; }
-        R = vv;
+    }
+    // wait for the peers' roots (phase 0 of the mbarrier)
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra W_%=;\n}" ::"r"(smem_addr(cbar))
+        : "memory");
+    __syncwarp();
+    if (lane == 0) {
+      // segments left (P) and right (Q) of this one, merged in order; then
+      // the three-segment system P | S | Q with L = R = 0 at the ends
+      const TwoPort<K> S = croots[crank];
+      TwoPort<K> P, Q, m;
+      MergeInfo<K> mi;
+      const bool hasP = crank > 0, hasQ = crank < csize - 1;
+      if (hasP) {
+        P = croots[0];
+        for (int r = 1; r < crank; ++r) { ok &= merge<K>(P, croots[r], m, mi); P = m; }
       }
-      if (!found) { Lseg = L; Rseg = R; }
+      if (hasQ) {
+        Q = croots[crank + 1];
+        for (int r = crank + 2; r < csize; ++r) { ok &= merge<K>(Q, croots[r], m, mi); Q = m; }
+      }
+      if (hasP && hasQ) {
+        MergeInfo<K> m1, m2;
+        TwoPort<K> PS, PSQ;
+        ok &= merge<K>(P, S, PS, m1);
+        ok &= merge<K>(PS, Q, PSQ, m2);
+        Rseg = m2.v.g;                      // F of Q with root L = R = 0
+        Lseg = vadd<K>(m1.u.g, mv<K>(m1.u.B, Rseg));  // E of P given R(PS) = F of Q
+      } else if (hasQ) {
+        ok &= merge<K>(S, Q, m, mi);
+        Rseg = mi.v.g;
+      } else {
+        ok &= merge<K>(P, S, m, mi);
+        Lseg = mi.u.g;
+      }
     }
   }
 
+#ifdef BX_TRACE
+  {  // make the clock wait for the cluster-level results
+    double d0, d1;
+    asm volatile("mov.b64 %0, %1;" : "=d"(d0) : "d"(Lseg.v[0]));
+    asm volatile("mov.b64 %0, %1;" : "=d"(d1) : "d"(Rseg.v[0]));
+    if (d0 == 1.2345e300 && d1 == 1.2345e300) misc[1] = 1;
+  }
+#endif
   BX_TR(5);
   // ---------------- tree descent -------------------------------------------
   if (warp == 0) {
@@ -585,7 +645,9 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
       for (int k = 0; k < K; ++k) { wlr[lane * 2 * K + k] = L.v[k]; wlr[lane * 2 * K + K + k] = R.v[k]; }
     }
   }
+  BX_TR(10);
   __syncthreads();
+  BX_TR(11);
   Vec<K> L, R;
 #pragma unroll
   for (int k = 0; k < K; ++k) { L.v[k] = wlr[warp * 2 * K + k]; R.v[k] = wlr[warp * 2 * K + K + k]; }
@@ -637,11 +699,11 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     if (index && bad >= 0) atomicMin(reinterpret_cast<unsigned int *>(index + s), (unsigned int)bad);
   }
 #ifdef BX_TRACE
-  if (threadIdx.x == 0 && blockIdx.x < 4096) {
+  if (threadIdx.x == 0 && blockIdx.x - BX_TRACE_BASE < 4096u) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    g_bx_trace[blockIdx.x][8] = clock64();
-    g_bx_trace[blockIdx.x][9] = smid;
+    g_bx_trace[blockIdx.x - BX_TRACE_BASE][8] = clock64();
+    g_bx_trace[blockIdx.x - BX_TRACE_BASE][9] = smid;
   }
 #endif
   if (K == 2 && nz_out) {

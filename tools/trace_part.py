@@ -20,7 +20,8 @@ objs = []
 for src in B.sources():
     o = os.path.join(out, os.path.basename(src) + ".o")
     subprocess.run([B.nvcc(), *B.ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", B.INCLUDE,
-                    "-I", B.CSRC, "-DBX_TRACE", "-c", src, "-o", o], check=True)
+                    "-I", B.CSRC, "-DBX_TRACE",
+                    "-DBX_TRACE_BASE=" + os.environ.get("BX_TRACE_BASE", "0"), "-c", src, "-o", o], check=True)
     objs.append(o)
 lib = os.path.join(out, "libbxtrace.so")
 subprocess.run([B.nvcc(), *B.ARCH, "-shared", "-o", lib, *objs, "-lcudart"], check=True)
@@ -47,7 +48,7 @@ for _ in range(3):
         rc = L.bx_npdm_f64(*(p(a) for a in arrs), p(x), p(st), p(ix), batch, n, n, 1, 1, None, 0, s)
     assert rc == 0, L.bx_last_error()
 torch.cuda.synchronize()
-buf = np.zeros((4096, 10), dtype=np.int64)
+buf = np.zeros((4096, 16), dtype=np.int64)
 L.bx_trace_read(buf.ctypes.data, buf.nbytes)
 names = ["down", "up", "port+warp-asc", "xwarp-asc", "cluster", "descent", "phase3", "status"]
 d = np.diff(buf[:, :9], axis=1)
@@ -55,5 +56,27 @@ ok = buf[:, 0] > 0
 print(f"K={k} n={n} B={batch} cfg={os.environ.get('BX_PART_CFG', 'auto')} CTAs traced={ok.sum()}")
 for j, nm in enumerate(names):
     print(f"  {nm:10s} median {np.median(d[ok, j]):9.0f} cyc   p90 {np.percentile(d[ok, j], 90):9.0f}")
+for nm, a, b in (("desc:xwarp", 5, 10), ("desc:sync", 10, 11), ("desc:inwarp", 11, 6)):
+    dd = buf[ok, b] - buf[ok, a]
+    print(f"  {nm:10s} median {np.median(dd):9.0f} cyc   p90 {np.percentile(dd, 90):9.0f}")
 tot = buf[ok, 8] - buf[ok, 0]
 print(f"  total      median {np.median(tot):9.0f} cyc   p90 {np.percentile(tot, 90):9.0f}")
+# per-SM occupancy of the memory phase: fraction of the traced window during
+# which at least one resident CTA of that SM is in its down (load) pass
+fr = []
+for sm in np.unique(buf[ok, 9]):
+    sel = ok & (buf[:, 9] == sm)
+    iv = sorted(zip(buf[sel, 0], buf[sel, 1]))
+    lo, hi = buf[sel, 0].min(), buf[sel, 8].max()
+    cov, cs, ce = 0, None, None
+    for a, b in iv:
+        if cs is None or a > ce:
+            if cs is not None:
+                cov += ce - cs
+            cs, ce = a, b
+        else:
+            ce = max(ce, b)
+    cov += ce - cs
+    fr.append(cov / max(1, hi - lo))
+print(f"  SMs {len(fr)}: down-pass coverage median {np.median(fr):.2f}  "
+      f"CTAs/SM median {np.median(np.bincount(buf[ok, 9].astype(int))[np.unique(buf[ok, 9]).astype(int)]):.0f}")
