@@ -58,6 +58,34 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def load_traffic(args):
+    """DRAM bytes per launch of the dominant kernel from the committed
+    `ncu --set full` capture summary (profiles/traffic.json), if present."""
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        key = args.workload if args.workload != "npdm" or args.algo == "partitioned" else "npdm_seq"
+        return t.get(key)
+    except Exception:
+        return None
+
+
+def pcie_h2d_gbs(dev, nbytes=1 << 29, reps=3):
+    """Pinned host -> device copy bandwidth on this box (the e2e ceiling)."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        d.copy_(h, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    return nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
 
@@ -242,6 +270,8 @@ class Direct:
             from paper_1804_09666_b200.pipeline import HostPipeline
             self.pipe = HostPipeline(self.solver, self.n, max(1, self.batch // 8), self.x.device,
                                      algo=self.args.algo)
+            self.e2e_path = ("pinned host -> bx C ABI per chunk -> pinned host x (system-major: "
+                             "8 chunks, H2D / solve / D2H overlapped on 3 streams, pipeline.py)")
         else:
             self.d_e2e = [torch.empty_like(t) for t in self.d_in]
             self.x_e2e = torch.empty_like(self.x)
@@ -749,7 +779,12 @@ def run_ours(args):
     value = wl.units * world * args.steps / elapsed
     peak, peak_src = load_peaks()
     roof = wl.roofline(mean_launch, peak)
-    roof.update(mean_launch_ms=1e3 * mean_launch, peak_source=peak_src)
+    roof["mean_launch_ms"] = 1e3 * mean_launch
+    roof.setdefault("peak_source", peak_src)
+    traffic = load_traffic(args)
+    if traffic is not None:
+        roof["traffic"] = traffic["bytes_per_launch"]
+        roof["traffic_source"] = traffic["source"]
 
     wl.e2e_prepare()
     for _ in range(max(1, min(args.warmup, 2))):
@@ -765,6 +800,7 @@ def run_ours(args):
     e2e_elapsed = max_over_ranks(e0.elapsed_time(e1) / 1e3)
     if args.workload not in ("hb",):
         assert torch.equal(wl.x_host, wl.x.cpu()), "e2e result differs from the resident run"
+    pcie = pcie_h2d_gbs(dev) if rank == 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -781,8 +817,11 @@ def run_ours(args):
             "data": "synthetic", "config": cfg, "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": wl.units * world * e2e_steps / e2e_elapsed, "unit": wl.unit,
                     "h2d_bytes_per_step": wl.h2d, "d2h_bytes_per_step": wl.d2h,
-                    "path": "pinned host -> cudaMemcpyAsync -> bx C ABI -> D2H x "
-                            "(system-major: 8 chunks pipelined on 3 streams, pipeline.py)"},
+                    "path": getattr(wl, "e2e_path", "pinned host -> H2D (cudaMemcpyAsync) -> bx C ABI "
+                                                     "-> D2H x, one stream"),
+                    "pcie_h2d_gbs_measured": pcie,
+                    "h2d_gbs_achieved": wl.h2d * e2e_steps / e2e_elapsed / 1e9,
+                    "pcie_frac": (wl.h2d * e2e_steps / e2e_elapsed / 1e9 / pcie) if pcie else None},
             "gpu_launches": args.steps * wl.launches_per_step,
             "clocks": clocks,
         }
