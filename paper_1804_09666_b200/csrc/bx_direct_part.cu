@@ -35,7 +35,7 @@ namespace cg = cooperative_groups;
 
 #ifdef BX_TRACE
 // developer instrumentation (tools/trace_part.py): per-CTA phase clocks
-__device__ long long g_bx_trace[4096][16];
+__device__ long long g_bx_trace[4096][24];
 extern "C" int bx_trace_read(void *host, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(host, g_bx_trace, bytes < sizeof(g_bx_trace) ? bytes : sizeof(g_bx_trace));
 }
@@ -270,7 +270,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
             const double *__restrict__ ep, const double *__restrict__ f1p,
             const double *__restrict__ f2p, const double *__restrict__ bp,
             double *__restrict__ xp, int32_t *status, int32_t *index, int64_t *nz_out,
-            int64_t batch, int64_t n, Lay lay, int csize) {
+            int64_t batch, int64_t n, Lay lay, int csize, int pf_ahead) {
   using SM = Smem<K, M, T>;
   constexpr int NW = SM::NW;
   static_assert(T % 32 == 0 && (NW & (NW - 1)) == 0, "T must be 32 * power of two");
@@ -350,14 +350,27 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
       }
     }
   };
-  if (VEC && t < (K == 2 ? 6 : 4)) {
-    // warm L2 with this CTA's whole segment of one array per thread (TMA bulk
-    // prefetch, no registers): the per-group loads below then see L2, not
-    // HBM, latency.  Bytes are still fetched from HBM exactly once.
-    const double *arr = t == 0 ? bp : t == 1 ? ep : t == 2 ? c1p : t == 3 ? f1p : t == 4 ? c2p : f2p;
-    const int64_t rows = min((int64_t)(T * M), n - seg0) & ~(int64_t)1;
-    if (rows > 0) {
-      const double *src = arr + lay(seg0, s);
+  constexpr int NA = K == 2 ? 6 : 4;  // input arrays
+  if (VEC && t < 2 * NA) {
+    // warm L2 (TMA bulk prefetch, no registers) with one array per thread of
+    // this CTA's segment (threads 0..NA-1) and of the segment of the CTA
+    // `pf_ahead` launches later (threads NA..2NA-1), which starts about one
+    // CTA lifetime from now on the SM this one frees: the HBM stream runs
+    // during the tree phases and the down pass sees L2, not HBM, latency.
+    // Every byte is still fetched from HBM once.
+    const int a = t % NA;
+    const double *arr = a == 0 ? bp : a == 1 ? ep : a == 2 ? c1p : a == 3 ? f1p : a == 4 ? c2p : f2p;
+    int64_t ss = s, sg = seg0;
+    bool go = true;
+    if (t >= NA) {
+      const int64_t b2 = (int64_t)blockIdx.x + pf_ahead;
+      go = pf_ahead > 0 && b2 < (int64_t)gridDim.x;
+      ss = b2 / csize;
+      sg = (b2 % csize) * (int64_t)(T * M);
+    }
+    const int64_t rows = min((int64_t)(T * M), n - sg) & ~(int64_t)1;
+    if (go && rows > 0) {
+      const double *src = arr + lay(sg, ss);
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src),
                    "r"((unsigned)(rows * sizeof(double)))
                    : "memory");
@@ -502,33 +515,35 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   for (int l = 0; l < 5; ++l) {
     const int step = 1 << l;
     const TwoPort<K> other = shfl_down_port<K>(port, step);
-    if ((lane & (2 * step - 1)) == 0) {
-      MergeInfo<K> mi;
-      TwoPort<K> m;
-      ok &= merge<K>(port, other, m, mi);
-      store_info<K, T>(info, warp * 31 + (32 - (32 >> l)) + (lane >> (l + 1)), mi);
-      port = m;
-    }
+    // divergence-free: every lane merges (inactive lanes discard), so the
+    // warp stays converged for the next level's shuffles; inactive lanes park
+    // their merge info in the spare node T-1
+    const bool act = (lane & (2 * step - 1)) == 0;
+    MergeInfo<K> mi;
+    TwoPort<K> m;
+    const bool okm = merge<K>(port, other, m, mi);
+    ok &= okm || !act;
+    store_info<K, T>(info, act ? warp * 31 + (32 - (32 >> l)) + (lane >> (l + 1)) : T - 1, mi);
+    if (act) port = m;
   }
   BX_TR(3);
   if (lane == 0) wport[warp] = port;
   __syncthreads();
   if (NW > 1 && warp == 0) {
     // levels over the NW warp ports (lanes 0..NW-1)
-    TwoPort<K> wp;
-    if (lane < NW) wp = wport[lane];
+    TwoPort<K> wp = wport[lane & (NW - 1)];
     int off = NW * 31;
 #pragma unroll 1
     for (int l = 0; (1 << l) < NW; ++l) {
       const int step = 1 << l;
       const TwoPort<K> other = shfl_down_port<K>(wp, step);
-      if (lane < NW && (lane & (2 * step - 1)) == 0) {
-        MergeInfo<K> mi;
-        TwoPort<K> m;
-        ok &= merge<K>(wp, other, m, mi);
-        store_info<K, T>(info, off + (lane >> (l + 1)), mi);
-        wp = m;
-      }
+      const bool act = lane < NW && (lane & (2 * step - 1)) == 0;
+      MergeInfo<K> mi;
+      TwoPort<K> m;
+      const bool okm = merge<K>(wp, other, m, mi);
+      ok &= okm || !act;
+      store_info<K, T>(info, act ? off + (lane >> (l + 1)) : T - 1, mi);
+      if (act) wp = m;
       off += NW >> (l + 1);
     }
     if (lane == 0) wport[0] = wp;
@@ -613,6 +628,8 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     asm volatile("mov.b64 %0, %1;" : "=d"(d1) : "d"(Rseg.v[0]));
     if (d0 == 1.2345e300 && d1 == 1.2345e300) misc[1] = 1;
   }
+  BX_TR(12);
+  __syncwarp();
 #endif
   BX_TR(5);
   // ---------------- tree descent -------------------------------------------
@@ -626,19 +643,20 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
       int offs[6];
       int off = NW * 31;
       for (int l = 0; l < nlev; ++l) { offs[l] = off; off += NW >> (l + 1); }
+      BX_TR(13);
       for (int l = nlev - 1; l >= 0; --l) {
         const int step = 1 << l;
         const bool act = lane < NW && (lane & (2 * step - 1)) == 0;
-        Vec<K> uu = L, vv = R;
-        if (act) {
-          const MergeInfo<K> mi = load_info<K, T>(info, offs[l] + (lane >> (l + 1)));
-          uu = apply<K>(mi.u, L, R);
-          vv = apply<K>(mi.v, L, R);
-        }
+        // divergence-free: every lane loads (broadcast) and applies, inactive
+        // lanes discard -- the shuffles below then find the warp converged
+        const MergeInfo<K> mi = load_info<K, T>(info, offs[l] + ((lane & (NW - 1)) >> (l + 1)));
+        Vec<K> uu = apply<K>(mi.u, L, R), vv = apply<K>(mi.v, L, R);
+        if (!act) { uu = L; vv = R; }
         const Vec<K> pu = shfl_up_vec<K>(uu, step), pR = shfl_up_vec<K>(R, step);
         if (lane < NW && (lane & (2 * step - 1)) == step) { L = pu; R = pR; }
         if (act) R = vv;
       }
+      BX_TR(15);
     }
     if (lane < NW) {
 #pragma unroll
@@ -655,12 +673,9 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   for (int l = 4; l >= 0; --l) {
     const int step = 1 << l;
     const bool act = (lane & (2 * step - 1)) == 0;
-    Vec<K> uu = L, vv = R;
-    if (act) {
-      const MergeInfo<K> mi = load_info<K, T>(info, warp * 31 + (32 - (32 >> l)) + (lane >> (l + 1)));
-      uu = apply<K>(mi.u, L, R);
-      vv = apply<K>(mi.v, L, R);
-    }
+    const MergeInfo<K> mi = load_info<K, T>(info, warp * 31 + (32 - (32 >> l)) + (lane >> (l + 1)));
+    Vec<K> uu = apply<K>(mi.u, L, R), vv = apply<K>(mi.v, L, R);
+    if (!act) { uu = L; vv = R; }
     const Vec<K> pu = shfl_up_vec<K>(uu, step), pR = shfl_up_vec<K>(R, step);
     if ((lane & (2 * step - 1)) == step) { L = pu; R = pR; }
     if (act) R = vv;
@@ -729,7 +744,10 @@ static int launch(const double *c2, const double *c1, const double *e, const dou
                    8 * rows);
     return BX_ERR_UNSUPPORTED;
   }
-  const size_t smem = Smem<K, M, T>::bytes;
+  size_t smem = Smem<K, M, T>::bytes;
+#ifdef BX_TRACE
+  if (getenv("BX_TRACE_SMEM")) smem = (size_t)atoi(getenv("BX_TRACE_SMEM"));  // occupancy experiments
+#endif
   auto kern = part_kernel<K, M, T, VEC, Lay>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (nz) cudaMemsetAsync(nz, 0, sizeof(int64_t) * (size_t)batch, stream);
@@ -747,8 +765,20 @@ static int launch(const double *c2, const double *c1, const double *e, const dou
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // CTAs resident at once (rounded to whole clusters): the launch distance
+  // at which a CTA's successor on the same SM slot starts
+  static int resident = -1;  // per configuration (template instance)
+  if (resident < 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
+    resident = per_sm * sms;
+  }
+  int pf_ahead = resident / csize * csize;
+  if (const char *env = getenv("BX_PART_PF")) pf_ahead = atoi(env);  // dev knob (0 = off)
   cudaError_t err = cudaLaunchKernelEx(&cfg, kern, c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n,
-                                       lay, csize);
+                                       lay, csize, pf_ahead);
   if (err != cudaSuccess) {
     bxh::set_error("partitioned solver launch: %s", cudaGetErrorString(err));
     return BX_ERR_CUDA;

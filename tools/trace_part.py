@@ -48,7 +48,7 @@ for _ in range(3):
         rc = L.bx_npdm_f64(*(p(a) for a in arrs), p(x), p(st), p(ix), batch, n, n, 1, 1, None, 0, s)
     assert rc == 0, L.bx_last_error()
 torch.cuda.synchronize()
-buf = np.zeros((4096, 16), dtype=np.int64)
+buf = np.zeros((4096, 24), dtype=np.int64)
 L.bx_trace_read(buf.ctypes.data, buf.nbytes)
 names = ["down", "up", "port+warp-asc", "xwarp-asc", "cluster", "descent", "phase3", "status"]
 d = np.diff(buf[:, :9], axis=1)
@@ -56,7 +56,7 @@ ok = buf[:, 0] > 0
 print(f"K={k} n={n} B={batch} cfg={os.environ.get('BX_PART_CFG', 'auto')} CTAs traced={ok.sum()}")
 for j, nm in enumerate(names):
     print(f"  {nm:10s} median {np.median(d[ok, j]):9.0f} cyc   p90 {np.percentile(d[ok, j], 90):9.0f}")
-for nm, a, b in (("desc:xwarp", 5, 10), ("desc:sync", 10, 11), ("desc:inwarp", 11, 6)):
+for nm, a, b in (("clu:lane0", 4, 12), ("clu:syncwarp", 12, 5), ("desc:xwarp", 5, 10), ("xw:offs", 5, 13), ("xw:levels", 13, 15), ("xw:wlr", 15, 10), ("desc:sync", 10, 11), ("desc:inwarp", 11, 6)):
     dd = buf[ok, b] - buf[ok, a]
     print(f"  {nm:10s} median {np.median(dd):9.0f} cyc   p90 {np.percentile(dd, 90):9.0f}")
 tot = buf[ok, 8] - buf[ok, 0]
