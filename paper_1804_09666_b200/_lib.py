@@ -12,7 +12,7 @@ import os
 from .errors import CudaError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbandix_b200.so")
+LIB_PATH = os.environ.get("BX_LIB") or os.path.join(_HERE, "libbandix_b200.so")  # BX_LIB: dev A/B
 
 BX_OK = 0
 LAYOUT_INTERLEAVED = 0

@@ -196,16 +196,26 @@ struct Cfg {
   static constexpr int Q = 1 + 2 * K;
 };
 
-// shared-memory layout (doubles): state[Q][M][T] | info[20][T] | wport[T/32] |
-// wlr[T/32][2K] | croots[8] (cluster roots, pushed by every CTA) | misc
+// shared-memory layout (doubles): state[Q][M][T] | info[20][T] | wport[T/4] |
+// wlr[T/4][2K] | croots[8] (cluster roots, pushed by every CTA) | misc
 template <int K, int M, int T>
 struct Smem {
   static constexpr int Q = Cfg<K>::Q;
   static constexpr int NW = T / 32;
   static constexpr int kState = Q * M * T;
   static constexpr int kInfo = T * (int)(sizeof(MergeInfo<K>) / 8);  // SoA, T nodes
-  static constexpr int kWPort = NW * (int)(sizeof(TwoPort<K>) / 8);
-  static constexpr int kWLR = NW * 2 * K;
+  // in-warp tree levels (all warps); the remaining NU nodes are reduced by
+  // warp 0.  K=2 merges are FP64-heavy: hand them to one warp early; K=1
+  // merges are cheap: stay warp-parallel longer.
+#ifndef BX_NLW2
+#define BX_NLW2 2
+#endif
+  static constexpr int NLW = K == 2 ? BX_NLW2 : 5;
+  static constexpr int NPW = 32 >> NLW;  // nodes per warp after the in-warp levels
+  static constexpr int NIW = 32 - NPW;   // merge nodes per warp (in-warp levels)
+  static constexpr int NU = NW * NPW;
+  static constexpr int kWPort = NU * (int)(sizeof(TwoPort<K>) / 8);
+  static constexpr int kWLR = NU * 2 * K;
   static constexpr int kRoots = 8 * (int)(sizeof(TwoPort<K>) / 8);
   static constexpr int kMisc = 8;
   static constexpr size_t bytes =
@@ -507,12 +517,17 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     }
   }
 
-  // ---------------- tree ascent: warp-synchronous, then across warps --------
-  // merge info for the in-warp levels: node (level l, index k) of warp w at
-  // info[w*31 + (32 - (32 >> l)) + k]; cross-warp nodes after NW*31.
+  // ---------------- tree ascent ---------------------------------------------
+  // Levels 0..NLW-1 inside every warp (shuffles), then warp 0 alone reduces
+  // the NU remaining nodes (shuffles again): for K=2 the upper levels then
+  // cost one warp's issue slots instead of every warp's, and the other warps
+  // leave the FP64 pipes to the co-resident CTA.  Merge-info nodes: in-warp
+  // level l of warp w at info[w*NIW + (32 - (32 >> l)) + k], upper levels
+  // after NW*NIW.
+  constexpr int NU = SM::NU, NLW = SM::NLW, NPW = SM::NPW, NIW = SM::NIW;
   bool ok = true;
 #pragma unroll 1
-  for (int l = 0; l < 5; ++l) {
+  for (int l = 0; l < NLW; ++l) {
     const int step = 1 << l;
     const TwoPort<K> other = shfl_down_port<K>(port, step);
     // divergence-free: every lane merges (inactive lanes discard), so the
@@ -523,28 +538,27 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     TwoPort<K> m;
     const bool okm = merge<K>(port, other, m, mi);
     ok &= okm || !act;
-    store_info<K, T>(info, act ? warp * 31 + (32 - (32 >> l)) + (lane >> (l + 1)) : T - 1, mi);
+    store_info<K, T>(info, act ? warp * NIW + (32 - (32 >> l)) + (lane >> (l + 1)) : T - 1, mi);
     if (act) port = m;
   }
   BX_TR(3);
-  if (lane == 0) wport[warp] = port;
+  if ((lane & ((1 << NLW) - 1)) == 0) wport[warp * NPW + (lane >> NLW)] = port;
   __syncthreads();
-  if (NW > 1 && warp == 0) {
-    // levels over the NW warp ports (lanes 0..NW-1)
-    TwoPort<K> wp = wport[lane & (NW - 1)];
-    int off = NW * 31;
+  if (warp == 0) {
+    TwoPort<K> wp = wport[lane & (NU - 1)];
+    int off = NW * NIW;
 #pragma unroll 1
-    for (int l = 0; (1 << l) < NW; ++l) {
+    for (int l = 0; (1 << l) < NU; ++l) {
       const int step = 1 << l;
       const TwoPort<K> other = shfl_down_port<K>(wp, step);
-      const bool act = lane < NW && (lane & (2 * step - 1)) == 0;
+      const bool act = lane < NU && (lane & (2 * step - 1)) == 0;
       MergeInfo<K> mi;
       TwoPort<K> m;
       const bool okm = merge<K>(wp, other, m, mi);
       ok &= okm || !act;
       store_info<K, T>(info, act ? off + (lane >> (l + 1)) : T - 1, mi);
       if (act) wp = m;
-      off += NW >> (l + 1);
+      off += NU >> (l + 1);
     }
     if (lane == 0) wport[0] = wp;
   }
@@ -634,31 +648,28 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   BX_TR(5);
   // ---------------- tree descent -------------------------------------------
   if (warp == 0) {
-    // root of the CTA (lane 0), then the cross-warp levels (lanes 0..NW-1)
+    // root of the CTA (lane 0), then the upper levels (lanes 0..NU-1)
     Vec<K> L = Lseg, R = Rseg;
-    if (NW > 1) {
-      int nlev = 0;
-      while ((1 << nlev) < NW) ++nlev;
-      // offsets of cross-warp levels
-      int offs[6];
-      int off = NW * 31;
-      for (int l = 0; l < nlev; ++l) { offs[l] = off; off += NW >> (l + 1); }
-      BX_TR(13);
-      for (int l = nlev - 1; l >= 0; --l) {
-        const int step = 1 << l;
-        const bool act = lane < NW && (lane & (2 * step - 1)) == 0;
-        // divergence-free: every lane loads (broadcast) and applies, inactive
-        // lanes discard -- the shuffles below then find the warp converged
-        const MergeInfo<K> mi = load_info<K, T>(info, offs[l] + ((lane & (NW - 1)) >> (l + 1)));
-        Vec<K> uu = apply<K>(mi.u, L, R), vv = apply<K>(mi.v, L, R);
-        if (!act) { uu = L; vv = R; }
-        const Vec<K> pu = shfl_up_vec<K>(uu, step), pR = shfl_up_vec<K>(R, step);
-        if (lane < NW && (lane & (2 * step - 1)) == step) { L = pu; R = pR; }
-        if (act) R = vv;
-      }
-      BX_TR(15);
+    constexpr int nlev = NU >= 32 ? 5 : NU >= 16 ? 4 : NU >= 8 ? 3 : NU >= 4 ? 2 : NU >= 2 ? 1 : 0;
+    int offs[nlev > 0 ? nlev : 1];
+    {
+      int off = NW * NIW;
+#pragma unroll
+      for (int l = 0; l < nlev; ++l) { offs[l] = off; off += NU >> (l + 1); }
     }
-    if (lane < NW) {
+#pragma unroll
+    for (int l = nlev - 1; l >= 0; --l) {
+      const int step = 1 << l;
+      const bool act = lane < NU && (lane & (2 * step - 1)) == 0;
+      // divergence-free: every lane loads and applies, inactive lanes discard
+      const MergeInfo<K> mi = load_info<K, T>(info, offs[l] + ((lane & (NU - 1)) >> (l + 1)));
+      Vec<K> uu = apply<K>(mi.u, L, R), vv = apply<K>(mi.v, L, R);
+      if (!act) { uu = L; vv = R; }
+      const Vec<K> pu = shfl_up_vec<K>(uu, step), pR = shfl_up_vec<K>(R, step);
+      if (lane < NU && (lane & (2 * step - 1)) == step) { L = pu; R = pR; }
+      if (act) R = vv;
+    }
+    if (lane < NU) {
 #pragma unroll
       for (int k = 0; k < K; ++k) { wlr[lane * 2 * K + k] = L.v[k]; wlr[lane * 2 * K + K + k] = R.v[k]; }
     }
@@ -667,13 +678,16 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   __syncthreads();
   BX_TR(11);
   Vec<K> L, R;
+  {
+    const int nd = warp * NPW + (lane >> NLW);  // this lane's node (used by lanes 2^NLW i)
 #pragma unroll
-  for (int k = 0; k < K; ++k) { L.v[k] = wlr[warp * 2 * K + k]; R.v[k] = wlr[warp * 2 * K + K + k]; }
+    for (int k = 0; k < K; ++k) { L.v[k] = wlr[nd * 2 * K + k]; R.v[k] = wlr[nd * 2 * K + K + k]; }
+  }
 #pragma unroll 1
-  for (int l = 4; l >= 0; --l) {
+  for (int l = NLW - 1; l >= 0; --l) {
     const int step = 1 << l;
     const bool act = (lane & (2 * step - 1)) == 0;
-    const MergeInfo<K> mi = load_info<K, T>(info, warp * 31 + (32 - (32 >> l)) + (lane >> (l + 1)));
+    const MergeInfo<K> mi = load_info<K, T>(info, warp * NIW + (32 - (32 >> l)) + (lane >> (l + 1)));
     Vec<K> uu = apply<K>(mi.u, L, R), vv = apply<K>(mi.v, L, R);
     if (!act) { uu = L; vv = R; }
     const Vec<K> pu = shfl_up_vec<K>(uu, step), pR = shfl_up_vec<K>(R, step);
