@@ -47,8 +47,11 @@ struct Skew {
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void mbar_init(uint64_t *bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_expect(uint64_t *bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
@@ -80,7 +83,7 @@ __device__ __forceinline__ double nan_max(double a, double b) {
 constexpr int NPL = 11;  // plane rows per ring stage
 
 template <class Lay>
-__global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
+__global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
                                 const double *__restrict__ ep, const double *__restrict__ c1p,
                                 const double *__restrict__ c2p, const double *__restrict__ bp,
                                 const double *__restrict__ tol, double *__restrict__ xout,
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
     double mu_u = 0, phi_u = 0, psi_u = 0;  // own column, previous cell (p-1, q)
     for (int64_t t = 0; t < T; ++t) {
       const int64_t p = t - q;
-      const bool valid = p >= 0 && p < R;
+      const bool valid = q < m && p >= 0 && p < R;
       if (valid) {
         const int64_t i = p * m + q;
         const double a2 = i >= m ? ldg(a2p + lay(i, s)) : 0.0;
@@ -213,92 +216,75 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
   double *xs = sh;          // [4][m] window of the previous iterate
   double *ys = sh + 4 * m;  // [3][m]
   double *xn = sh + 7 * m;  // [4][m] window of the new iterate
-  // ring of NST stages x NPL plane rows (padded stride mp), filled by TMA bulk copies
-  const int64_t mp = S.mp;
+  // ring of NST stages x NPL plane rows (padded stride mp), filled by TMA bulk
+  // copies that a dedicated producer warp issues; full[] completes on the
+  // copies' bytes, empty[] when every consumer warp has finished the stage
+  const int mp = (int)S.mp;
   double *ring = sh + 11 * m + (11 * m & 1);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(ring + (int64_t)nst * NPL * mp);
-  auto R_ = [&](int stage, int j) { return ring + ((int64_t)stage * NPL + j) * mp; };
-  auto valid_cell = [&](int64_t t) { const int64_t p = t - q; return p >= 0 && p < R; };
+  uint64_t *full = reinterpret_cast<uint64_t *>(ring + (int64_t)nst * NPL * mp);
+  uint64_t *empty = full + nst;
+  const int NCW = (int)((m + 31) / 32), NCT = NCW * 32;  // consumer warps / threads
+  const bool producer = q >= NCT;
+  const int lane = q & 31;
+  auto R_ = [&](int stage, int j) { return ring + (stage * NPL + j) * mp; };
+  auto valid_cell = [&](int64_t t) { const int64_t p = t - q; return q < m && p >= 0 && p < R; };
   if (q == 0)
-    for (int i = 0; i < nst; ++i) mbar_init(bars + i);
+    for (int i = 0; i < nst; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, NCW); }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.global;" ::: "memory");  // setup's plane writes -> TMA reads
   __syncthreads();
-  // ring bookkeeping (identical in every thread): stage index + phase parity
-  int i_stg = 0, u_stg = 0;
-  unsigned u_par = 0;
-  const int lane = q & 31;
-  const int width = m < 32 ? (int)m : 32;  // lanes present in warp 0
-  const unsigned wmask = width == 32 ? 0xffffffffu : ((1u << width) - 1u);
-  // per phase, lane j of warp 0 owns plane row j: base pointer, slice offset, ring slot
+  // ring bookkeeping: producer (issue side) and consumers (use side) walk the
+  // same stage sequence; parity flips at every wrap
+  int p_stg = 0, c_stg = 0;
+  unsigned p_par = 0, c_par = 0;
+  // producer lane j owns plane row j of the current phase: base, slice offset
   const double *my_base = nullptr;
-  const int *rw_planes = nullptr, *rw_offs = nullptr;
   int my_off = 0, my_cnt = 0;
   auto set_rows = [&](const int *planes, const int *offs, int cnt) {
     my_cnt = cnt;
-    rw_planes = planes;
-    rw_offs = offs;
     if (lane < cnt) { my_base = S.at(planes[lane], s, 0); my_off = offs[lane]; }
   };
-  // valid columns of slice u, widened to 16-byte alignment: [a0, a0 + nb/8)
-  auto span = [&](int u, int &a0, unsigned &nb) {
-    nb = 0;
-    a0 = 0;
-    if (u >= 0 && u < (int)T) {
+  // producer: wait until the consumers released the stage, then queue the
+  // rows of step slice tb (row j uses slice tb + off_j); valid columns only,
+  // widened to 16-byte alignment
+  auto produce = [&](int tb) {
+    mbar_wait(empty + p_stg, p_par ^ 1u);  // first round passes (fresh barrier)
+    unsigned nb = 0;
+    int a0 = 0;
+    const int u = tb + my_off;
+    if (lane < my_cnt && u >= 0 && u < (int)T) {
       const int qlo = u - (int)R + 1 > 0 ? u - (int)R + 1 : 0, qhi = u < (int)m - 1 ? u : (int)m - 1;
       if (qlo <= qhi) {
         a0 = qlo & ~1;
         nb = (unsigned)(((qhi + 2) & ~1) - a0) * (unsigned)sizeof(double);
       }
     }
+    const unsigned bytes = __reduce_add_sync(0xffffffffu, nb);
+    if (lane == 0) mbar_expect(full + p_stg, bytes);
+    __syncwarp();
+    if (nb) bulk_g2s(R_(p_stg, lane) + a0, my_base + (int64_t)u * mp + a0, nb, full + p_stg);
+    if (++p_stg == nst) { p_stg = 0; p_par ^= 1u; }
   };
-  // warp 0: queue the rows of step slice tb (row j uses slice tb + off_j)
-  auto issue = [&](int tb) {
-    if (width >= my_cnt) {  // one row per lane
-      unsigned nb = 0;
-      int a0 = 0;
-      if (lane < my_cnt) span(tb + my_off, a0, nb);
-      const unsigned bytes = __reduce_add_sync(wmask, nb);
-      if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect(bars + i_stg, bytes);
-      }
-      __syncwarp(wmask);
-      if (nb)
-        bulk_g2s(R_(i_stg, lane) + a0, my_base + (int64_t)(tb + my_off) * mp + a0, nb, bars + i_stg);
-    } else {  // narrow grids (m < rows per step): lanes loop over rows
-      unsigned bytes = 0, nb;
-      int a0;
-      for (int j = 0; j < my_cnt; ++j) {
-        span(tb + rw_offs[j], a0, nb);
-        bytes += nb;
-      }
-      if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect(bars + i_stg, bytes);
-      }
-      __syncwarp(wmask);
-      for (int j = lane; j < my_cnt; j += width) {
-        const int u = tb + rw_offs[j];
-        span(u, a0, nb);
-        if (nb) bulk_g2s(R_(i_stg, j) + a0, S.at(rw_planes[j], s, u) + a0, nb, bars + i_stg);
-      }
-    }
-    i_stg = i_stg + 1 == nst ? 0 : i_stg + 1;
-  };
-  auto wait_stage = [&]() -> int {
-    const int stg = u_stg;
-    mbar_wait(bars + stg, u_par);
-    if (++u_stg == nst) { u_stg = 0; u_par ^= 1u; }
+  auto consume_wait = [&]() -> int {
+    const int stg = c_stg;
+    mbar_wait(full + stg, c_par);
     return stg;
   };
+  auto consume_release = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + c_stg);
+    if (++c_stg == nst) { c_stg = 0; c_par ^= 1u; }
+  };
+  // consumer-only barrier (named barrier 1): the producer warp runs ahead
+  auto cons_sync = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(NCT) : "memory"); };
 
   // residual of cell (slice tt, column q) from a window w[4][m] of x slices
   // tt-1..tt+1 and the row's A/b values (iterative.py:213-221 order, acc from 0)
-  auto residual_from = [&](const double *w, int64_t tt, double a2, double a1, double e,
+  auto residual_from = [&](const double *w, int tt, double a2, double a1, double e,
                            double c1, double c2, double bb) -> double {
-    const int64_t p = tt - q, i = p * m + q;
-    auto X = [&](int64_t sl, int col) { return w[(int)(((sl % 4) + 4) % 4) * m + col]; };
+    const int p = tt - q;
+    const int64_t i = (int64_t)p * m + q;
+    auto X = [&](int sl, int col) { return w[(sl & 3) * (int)m + col]; };
     double acc = add(0.0, mul(e, X(tt, q)));
     if (i >= 1) {
       if (q >= 1) acc = add(acc, mul(a1, X(tt - 1, q - 1)));
@@ -308,12 +294,12 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
       if (q <= m - 2) acc = add(acc, mul(c1, X(tt + 1, q + 1)));
       else if (m == 2) acc = add(acc, mul(c1, X(tt, q - 1)));
     }
-    if (i >= m) acc = add(acc, mul(a2, X(tt - 1, q)));
-    if (i + m <= n - 1) acc = add(acc, mul(c2, X(tt + 1, q)));
+    if (p >= 1) acc = add(acc, mul(a2, X(tt - 1, q)));
+    if (p <= (int)R - 2) acc = add(acc, mul(c2, X(tt + 1, q)));
     return fabs(sub(bb, acc));
   };
   auto residual_cell = [&](const double *w, int64_t tt) -> double {
-    return residual_from(w, tt, *(S.at(PA2, s, tt) + q), *(S.at(PA1, s, tt) + q),
+    return residual_from(w, (int)tt, *(S.at(PA2, s, tt) + q), *(S.at(PA1, s, tt) + q),
                          *(S.at(PE, s, tt) + q), *(S.at(PC1, s, tt) + q), *(S.at(PC2, s, tt) + q),
                          *(S.at(PB, s, tt) + q));
   };
@@ -324,8 +310,7 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
     if ((q & 31) == 0) s_red[q >> 5] = v;
     __syncthreads();
     double r = 0.0;
-    const int nw = (int)((m + 31) / 32);
-    for (int w = 0; w < nw; ++w) r = nan_max(r, s_red[w]);
+    for (int w = 0; w < NCW; ++w) r = nan_max(r, s_red[w]);
     return r;
   };
 
@@ -338,7 +323,7 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
       if (valid_cell(t)) rloc = nan_max(rloc, fabs(*(S.at(PB, s, t) + q)));
   } else {
     for (int64_t t = 0; t < T + 1; ++t) {
-      if (t < T) xn[(int)(t % 4) * m + q] = valid_cell(t) ? *(S.at(PXA, s, t) + q) : 0.0;
+      if (t < T && q < m) xn[(int)(t % 4) * m + q] = valid_cell(t) ? *(S.at(PXA, s, t) + q) : 0.0;
       __syncthreads();
       if (t >= 1 && valid_cell(t - 1)) rloc = nan_max(rloc, residual_cell(xn, t - 1));
     }
@@ -351,6 +336,8 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
   int cur = 0, best_loc = 0;
   const double tl = tol[s];
   const int XP[3] = {PXA, PXB, PXBEST};
+  const int Ti = (int)T, Ri = (int)R, mi_ = (int)m;
+  const int p_hi = Ri - 2;  // cells with p <= p_hi have a +m neighbour
 
   while (true) {
     if (q == 0) {
@@ -369,85 +356,101 @@ __global__ void __launch_bounds__(512) sip_wave_kernel(const double *__restrict_
       for (int64_t t = 0; t < T; ++t)
         if (valid_cell(t)) *(S.at(PXBEST, s, t) + q) = *(S.at(XP[nxt], s, t) + q);
       best_loc = 2;
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __syncthreads();
     }
     const int xo = XP[cur], xw = XP[nxt];
     // ---- forward: newRHS = K x + b, then L y = newRHS (iterative.py:293-294)
     // ring rows per step t: K (7), b, l1, l2 at slice t; x_old at slice t+1
-    const int fpl[NPL] = {PK0, PKN1, PKP1, PKNM, PKPM, PKNQ, PKPQ, PB, PL1, PL2, xo};
-    const int foff[NPL] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1};
-    if (q < 32) {
+    if (producer) {
+      const int fpl[NPL] = {PK0, PKN1, PKP1, PKNM, PKPM, PKNQ, PKPQ, PB, PL1, PL2, xo};
+      const int foff[NPL] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1};
       set_rows(fpl, foff, NPL);
-      for (int t = 0; t < nst - 1 && t < (int)T; ++t) issue(t);
-    }
-    xs[0 * m + q] = valid_cell(0) ? *(S.at(xo, s, 0) + q) : 0.0;
-    double y_u = 0.0;  // own column, previous cell
-    for (int64_t t = 0; t < T; ++t) {
-      const int stg = wait_stage();
-      if (t + 1 < T) xs[(int)((t + 1) % 4) * m + q] = valid_cell(t + 1) ? R_(stg, 10)[q] : 0.0;
-      __syncthreads();
-      if (q < 32 && t + nst - 1 < T) issue((int)(t + nst - 1));
-      if (valid_cell(t)) {
-        const int64_t p = t - q, i = p * m + q;
-        auto X = [&](int64_t sl, int col) { return xs[(int)(((sl % 4) + 4) % 4) * m + col]; };
-        double acc = add(0.0, mul(R_(stg, 0)[q], X(t, q)));
-        if (i >= 1) {
-          if (q >= 1) acc = add(acc, mul(R_(stg, 1)[q], X(t - 1, q - 1)));
-          else if (m == 2) acc = add(acc, mul(R_(stg, 1)[q], X(t, q + 1)));
+      for (int t = 0; t < Ti; ++t) produce(t);
+    } else {
+      const bool live = q < m;
+      double *py = S.at(PY, s, 0) + q;
+      if (live) xs[q] = valid_cell(0) ? *(S.at(xo, s, 0) + q) : 0.0;
+      double y_u = 0.0;  // own column, previous cell
+      for (int t = 0; t < Ti; ++t) {
+        const int stg = consume_wait();
+        const double *rb = R_(stg, 0) + q;
+        if (live && t + 1 < Ti) {
+          const int p1 = t + 1 - q;
+          xs[((t + 1) & 3) * mi_ + q] = (p1 >= 0 && p1 < Ri) ? rb[10 * mp] : 0.0;
         }
-        if (i <= n - 2) {
-          if (q <= m - 2) acc = add(acc, mul(R_(stg, 2)[q], X(t + 1, q + 1)));
-          else if (m == 2) acc = add(acc, mul(R_(stg, 2)[q], X(t, q - 1)));
+        cons_sync();
+        const int p = t - q;
+        if (live && p >= 0 && p < Ri) {
+          const int64_t i = (int64_t)p * m + q;
+          auto X = [&](int sl, int col) { return xs[(sl & 3) * mi_ + col]; };
+          double acc = add(0.0, mul(rb[0], X(t, q)));
+          if (i >= 1) {
+            if (q >= 1) acc = add(acc, mul(rb[mp], X(t - 1, q - 1)));
+            else if (m == 2) acc = add(acc, mul(rb[mp], X(t, q + 1)));
+          }
+          if (i <= n - 2) {
+            if (q <= m - 2) acc = add(acc, mul(rb[2 * mp], X(t + 1, q + 1)));
+            else if (m == 2) acc = add(acc, mul(rb[2 * mp], X(t, q - 1)));
+          }
+          if (p >= 1) acc = add(acc, mul(rb[3 * mp], X(t - 1, q)));
+          if (p <= p_hi) acc = add(acc, mul(rb[4 * mp], X(t + 1, q)));
+          if (m != 2) {
+            if (i >= m - 1 && q <= m - 2 && p >= 1) acc = add(acc, mul(rb[5 * mp], X(t, q + 1)));
+            if (i + m - 1 <= n - 1 && q >= 1) acc = add(acc, mul(rb[6 * mp], X(t, q - 1)));
+          }
+          const double v = add(acc, rb[7 * mp]);
+          double y = v;
+          if (i >= 1 && q >= 1) y = sub(y, mul(rb[8 * mp], ys[((t + 2) % 3) * mi_ + q - 1]));
+          if (p >= 1) y = sub(y, mul(rb[9 * mp], y_u));
+          py[(int64_t)t * mp] = y;
+          ys[(t % 3) * mi_ + q] = y;
+          y_u = y;
         }
-        if (i >= m) acc = add(acc, mul(R_(stg, 3)[q], X(t - 1, q)));
-        if (i + m <= n - 1) acc = add(acc, mul(R_(stg, 4)[q], X(t + 1, q)));
-        if (m != 2) {
-          if (i >= m - 1 && q <= m - 2 && p >= 1) acc = add(acc, mul(R_(stg, 5)[q], X(t, q + 1)));
-          if (i + m - 1 <= n - 1 && q >= 1) acc = add(acc, mul(R_(stg, 6)[q], X(t, q - 1)));
-        }
-        const double v = add(acc, R_(stg, 7)[q]);
-        double y = v;
-        if (i >= 1 && q >= 1) y = sub(y, mul(R_(stg, 8)[q], ys[(int)((t + 2) % 3) * m + q - 1]));
-        if (i >= m) y = sub(y, mul(R_(stg, 9)[q], y_u));
-        *(S.at(PY, s, t) + q) = y;
-        ys[(int)(t % 3) * m + q] = y;
-        y_u = y;
+        consume_release();
       }
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // y rows -> TMA reads below
     }
-    asm volatile("fence.proxy.async.global;" ::: "memory");  // y rows -> TMA reads below
     __syncthreads();
     // ---- backward U x = y (iterative.py:295) + fused residual (296-297)
     // ring rows per step (t = T-1-j): y, phi, psi, mu at t; A (5), b at t+1
-    const int bpl[10] = {PY, PPHI, PPSI, PMU, PA2, PA1, PE, PC1, PC2, PB};
-    const int boff[10] = {0, 0, 0, 0, 1, 1, 1, 1, 1, 1};
-    if (q < 32) {
-      set_rows(bpl, boff, 10);
-      for (int64_t j = 0; j < nst - 1 && j <= T; ++j) issue((int)(T - 1 - j));
-    }
-    double x_d = 0.0;  // own column, next cell (p+1, q)
     rloc = 0.0;
-    for (int64_t j = 0; j <= T; ++j) {
-      const int64_t t = T - 1 - j;
-      const int stg = wait_stage();
-      if (t >= 0 && valid_cell(t)) {
-        const int64_t p = t - q, i = p * m + q;
-        double v = R_(stg, 0)[q];
-        if (i <= n - 2 && q <= m - 2)
-          v = sub(v, mul(R_(stg, 1)[q], xn[(int)((t + 1) % 4) * m + q + 1]));
-        if (i + m <= n - 1) v = sub(v, mul(R_(stg, 2)[q], x_d));
-        const double xv = dvd(v, R_(stg, 3)[q]);
-        *(S.at(xw, s, t) + q) = xv;
-        xn[(int)(t % 4) * m + q] = xv;
-        x_d = xv;
-      } else if (t >= 0) {
-        xn[(int)(t % 4) * m + q] = 0.0;
+    if (producer) {
+      const int bpl[10] = {PY, PPHI, PPSI, PMU, PA2, PA1, PE, PC1, PC2, PB};
+      const int boff[10] = {0, 0, 0, 0, 1, 1, 1, 1, 1, 1};
+      set_rows(bpl, boff, 10);
+      for (int j = 0; j <= Ti; ++j) produce(Ti - 1 - j);
+    } else {
+      const bool live = q < m;
+      double *px = S.at(xw, s, 0) + q;
+      double x_d = 0.0;  // own column, next cell (p+1, q)
+      for (int j = 0; j <= Ti; ++j) {
+        const int t = Ti - 1 - j;
+        const int stg = consume_wait();
+        const double *rb = R_(stg, 0) + q;
+        const int p = t - q;
+        if (live && t >= 0) {
+          if (p >= 0 && p < Ri) {
+            const int64_t i = (int64_t)p * m + q;
+            double v = rb[0];
+            if (i <= n - 2 && q <= m - 2) v = sub(v, mul(rb[mp], xn[((t + 1) & 3) * mi_ + q + 1]));
+            if (p <= p_hi) v = sub(v, mul(rb[2 * mp], x_d));
+            const double xv = dvd(v, rb[3 * mp]);
+            px[(int64_t)t * mp] = xv;
+            xn[(t & 3) * mi_ + q] = xv;
+            x_d = xv;
+          } else {
+            xn[(t & 3) * mi_ + q] = 0.0;
+          }
+        }
+        cons_sync();
+        if (live && t + 1 <= Ti - 1 && p + 1 >= 0 && p + 1 < Ri)
+          rloc = nan_max(rloc, residual_from(xn, t + 1, rb[4 * mp], rb[5 * mp], rb[6 * mp],
+                                             rb[7 * mp], rb[8 * mp], rb[9 * mp]));
+        consume_release();
       }
-      __syncthreads();
-      if (q < 32 && j + nst - 1 <= T) issue((int)(T - 1 - (j + nst - 1)));
-      if (t + 1 <= T - 1 && valid_cell(t + 1))
-        rloc = nan_max(rloc, residual_from(xn, t + 1, R_(stg, 4)[q], R_(stg, 5)[q], R_(stg, 6)[q],
-                                           R_(stg, 7)[q], R_(stg, 8)[q], R_(stg, 9)[q]));
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // x rows -> next forward's TMA
     }
-    asm volatile("fence.proxy.async.global;" ::: "memory");  // x rows -> next forward's TMA
     r = block_max(rloc);
     cur = nxt;
     ++k;
@@ -542,19 +545,21 @@ int sip_wave(const double *a2, const double *a1, const double *e, const double *
                    (long long)m);
     return BX_ERR_UNSUPPORTED;
   }
-  const size_t smem = win + stage * nst + sizeof(uint64_t) * nst + 16;
+  const size_t smem = win + stage * nst + sizeof(uint64_t) * 2 * nst + 16;
+  // consumer warps (one thread per grid column) + one TMA producer warp
+  const unsigned threads = (unsigned)(((m + 31) / 32) * 32 + 32);
   if (layout == BX_LAYOUT_INTERLEAVED) {
     auto k = sipw::sip_wave_kernel<Interleaved>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<(unsigned)batch, (unsigned)m, smem, stream>>>(a2, a1, e, c1, c2, b, tol, x, best_x, iters,
-                                                     res, best_res, st, ix, hist, S, n, alpha,
-                                                     max_iter, use_x0, Interleaved{ld}, nst);
+    k<<<(unsigned)batch, threads, smem, stream>>>(a2, a1, e, c1, c2, b, tol, x, best_x, iters,
+                                                 res, best_res, st, ix, hist, S, n, alpha,
+                                                 max_iter, use_x0, Interleaved{ld}, nst);
   } else {
     auto k = sipw::sip_wave_kernel<SystemMajor>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<(unsigned)batch, (unsigned)m, smem, stream>>>(a2, a1, e, c1, c2, b, tol, x, best_x, iters,
-                                                     res, best_res, st, ix, hist, S, n, alpha,
-                                                     max_iter, use_x0, SystemMajor{ld}, nst);
+    k<<<(unsigned)batch, threads, smem, stream>>>(a2, a1, e, c1, c2, b, tol, x, best_x, iters,
+                                                 res, best_res, st, ix, hist, S, n, alpha,
+                                                 max_iter, use_x0, SystemMajor{ld}, nst);
   }
   return BX_OK;
 }
