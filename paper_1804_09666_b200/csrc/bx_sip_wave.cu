@@ -21,9 +21,25 @@
 // converted once in the setup pass; iterations then stream the planes.
 //   reference: ilu0_penta / defect_matrix / sip_solve (iterative.py:62-308)
 #include <math.h>
+#include <stdlib.h>
 
 #include "bx_common.cuh"
 #include "bx_kernels.h"
+
+#ifdef BX_SIP_TRACE
+__device__ long long g_sip_trace[64][40];
+extern "C" int bx_sip_trace_read(void *host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, g_sip_trace, bytes < sizeof(g_sip_trace) ? bytes : sizeof(g_sip_trace));
+}
+#define SIP_TR(slot)                                                                      \
+  do {                                                                                    \
+    if (threadIdx.x == 0 && blockIdx.x < 64 && (slot) < 40) g_sip_trace[blockIdx.x][slot] = clock64(); \
+  } while (0)
+#else
+#define SIP_TR(slot) \
+  do {               \
+  } while (0)
+#endif
 
 namespace bx {
 namespace sipw {
@@ -35,11 +51,45 @@ enum Plane {
   PY, PXA, PXB, PXBEST, kPlanes
 };
 
+// Workspace of one system (doubles), laid out so that every wavefront step
+// streams two contiguous blocks:
+//   FG[t]  slice t, 10 rows of width W(t): K0 KN1 KP1 KNM KPM KNQ KPQ b l1 l2
+//   BG[t]  t = -1..T-1: 3 rows of width W(t) (phi psi mu of slice t) then
+//          6 rows of width W(t+1) (a2 a1 e c1 c2 b of slice t+1)
+//   then full-stride planes (T x mp): y, x_a, x_b, x_best
+// A row holds the valid cells (t-q, q), q = qlo(t) .. qlo(t)+nv(t)-1, of its
+// slice; W(t) = nv(t) rounded up to even keeps every row 16-byte aligned.
 struct Skew {
   double *ws;
-  int64_t batch, m, T, mp;  // T = R + m - 1 slices; mp = row stride (m rounded up to even)
+  int64_t batch, m, T, mp, R;
+  int64_t P;        // sum of W(t) over the slices
+  int64_t per_sys;  // doubles per system
+  __device__ __forceinline__ int width(int t) const {
+    if (t < 0 || t >= (int)T) return 0;
+    int nv = t + 1;
+    if ((int)m < nv) nv = (int)m;
+    if ((int)R < nv) nv = (int)R;
+    if ((int)T - t < nv) nv = (int)T - t;
+    return nv + (nv & 1);
+  }
+  __device__ __forceinline__ int qlo(int t) const { return t - (int)R + 1 > 0 ? t - (int)R + 1 : 0; }
+  __device__ __forceinline__ double *fg(int64_t s) const { return ws + s * per_sys; }
+  __device__ __forceinline__ double *bg(int64_t s) const { return fg(s) + 10 * P; }
+  // full-stride planes only (PY, PXA, PXB, PXBEST)
   __device__ __forceinline__ double *at(int p, int64_t s, int64_t t) const {
-    return ws + (((int64_t)p * batch + s) * T + t) * mp;
+    return fg(s) + 19 * P + ((int64_t)(p - PY) * T + t) * mp;
+  }
+};
+
+// running block offsets while walking the slices upward: F = FG[t],
+// Bm = BG[t-1], Bt = BG[t] (relative to fg(s) / bg(s))
+struct Walk {
+  int64_t F, Bm, Bt;
+  __device__ __forceinline__ void start(const Skew &S) { F = 0; Bm = 0; Bt = 6 * (int64_t)S.width(0); }
+  __device__ __forceinline__ void next(const Skew &S, int t) {  // from slice t to t+1
+    F += 10 * (int64_t)S.width(t);
+    Bm = Bt;
+    Bt += 3 * (int64_t)S.width(t) + 6 * (int64_t)S.width(t + 1);
   }
 };
 
@@ -92,6 +142,7 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
                                 double *history, Skew S, int64_t n, double alpha,
                                 int64_t max_iter, int use_x0, Lay lay, int nst) {
   extern __shared__ double sh[];
+  SIP_TR(0);
   const int64_t m = S.m, R = n / m, T = S.T;
   const int q = threadIdx.x;
   const int64_t s = blockIdx.x;
@@ -101,19 +152,45 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
   __syncthreads();
 
   // ---------------- setup: skew A, b, x0; ILU(0)/Stone; defect ------------
+  // The six input values of each thread's cell DS steps ahead are staged in
+  // shared memory with cp.async (stage area = the later TMA ring), so the
+  // per-step recurrence never waits a full global-memory round trip.
+  double rb0 = 0.0;  // max |b| of the own cells (r0 when x0 = 0)
   {
     double *smu = sh, *sphi = sh + 3 * m, *spsi = sh + 6 * m;
+    double *stg_in = sh + 11 * m + (11 * m & 1);  // [DS][6][m]
+    constexpr int DS = 4;
+    auto stage_cell = [&](int64_t tt) {
+      const int64_t pp = tt - q;
+      if (q < m && tt < T && pp >= 0 && pp < R) {
+        const int64_t i = pp * m + q;
+        const double *srcs[6] = {a2p, a1p, ep, c1p, c2p, bp};
+        double *d = stg_in + ((int)(tt % DS) * 6) * m + q;
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + a * m)),
+                       "l"(srcs[a] + lay(i, s))
+                       : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int64_t tt = 0; tt < DS - 1; ++tt) stage_cell(tt);
     double mu_u = 0, phi_u = 0, psi_u = 0;  // own column, previous cell (p-1, q)
+    Walk W;
+    W.start(S);
     for (int64_t t = 0; t < T; ++t) {
+      stage_cell(t + DS - 1);
+      asm volatile("cp.async.wait_group %0;" ::"n"(DS - 1) : "memory");
       const int64_t p = t - q;
       const bool valid = q < m && p >= 0 && p < R;
       if (valid) {
         const int64_t i = p * m + q;
-        const double a2 = i >= m ? ldg(a2p + lay(i, s)) : 0.0;
-        const double a1 = i >= 1 ? ldg(a1p + lay(i, s)) : 0.0;
-        const double e = ldg(ep + lay(i, s));
-        const double c1 = i <= n - 2 ? ldg(c1p + lay(i, s)) : 0.0;
-        const double c2 = i <= n - m - 1 ? ldg(c2p + lay(i, s)) : 0.0;
+        const double *in = stg_in + ((int)(t % DS) * 6) * m + q;
+        const double a2 = i >= m ? in[0] : 0.0;
+        const double a1 = i >= 1 ? in[m] : 0.0;
+        const double e = in[2 * m];
+        const double c1 = i <= n - 2 ? in[3 * m] : 0.0;
+        const double c2 = i <= n - m - 1 ? in[4 * m] : 0.0;
         if ((q == 0 && a1 != 0.0) || (q == m - 1 && c1 != 0.0)) s_notgrid = 1;
         const int sl = (int)((t + 2) % 3);  // slot of step t-1
         const double mu_l = q >= 1 ? smu[sl * m + q - 1] : 0.0;
@@ -174,26 +251,35 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
         double p1 = i <= n - 2 ? ph : 0.0;
         if (m == 2 && i >= 1 && i <= n - 2 && q >= 1) p1 = add(p1, mul(l1, psi_l));
         const double pp = i <= n - m - 1 ? ps : 0.0;
-        *(S.at(PKNM, s, t) + q) = sub(pm, i >= m ? a2 : 0.0);
-        *(S.at(PKN1, s, t) + q) = sub(p_1, i >= 1 ? a1 : 0.0);
-        *(S.at(PK0, s, t) + q) = sub(p0, e);
-        *(S.at(PKP1, s, t) + q) = sub(p1, i <= n - 2 ? c1 : 0.0);
-        *(S.at(PKPM, s, t) + q) = sub(pp, i <= n - m - 1 ? c2 : 0.0);
-        if (m != 2) {
-          *(S.at(PKNQ, s, t) + q) = i >= m ? mul(l2, phi_u) : 0.0;
-          *(S.at(PKPQ, s, t) + q) = (i >= 1 && i <= n - m && q >= 1) ? mul(l1, psi_l) : 0.0;
+        {
+          const int Wt = S.width((int)t), Wm = S.width((int)t - 1);
+          double *fgp = S.fg(s) + W.F + (q - S.qlo((int)t));
+          double *up = S.bg(s) + W.Bt + (q - S.qlo((int)t));
+          double *ab = S.bg(s) + W.Bm + 3 * Wm + (q - S.qlo((int)t));
+          fgp[3 * Wt] = sub(pm, i >= m ? a2 : 0.0);              // KNM
+          fgp[1 * Wt] = sub(p_1, i >= 1 ? a1 : 0.0);             // KN1
+          fgp[0] = sub(p0, e);                                   // K0
+          fgp[2 * Wt] = sub(p1, i <= n - 2 ? c1 : 0.0);          // KP1
+          fgp[4 * Wt] = sub(pp, i <= n - m - 1 ? c2 : 0.0);      // KPM
+          if (m != 2) {
+            fgp[5 * Wt] = i >= m ? mul(l2, phi_u) : 0.0;                            // KNQ
+            fgp[6 * Wt] = (i >= 1 && i <= n - m && q >= 1) ? mul(l1, psi_l) : 0.0;  // KPQ
+          }
+          const double bb = in[5 * m];
+          rb0 = nan_max(rb0, fabs(bb));
+          fgp[7 * Wt] = bb;
+          fgp[8 * Wt] = l1;
+          fgp[9 * Wt] = l2;
+          up[0] = ph;
+          up[Wt] = ps;
+          up[2 * Wt] = mi;
+          ab[0] = a2;
+          ab[Wt] = a1;
+          ab[2 * Wt] = e;
+          ab[3 * Wt] = c1;
+          ab[4 * Wt] = c2;
+          ab[5 * Wt] = bb;
         }
-        *(S.at(PA2, s, t) + q) = a2;
-        *(S.at(PA1, s, t) + q) = a1;
-        *(S.at(PE, s, t) + q) = e;
-        *(S.at(PC1, s, t) + q) = c1;
-        *(S.at(PC2, s, t) + q) = c2;
-        *(S.at(PB, s, t) + q) = ldg(bp + lay(i, s));
-        *(S.at(PL1, s, t) + q) = l1;
-        *(S.at(PL2, s, t) + q) = l2;
-        *(S.at(PMU, s, t) + q) = mi;
-        *(S.at(PPHI, s, t) + q) = ph;
-        *(S.at(PPSI, s, t) + q) = ps;
         *(S.at(PXA, s, t) + q) = use_x0 ? xout[lay(i, s)] : 0.0;
         const int ws_ = (int)(t % 3);
         smu[ws_ * m + q] = mi;
@@ -201,8 +287,10 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
         spsi[ws_ * m + q] = ps;
         mu_u = mi; phi_u = ph; psi_u = ps;
       }
+      W.next(S, (int)t);
       __syncthreads();
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");  // staging area becomes the TMA ring
   }
   if (s_notgrid || s_bad != 0x7fffffff) {
     if (q == 0) {
@@ -213,6 +301,7 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
     return;
   }
 
+  SIP_TR(1);
   double *xs = sh;          // [4][m] window of the previous iterate
   double *ys = sh + 4 * m;  // [3][m]
   double *xn = sh + 7 * m;  // [4][m] window of the new iterate
@@ -237,32 +326,25 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
   // same stage sequence; parity flips at every wrap
   int p_stg = 0, c_stg = 0;
   unsigned p_par = 0, c_par = 0;
-  // producer lane j owns plane row j of the current phase: base, slice offset
-  const double *my_base = nullptr;
-  int my_off = 0, my_cnt = 0;
-  auto set_rows = [&](const int *planes, const int *offs, int cnt) {
-    my_cnt = cnt;
-    if (lane < cnt) { my_base = S.at(planes[lane], s, 0); my_off = offs[lane]; }
-  };
-  // producer: wait until the consumers released the stage, then queue the
-  // rows of step slice tb (row j uses slice tb + off_j); valid columns only,
-  // widened to 16-byte alignment
-  auto produce = [&](int tb) {
+  // producer: wait until the consumers released the stage, then queue one
+  // contiguous group block (lane 0) and one full-stride row's valid range
+  // (lane 1) for the step; both complete on the stage's full barrier
+  auto produce = [&](const double *gsrc, unsigned gbytes, const double *rowp, int rslice) {
     mbar_wait(empty + p_stg, p_par ^ 1u);  // first round passes (fresh barrier)
-    unsigned nb = 0;
+    unsigned rb_ = 0;
     int a0 = 0;
-    const int u = tb + my_off;
-    if (lane < my_cnt && u >= 0 && u < (int)T) {
-      const int qlo = u - (int)R + 1 > 0 ? u - (int)R + 1 : 0, qhi = u < (int)m - 1 ? u : (int)m - 1;
-      if (qlo <= qhi) {
-        a0 = qlo & ~1;
-        nb = (unsigned)(((qhi + 2) & ~1) - a0) * (unsigned)sizeof(double);
-      }
+    if (rowp != nullptr && rslice >= 0 && rslice < (int)T) {
+      a0 = S.qlo(rslice) & ~1;
+      const int qhi = rslice < (int)m - 1 ? rslice : (int)m - 1;
+      rb_ = (unsigned)(((qhi + 2) & ~1) - a0) * (unsigned)sizeof(double);
     }
-    const unsigned bytes = __reduce_add_sync(0xffffffffu, nb);
-    if (lane == 0) mbar_expect(full + p_stg, bytes);
+    if (lane == 0) {
+      mbar_expect(full + p_stg, gbytes + rb_);
+      if (gbytes) bulk_g2s(R_(p_stg, 0), gsrc, gbytes, full + p_stg);
+    } else if (lane == 1 && rb_) {
+      bulk_g2s(R_(p_stg, 10) + a0, rowp + (int64_t)rslice * mp + a0, rb_, full + p_stg);
+    }
     __syncwarp();
-    if (nb) bulk_g2s(R_(p_stg, lane) + a0, my_base + (int64_t)u * mp + a0, nb, full + p_stg);
     if (++p_stg == nst) { p_stg = 0; p_par ^= 1u; }
   };
   auto consume_wait = [&]() -> int {
@@ -298,10 +380,11 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
     if (p <= (int)R - 2) acc = add(acc, mul(c2, X(tt + 1, q)));
     return fabs(sub(bb, acc));
   };
-  auto residual_cell = [&](const double *w, int64_t tt) -> double {
-    return residual_from(w, (int)tt, *(S.at(PA2, s, tt) + q), *(S.at(PA1, s, tt) + q),
-                         *(S.at(PE, s, tt) + q), *(S.at(PC1, s, tt) + q), *(S.at(PC2, s, tt) + q),
-                         *(S.at(PB, s, tt) + q));
+  // A/b of slice tt live in BG[tt-1] (offset Bm of the walk at slice tt)
+  auto residual_cell = [&](const double *w, int tt, int64_t Bm) -> double {
+    const int Wt = S.width(tt), Wm = S.width(tt - 1);
+    const double *ab = S.bg(s) + Bm + 3 * Wm + (q - S.qlo(tt));
+    return residual_from(w, tt, ab[0], ab[Wt], ab[2 * Wt], ab[3 * Wt], ab[4 * Wt], ab[5 * Wt]);
   };
 
   auto block_max = [&](double v) -> double {
@@ -316,16 +399,22 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
 
   // initial residual of x0 (iterative.py:279-283)
   double rloc = 0.0;
-  if (!use_x0) {
-    // x0 = 0: every product of the sweep is a signed zero and 0 + (+-0) = +0,
-    // so b - A x0 == b exactly and r0 = max |b|
-    for (int64_t t = 0; t < T; ++t)
-      if (valid_cell(t)) rloc = nan_max(rloc, fabs(*(S.at(PB, s, t) + q)));
-  } else {
-    for (int64_t t = 0; t < T + 1; ++t) {
-      if (t < T && q < m) xn[(int)(t % 4) * m + q] = valid_cell(t) ? *(S.at(PXA, s, t) + q) : 0.0;
-      __syncthreads();
-      if (t >= 1 && valid_cell(t - 1)) rloc = nan_max(rloc, residual_cell(xn, t - 1));
+  {
+    Walk W;
+    W.start(S);
+    if (!use_x0) {
+      // x0 = 0: every product of the sweep is a signed zero and 0 + (+-0) = +0,
+      // so b - A x0 == b exactly and r0 = max |b| (taken during the setup)
+      rloc = rb0;
+    } else {
+      int64_t Bprev = 0;  // BG offset for slice t-1's A/b (= walk Bm at slice t-1)
+      for (int t = 0; t < (int)T + 1; ++t) {
+        if (t < (int)T && q < m) xn[(t % 4) * m + q] = valid_cell(t) ? *(S.at(PXA, s, t) + q) : 0.0;
+        __syncthreads();
+        if (t >= 1 && valid_cell(t - 1)) rloc = nan_max(rloc, residual_cell(xn, t - 1, Bprev));
+        Bprev = W.Bm;
+        if (t < (int)T) W.next(S, t);
+      }
     }
   }
   double r = block_max(rloc);
@@ -359,14 +448,18 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
       asm volatile("fence.proxy.async.global;" ::: "memory");
       __syncthreads();
     }
+    SIP_TR(2 + 2 * (int)k);
     const int xo = XP[cur], xw = XP[nxt];
     // ---- forward: newRHS = K x + b, then L y = newRHS (iterative.py:293-294)
     // ring rows per step t: K (7), b, l1, l2 at slice t; x_old at slice t+1
     if (producer) {
-      const int fpl[NPL] = {PK0, PKN1, PKP1, PKNM, PKPM, PKNQ, PKPQ, PB, PL1, PL2, xo};
-      const int foff[NPL] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1};
-      set_rows(fpl, foff, NPL);
-      for (int t = 0; t < Ti; ++t) produce(t);
+      const double *xrow = S.at(xo, s, 0);
+      int64_t F = 0;
+      for (int t = 0; t < Ti; ++t) {
+        const int Wt = S.width(t);
+        produce(S.fg(s) + F, (unsigned)(10 * Wt * sizeof(double)), xrow, t + 1);
+        F += 10 * Wt;
+      }
     } else {
       const bool live = q < m;
       double *py = S.at(PY, s, 0) + q;
@@ -374,10 +467,11 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
       double y_u = 0.0;  // own column, previous cell
       for (int t = 0; t < Ti; ++t) {
         const int stg = consume_wait();
-        const double *rb = R_(stg, 0) + q;
+        const int Wt = S.width(t);
+        const double *rb = R_(stg, 0) + (q - S.qlo(t));  // group rows (valid cells only)
         if (live && t + 1 < Ti) {
           const int p1 = t + 1 - q;
-          xs[((t + 1) & 3) * mi_ + q] = (p1 >= 0 && p1 < Ri) ? rb[10 * mp] : 0.0;
+          xs[((t + 1) & 3) * mi_ + q] = (p1 >= 0 && p1 < Ri) ? R_(stg, 10)[q] : 0.0;
         }
         cons_sync();
         const int p = t - q;
@@ -386,23 +480,23 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
           auto X = [&](int sl, int col) { return xs[(sl & 3) * mi_ + col]; };
           double acc = add(0.0, mul(rb[0], X(t, q)));
           if (i >= 1) {
-            if (q >= 1) acc = add(acc, mul(rb[mp], X(t - 1, q - 1)));
-            else if (m == 2) acc = add(acc, mul(rb[mp], X(t, q + 1)));
+            if (q >= 1) acc = add(acc, mul(rb[Wt], X(t - 1, q - 1)));
+            else if (m == 2) acc = add(acc, mul(rb[Wt], X(t, q + 1)));
           }
           if (i <= n - 2) {
-            if (q <= m - 2) acc = add(acc, mul(rb[2 * mp], X(t + 1, q + 1)));
-            else if (m == 2) acc = add(acc, mul(rb[2 * mp], X(t, q - 1)));
+            if (q <= m - 2) acc = add(acc, mul(rb[2 * Wt], X(t + 1, q + 1)));
+            else if (m == 2) acc = add(acc, mul(rb[2 * Wt], X(t, q - 1)));
           }
-          if (p >= 1) acc = add(acc, mul(rb[3 * mp], X(t - 1, q)));
-          if (p <= p_hi) acc = add(acc, mul(rb[4 * mp], X(t + 1, q)));
+          if (p >= 1) acc = add(acc, mul(rb[3 * Wt], X(t - 1, q)));
+          if (p <= p_hi) acc = add(acc, mul(rb[4 * Wt], X(t + 1, q)));
           if (m != 2) {
-            if (i >= m - 1 && q <= m - 2 && p >= 1) acc = add(acc, mul(rb[5 * mp], X(t, q + 1)));
-            if (i + m - 1 <= n - 1 && q >= 1) acc = add(acc, mul(rb[6 * mp], X(t, q - 1)));
+            if (i >= m - 1 && q <= m - 2 && p >= 1) acc = add(acc, mul(rb[5 * Wt], X(t, q + 1)));
+            if (i + m - 1 <= n - 1 && q >= 1) acc = add(acc, mul(rb[6 * Wt], X(t, q - 1)));
           }
-          const double v = add(acc, rb[7 * mp]);
+          const double v = add(acc, rb[7 * Wt]);
           double y = v;
-          if (i >= 1 && q >= 1) y = sub(y, mul(rb[8 * mp], ys[((t + 2) % 3) * mi_ + q - 1]));
-          if (p >= 1) y = sub(y, mul(rb[9 * mp], y_u));
+          if (i >= 1 && q >= 1) y = sub(y, mul(rb[8 * Wt], ys[((t + 2) % 3) * mi_ + q - 1]));
+          if (p >= 1) y = sub(y, mul(rb[9 * Wt], y_u));
           py[(int64_t)t * mp] = y;
           ys[(t % 3) * mi_ + q] = y;
           y_u = y;
@@ -412,14 +506,18 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
       asm volatile("fence.proxy.async.global;" ::: "memory");  // y rows -> TMA reads below
     }
     __syncthreads();
+    SIP_TR(3 + 2 * (int)k);
     // ---- backward U x = y (iterative.py:295) + fused residual (296-297)
     // ring rows per step (t = T-1-j): y, phi, psi, mu at t; A (5), b at t+1
     rloc = 0.0;
     if (producer) {
-      const int bpl[10] = {PY, PPHI, PPSI, PMU, PA2, PA1, PE, PC1, PC2, PB};
-      const int boff[10] = {0, 0, 0, 0, 1, 1, 1, 1, 1, 1};
-      set_rows(bpl, boff, 10);
-      for (int j = 0; j <= Ti; ++j) produce(Ti - 1 - j);
+      const double *yrow = S.at(PY, s, 0);
+      int64_t B = 9 * S.P - 3 * (int64_t)S.width(Ti - 1);  // BG[T-1]
+      for (int t = Ti - 1; t >= -1; --t) {
+        const int64_t sz = 3 * (int64_t)S.width(t) + 6 * (int64_t)S.width(t + 1);
+        produce(S.bg(s) + B, (unsigned)(sz * sizeof(double)), yrow, t);
+        B -= 3 * (int64_t)S.width(t - 1) + 6 * (int64_t)S.width(t);
+      }
     } else {
       const bool live = q < m;
       double *px = S.at(xw, s, 0) + q;
@@ -427,15 +525,17 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
       for (int j = 0; j <= Ti; ++j) {
         const int t = Ti - 1 - j;
         const int stg = consume_wait();
-        const double *rb = R_(stg, 0) + q;
+        const int Wt = S.width(t), W1 = S.width(t + 1);
+        const double *ub = R_(stg, 0) + (q - S.qlo(t));                // phi psi mu of slice t
+        const double *ab = R_(stg, 0) + 3 * Wt + (q - S.qlo(t + 1));   // A, b of slice t+1
         const int p = t - q;
         if (live && t >= 0) {
           if (p >= 0 && p < Ri) {
             const int64_t i = (int64_t)p * m + q;
-            double v = rb[0];
-            if (i <= n - 2 && q <= m - 2) v = sub(v, mul(rb[mp], xn[((t + 1) & 3) * mi_ + q + 1]));
-            if (p <= p_hi) v = sub(v, mul(rb[2 * mp], x_d));
-            const double xv = dvd(v, rb[3 * mp]);
+            double v = R_(stg, 10)[q];  // y
+            if (i <= n - 2 && q <= m - 2) v = sub(v, mul(ub[0], xn[((t + 1) & 3) * mi_ + q + 1]));
+            if (p <= p_hi) v = sub(v, mul(ub[Wt], x_d));
+            const double xv = dvd(v, ub[2 * Wt]);
             px[(int64_t)t * mp] = xv;
             xn[(t & 3) * mi_ + q] = xv;
             x_d = xv;
@@ -445,8 +545,8 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
         }
         cons_sync();
         if (live && t + 1 <= Ti - 1 && p + 1 >= 0 && p + 1 < Ri)
-          rloc = nan_max(rloc, residual_from(xn, t + 1, rb[4 * mp], rb[5 * mp], rb[6 * mp],
-                                             rb[7 * mp], rb[8 * mp], rb[9 * mp]));
+          rloc = nan_max(rloc, residual_from(xn, t + 1, ab[0], ab[W1], ab[2 * W1], ab[3 * W1],
+                                             ab[4 * W1], ab[5 * W1]));
         consume_release();
       }
       asm volatile("fence.proxy.async.global;" ::: "memory");  // x rows -> next forward's TMA
@@ -458,6 +558,7 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
     if (r < best) { best = r; best_loc = cur; }
     if (r0 > 0 && r > 1e6 * r0) { st = BX_STATUS_DIVERGED; break; }
   }
+  SIP_TR(39);
   // ---- outputs in the caller's layout
   for (int64_t t = 0; t < T; ++t) {
     if (!valid_cell(t)) continue;
@@ -515,10 +616,32 @@ bool sip_is_grid(const double *a1, const double *c1, int64_t batch, int64_t n, i
 
 static int64_t sipw_mp(int64_t m) { return (m + 1) & ~(int64_t)1; }
 
+// packed per-system layout (see Skew): sum of the even-rounded slice widths
+static sipw::Skew sipw_layout(double *base, int64_t batch, int64_t n, int64_t m) {
+  sipw::Skew S{};
+  S.ws = base;
+  S.batch = batch;
+  S.m = m;
+  S.R = n / m;
+  S.T = S.R + m - 1;
+  S.mp = sipw_mp(m);
+  int64_t P = 0;
+  for (int64_t t = 0; t < S.T; ++t) {
+    int64_t nv = t + 1;
+    if (m < nv) nv = m;
+    if (S.R < nv) nv = S.R;
+    if (S.T - t < nv) nv = S.T - t;
+    P += nv + (nv & 1);
+  }
+  S.P = P;
+  S.per_sys = 19 * P + 4 * S.T * S.mp;
+  return S;
+}
+
 size_t sip_wave_workspace_bytes(int64_t batch, int64_t n, int64_t m) {
   if (m < 2 || n % m) return 0;
-  const int64_t T = n / m + m - 1;
-  return sizeof(double) * (size_t)sipw::kPlanes * (size_t)batch * (size_t)T * (size_t)sipw_mp(m) + 256;
+  const sipw::Skew S = sipw_layout(nullptr, batch, n, m);
+  return sizeof(double) * (size_t)batch * (size_t)S.per_sys + 256;
 }
 
 int sip_wave(const double *a2, const double *a1, const double *e, const double *c1,
@@ -534,18 +657,21 @@ int sip_wave(const double *a2, const double *a1, const double *e, const double *
   const int64_t mp = sipw_mp(m);
   // workspace base 16-byte aligned for the TMA copies
   double *base = (double *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
-  sipw::Skew S{base, batch, m, n / m + m - 1, mp};
+  const sipw::Skew S = sipw_layout(base, batch, n, m);
   // ring stages: as many as fit next to the 11 m window doubles (<= 4)
   const size_t win = sizeof(double) * (size_t)(11 * m + 1);
   const size_t stage = sizeof(double) * (size_t)sipw::NPL * (size_t)mp;
   int nst = (int)((200 * 1024 - win) / stage);
   if (nst > 4) nst = 4;
+  if (const char *env = getenv("BX_SIP_NST")) nst = nst < atoi(env) ? nst : atoi(env);  // dev knob
   if (nst < 2) {
     bxh::set_error("wavefront SIP: grid width m=%lld too large for the shared-memory ring",
                    (long long)m);
     return BX_ERR_UNSUPPORTED;
   }
-  const size_t smem = win + stage * nst + sizeof(uint64_t) * 2 * nst + 16;
+  const size_t ring = stage * nst + sizeof(uint64_t) * 2 * nst + 16;
+  const size_t staging = sizeof(double) * 4 * 6 * (size_t)m + 16;  // setup cp.async stages (DS = 4)
+  const size_t smem = win + (ring > staging ? ring : staging);
   // consumer warps (one thread per grid column) + one TMA producer warp
   const unsigned threads = (unsigned)(((m + 31) / 32) * 32 + 32);
   if (layout == BX_LAYOUT_INTERLEAVED) {

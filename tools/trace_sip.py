@@ -1,0 +1,25 @@
+"""Developer tool: phase clocks of the wavefront SIP kernel (BX_SIP_TRACE build
+via tools/variant_lib.py), config-4 shape.  Not used by the product."""
+import ctypes, os, sys
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_1804_09666_b200 import StencilMatrix, SipConfig, sip_solve, workloads as W, _lib
+L = _lib.lib()
+g = W.five_point(64, 262144, 512, seed=3)
+A = StencilMatrix.from_diagonals(*g[:5], m=512, layout="system")
+cfg = SipConfig(tolerance=W.sip_tolerance(g[5]), max_iterations=500, alpha=0.5)
+for _ in range(2):
+    r = sip_solve(A, g[5], cfg)
+torch.cuda.synchronize()
+buf = np.zeros((64, 40), dtype=np.int64)
+L.bx_sip_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+L.bx_sip_trace_read(buf.ctypes.data, buf.nbytes)
+k = int(r.iterations.max())
+b = buf[0]
+print("iterations", k, "setup(+r0) cycles", b[1] - b[0], " to first iteration", b[2] - b[1])
+for it in range(k):
+    f = b[3 + 2 * it] - b[2 + 2 * it]
+    nx = b[2 + 2 * (it + 1)] if it + 1 < k else b[39]
+    print(f"  it {it}: forward {f} backward+residual {nx - b[3 + 2 * it]}")
+print("total", b[39] - b[0], "cycles")
