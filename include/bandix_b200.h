@@ -57,6 +57,7 @@ extern "C" {
 #define BX_STATUS_ZERO_DIAG 5       /* ZeroDiagonal(index)         errors.py:73-78 */
 #define BX_STATUS_WINDOW_OVERFLOW 6 /* fp64 symbolic window exceeded (no reference twin) */
 #define BX_STATUS_NOT_GRID 7        /* wavefront SIP given a system whose +-1 couplings cross grid rows */
+#define BX_STATUS_REDUCTION_PIVOT 8 /* ReductionPivotZero(index)   errors.py:37-42 */
 
 /* layouts */
 #define BX_LAYOUT_INTERLEAVED 0
@@ -74,6 +75,7 @@ extern "C" {
 #define BX_SOLVER_SPDM 4
 #define BX_SOLVER_SIP 5
 #define BX_SOLVER_HB 6
+#define BX_SOLVER_PD2TD 7          /* bx_pd2td_ntdm_f64 */
 
 const char *bx_version(void);
 const char *bx_last_error(void);
@@ -109,6 +111,30 @@ int bx_mnpdm_f64(const double *sub2, const double *sub1, const double *main,
                  int32_t *status, int32_t *index, int64_t *nz_sub2, int64_t batch, int64_t n,
                  int64_t ld, int32_t layout, int32_t algo, void *workspace,
                  size_t workspace_bytes, void *stream);
+
+/* pd_to_td (direct.py:116-165): Gaussian reduction of pentadiagonal systems
+ * to tridiagonal ones in the reference's operation order (bit-identical).
+ * Inputs as bx_npdm_f64 (layout/ld); outputs t_sub1/t_main/t_sup1/t_rhs are
+ * row-aligned in the same layout with leading dimension ld_out.  ops
+ * (3*batch int64, may be NULL): (muls, subs, divs) of each system's reduction
+ * (the reference's CounterBox).  status BX_STATUS_REDUCTION_PIVOT with index =
+ * the row whose elimination met a zero pivot (ReductionPivotZero(i)). */
+int bx_pd2td_f64(const double *sub2, const double *sub1, const double *main,
+                 const double *sup1, const double *sup2, const double *rhs, double *t_sub1,
+                 double *t_main, double *t_sup1, double *t_rhs, int64_t *ops, int32_t *status,
+                 int32_t *index, int64_t batch, int64_t n, int64_t ld, int64_t ld_out,
+                 int32_t layout, void *stream);
+
+/* solve_pd2td_ntdm (direct.py:168-177): pd_to_td, then the reference NTDM
+ * (bx_ntdm_f64, sequential) on the reduced system; x in the input layout.
+ * ops as bx_pd2td_f64 (reduction only; the Thomas part is 9N-7 closed form).
+ * status: REDUCTION_PIVOT from the reduction, else ZERO_PIVOT from NTDM.
+ * Workspace: bx_workspace_bytes(BX_SOLVER_PD2TD, batch, n, layout, 0). */
+int bx_pd2td_ntdm_f64(const double *sub2, const double *sub1, const double *main,
+                      const double *sup1, const double *sup2, const double *rhs, double *x,
+                      int64_t *ops, int32_t *status, int32_t *index, int64_t batch, int64_t n,
+                      int64_t ld, int32_t layout, void *workspace, size_t workspace_bytes,
+                      void *stream);
 
 /* ||b - A x||_inf per system, the report residual of _finish_report
  * (direct.py:66-70 -> core.py:243-321), in the reference's row-fused

@@ -22,7 +22,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import STATUS_OK, STATUS_ZERO_PIVOT
+from . import STATUS_OK, STATUS_REDUCTION_PIVOT, STATUS_ZERO_PIVOT
 
 
 def _f64(a):
@@ -258,3 +258,69 @@ def ops_npdm(n):
 
 def ops_mnpdm(n, nz):
     return {"adds": 0, "subs": 5 * n - 7 + 3 * nz, "muls": 7 * n - 8 + 4 * nz, "divs": n}
+
+
+def pd_to_td(sub2, sub1, main, sup1, sup2, rhs):
+    """``pd_to_td`` (direct.py:116-165), batched: sub2 entries eliminated in
+    ascending rows against the row above, then sup2 entries in descending rows
+    against the row below, each only where the entry is nonzero (is_zero
+    skips), with the reference's per-system CounterBox tallies.
+
+    Returns (sub1', main', sup1', rhs', ops (B,3) = muls/subs/divs, status,
+    index); a ReductionPivotZero(i) leaves status 8 / index i and NaN rows.
+    """
+    c, d, e, f, g, r = (_f64(a).copy() for a in (sub2, sub1, main, sup1, sup2, rhs))
+    bsz, n = e.shape
+    ops = np.zeros((bsz, 3), dtype=np.int64)
+    status = np.full(bsz, STATUS_OK, dtype=np.int32)
+    index = np.full(bsz, -1, dtype=np.int32)
+    live = np.ones(bsz, dtype=bool)
+    with np.errstate(all="ignore"):
+        for i in range(2, n):                              # direct.py:134-152
+            ci = c[:, i - 2]
+            act = live & (ci != 0.0)
+            piv = d[:, i - 2]
+            bad = act & (piv == 0.0)
+            status[bad], index[bad], live[bad] = STATUS_REDUCTION_PIVOT, i, False
+            act &= ~bad
+            m = ci / piv
+            d[act, i - 1] = d[act, i - 1] - m[act] * e[act, i - 1]
+            e[act, i] = e[act, i] - m[act] * f[act, i - 1]
+            ops[act] += (2, 2, 1)
+            if i - 1 <= n - 3:
+                ga = g[:, i - 1]
+                act_g = act & (ga != 0.0)
+                f[act_g, i] = f[act_g, i] - m[act_g] * ga[act_g]
+                ops[act_g] += (1, 1, 0)
+            r[act, i] = r[act, i] - m[act] * r[act, i - 1]
+            ops[act] += (1, 1, 0)
+            c[act, i - 2] = 0.0
+        for i in range(n - 3, -1, -1):                     # direct.py:153-164
+            gi = g[:, i]
+            act = live & (gi != 0.0)
+            piv = f[:, i + 1]
+            bad = act & (piv == 0.0)
+            status[bad], index[bad], live[bad] = STATUS_REDUCTION_PIVOT, i, False
+            act &= ~bad
+            m = gi / piv
+            e[act, i] = e[act, i] - m[act] * d[act, i]
+            f[act, i] = f[act, i] - m[act] * e[act, i + 1]
+            r[act, i] = r[act, i] - m[act] * r[act, i + 1]
+            ops[act] += (3, 3, 1)
+            g[act, i] = 0.0
+    for a in (d, e, f, r):
+        a[~live] = np.nan
+    return d, e, f, r, ops, status, index
+
+
+def pd2td_ntdm(sub2, sub1, main, sup1, sup2, rhs):
+    """``solve_pd2td_ntdm`` (direct.py:168-177): reduce, then NTDM on the
+    reduced system.  Returns (x, status, index, reduction ops (B,3))."""
+    d, e, f, r, ops, status, index = pd_to_td(sub2, sub1, main, sup1, sup2, rhs)
+    ok = status == STATUS_OK
+    x = np.full(e.shape, np.nan)
+    if ok.any():
+        xs, st2, ix2 = ntdm(d[ok], e[ok], f[ok], r[ok])
+        x[ok] = xs
+        status[ok], index[ok] = st2, ix2
+    return x, status, index, ops

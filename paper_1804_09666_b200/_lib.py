@@ -19,7 +19,7 @@ LAYOUT_INTERLEAVED = 0
 LAYOUT_SYSTEM_MAJOR = 1
 ALGO_SEQUENTIAL = 0
 ALGO_PARTITIONED = 1
-SOLVER = {"ntdm": 0, "npdm": 1, "mnpdm": 2, "stdm": 3, "spdm": 4, "sip": 5, "hb": 6}
+SOLVER = {"ntdm": 0, "npdm": 1, "mnpdm": 2, "stdm": 3, "spdm": 4, "sip": 5, "hb": 6, "pd2td": 7}
 
 _p = C.c_void_p
 _i64 = C.c_int64
@@ -35,6 +35,8 @@ _SIGS = {
     "bx_npdm_f64": ([_p] * 9 + [_i64, _i64, _i64, _i32, _i32, _p, _sz, _p], C.c_int),
     "bx_mnpdm_f64": ([_p] * 10 + [_i64, _i64, _i64, _i32, _i32, _p, _sz, _p], C.c_int),
     "bx_residual_inf_f64": ([_i32] + [_p] * 8 + [_i64, _i64, _i64, _i32, _p], C.c_int),
+    "bx_pd2td_f64": ([_p] * 13 + [_i64, _i64, _i64, _i64, _i32, _p], C.c_int),
+    "bx_pd2td_ntdm_f64": ([_p] * 10 + [_i64, _i64, _i64, _i32, _p, _sz, _p], C.c_int),
     "bx_stdm_f64": ([_p] * 8 + [_i64, _i64, _i64, _i32, _p, _sz, _p], C.c_int),
     "bx_spdm_f64": ([_p] * 10 + [_i64, _i64, _i64, _i32, _p, _sz, _p], C.c_int),
     "bx_transpose_f64": ([_p, _p] + [_i64] * 7 + [_p], C.c_int),

@@ -74,6 +74,8 @@ size_t bx_workspace_bytes(int32_t solver, int64_t batch, int64_t n, int32_t layo
       return algo == BX_ALGO_SEQUENTIAL ? 2 * rows : bx::part_workspace_bytes(2, batch, n);
     case BX_SOLVER_SIP:
       return algo == BX_ALGO_SEQUENTIAL ? bx::sip_workspace_bytes(batch, n) : 0;
+    case BX_SOLVER_PD2TD:
+      return bx::pd2td_workspace_bytes(batch, n);
     default:
       return bx::other_workspace_bytes(solver, batch, n);
   }
@@ -151,6 +153,42 @@ int bx_mnpdm_f64(const double *sub2, const double *sub1, const double *main, con
                  void *stream) {
   return penta_common("bx_mnpdm_f64", true, sub2, sub1, main, sup1, sup2, rhs, x, status, index,
                       nz_sub2, batch, n, ld, layout, algo, workspace, workspace_bytes, stream);
+}
+
+int bx_pd2td_f64(const double *sub2, const double *sub1, const double *main, const double *sup1,
+                 const double *sup2, const double *rhs, double *t_sub1, double *t_main,
+                 double *t_sup1, double *t_rhs, int64_t *ops, int32_t *status, int32_t *index,
+                 int64_t batch, int64_t n, int64_t ld, int64_t ld_out, int32_t layout,
+                 void *stream) {
+  int rc = check_common("bx_pd2td_f64", batch, n, 3, ld, layout);
+  if (rc) return rc;
+  rc = check_common("bx_pd2td_f64 (out)", batch, n, 3, ld_out, layout);
+  if (rc) return rc;
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(sub2 && sub1 && main && sup1 && sup2 && rhs && t_sub1 && t_main && t_sup1 && t_rhs,
+             "bx_pd2td_f64: null array pointer");
+  bx::pd2td(sub2, sub1, main, sup1, sup2, rhs, t_sub1, t_main, t_sup1, t_rhs, ops, status, index,
+            batch, n, ld, ld_out, layout, (cudaStream_t)stream);
+  return bxh::check_launch("bx_pd2td_f64");
+}
+
+int bx_pd2td_ntdm_f64(const double *sub2, const double *sub1, const double *main,
+                      const double *sup1, const double *sup2, const double *rhs, double *x,
+                      int64_t *ops, int32_t *status, int32_t *index, int64_t batch, int64_t n,
+                      int64_t ld, int32_t layout, void *workspace, size_t workspace_bytes,
+                      void *stream) {
+  int rc = check_common("bx_pd2td_ntdm_f64", batch, n, 3, ld, layout);
+  if (rc) return rc;
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(sub2 && sub1 && main && sup1 && sup2 && rhs && x, "bx_pd2td_ntdm_f64: null array pointer");
+  const size_t need = bx::pd2td_workspace_bytes(batch, n);
+  if (workspace_bytes < need || !workspace) {
+    set_error("bx_pd2td_ntdm_f64: workspace %zu bytes < required %zu", workspace_bytes, need);
+    return BX_ERR_WORKSPACE;
+  }
+  bx::pd2td_ntdm(sub2, sub1, main, sup1, sup2, rhs, x, ops, status, index, batch, n, ld, layout,
+                 workspace, (cudaStream_t)stream);
+  return bxh::check_launch("bx_pd2td_ntdm_f64");
 }
 
 int bx_residual_inf_f64(int32_t bandwidth, const double *sub2, const double *sub1,

@@ -20,6 +20,16 @@ void residual_inf(int bw, const double *c, const double *d, const double *e, con
 
 // bx_direct_part.cu
 size_t part_workspace_bytes(int bandwidth, int64_t batch, int64_t n);
+// pd_to_td / solve_pd2td_ntdm (bx_pd2td.cu)
+int pd2td(const double *c, const double *d, const double *e, const double *f, const double *g,
+          const double *b, double *td, double *te, double *tf, double *tr, int64_t *ops,
+          int32_t *st, int32_t *ix, int64_t batch, int64_t n, int64_t ld, int64_t ld_out,
+          int layout, cudaStream_t stream);
+size_t pd2td_workspace_bytes(int64_t batch, int64_t n);
+int pd2td_ntdm(const double *c, const double *d, const double *e, const double *f,
+               const double *g, const double *b, double *x, int64_t *ops, int32_t *st,
+               int32_t *ix, int64_t batch, int64_t n, int64_t ld, int layout, void *ws,
+               cudaStream_t stream);
 int ntdm_part(const double *d, const double *e, const double *f, const double *b, double *x,
               double *ws, int32_t *st, int32_t *ix, int64_t batch, int64_t n, int64_t ld,
               int layout, cudaStream_t stream);

@@ -23,6 +23,7 @@ from . import _lib
 from .core import (OpCounter, PentaMatrix, SolveReport, TriMatrix, _Timer, ptr, stream_handle,
                    vector_from_layout, workspace)
 from .errors import DimensionMismatch, STATUS_OK, exception_for
+from collections import namedtuple
 
 ALGOS = {"sequential": _lib.ALGO_SEQUENTIAL, "partitioned": _lib.ALGO_PARTITIONED}
 
@@ -152,6 +153,66 @@ def solve_mnpdm(a: PentaMatrix, b, *, algo="sequential", residual=True) -> Solve
               ws.numel(), stream_handle())
     timer.end()
     return _finish(a, x, status, index, timer, b_store, ops_mnpdm(a.n, nz), residual)
+
+
+ReductionResult = namedtuple("ReductionResult", "tri rhs ops status index")
+
+
+def pd_to_td(a: PentaMatrix, b):
+    """Gaussian reduction of pentadiagonal systems to tridiagonal ones
+    (direct.py:116-165), the reference's operation order (bit-identical).
+
+    One system (1-D inputs): returns ``(TriMatrix, rhs, OpCounter)`` like the
+    reference and raises ``ReductionPivotZero(i)``.  A batch: returns
+    ``ReductionResult(tri, rhs, ops, status, index)`` with per-system
+    ``OpCounter`` tensors and status ``STATUS_REDUCTION_PIVOT`` / index."""
+    a = _coerce(a, "penta")
+    b_store = a.rhs(b)
+    lay = a.layout
+    shape = (a.n, a.batch) if lay == _lib.LAYOUT_INTERLEAVED else (a.batch, a.n)
+    out = [torch.empty(shape, dtype=torch.float64, device=a.device) for _ in range(4)]
+    ops = torch.zeros((a.batch, 3), dtype=torch.int64, device=a.device)
+    status = torch.empty(a.batch, dtype=torch.int32, device=a.device)
+    index = torch.empty(a.batch, dtype=torch.int32, device=a.device)
+    c, d, e, f, g = a.rowaligned()
+    _lib.call("bx_pd2td_f64", ptr(c), ptr(d), ptr(e), ptr(f), ptr(g), ptr(b_store),
+              *(ptr(t) for t in out), ptr(ops), ptr(status), ptr(index), a.batch, a.n, a.ld,
+              out[0].stride(0), lay, stream_handle())
+    tri = TriMatrix.from_rowaligned(out[0], out[1], out[2], layout=lay)
+    counter = OpCounter(adds=0, subs=ops[:, 1], muls=ops[:, 0], divs=ops[:, 2])
+    rhs = vector_from_layout(out[3], lay)
+    if a.single:
+        st = int(status[0])
+        if st != STATUS_OK:
+            raise exception_for(st, int(index[0]))
+        tri.single = True
+        c1 = OpCounter(0, int(ops[0, 1]), int(ops[0, 0]), int(ops[0, 2]))
+        r1 = rhs[0].detach().cpu().numpy()
+        r1.setflags(write=False)
+        return tri, r1, c1
+    return ReductionResult(tri, rhs, counter, status, index)
+
+
+def solve_pd2td_ntdm(a: PentaMatrix, b, *, residual=True) -> SolveReport:
+    """Reduce to tridiagonal, then the Thomas method (direct.py:168-177); the
+    report residual is taken against the original pentadiagonal system and the
+    op count is the reduction's plus NTDM's 9N-7."""
+    a = _coerce(a, "penta")
+    b_store = a.rhs(b)
+    x = a.new_vector()
+    ops = torch.zeros((a.batch, 3), dtype=torch.int64, device=a.device)
+    status = torch.empty(a.batch, dtype=torch.int32, device=a.device)
+    index = torch.empty(a.batch, dtype=torch.int32, device=a.device)
+    nbytes = _lib.lib().bx_workspace_bytes(_lib.SOLVER["pd2td"], a.batch, a.n, a.layout, 0)
+    ws = workspace(nbytes, a.device)
+    c, d, e, f, g = a.rowaligned()
+    timer = _Timer()
+    _lib.call("bx_pd2td_ntdm_f64", ptr(c), ptr(d), ptr(e), ptr(f), ptr(g), ptr(b_store), ptr(x),
+              ptr(ops), ptr(status), ptr(index), a.batch, a.n, a.ld, a.layout, ptr(ws), ws.numel(),
+              stream_handle())
+    timer.end()
+    red = OpCounter(adds=0, subs=ops[:, 1], muls=ops[:, 0], divs=ops[:, 2])
+    return _finish(a, x, status, index, timer, b_store, red.merged(ops_ntdm(a.n)), residual)
 
 
 def check_rhs(n, b):

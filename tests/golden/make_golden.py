@@ -26,7 +26,7 @@ sys.path.insert(0, REPO)
 sys.path.insert(0, "/root/reference/pkg/src")
 
 from bandix import core, direct, exact, inverse, iterative  # noqa: E402
-from bandix.errors import (MaxIterationsExceeded, ZeroPivot)  # noqa: E402
+from bandix.errors import (MaxIterationsExceeded, ReductionPivotZero, ZeroPivot)  # noqa: E402
 
 from paper_1804_09666_b200 import workloads as W  # noqa: E402
 
@@ -233,7 +233,72 @@ def golden_exact():
     _save("exact", **out)
 
 
+def _run_pd2td(p):
+    """Reference pd_to_td + solve_pd2td_ntdm per system (direct.py:116-177)."""
+    sub2, sub1, main, sup1, sup2, rhs = p
+    bsz, n = rhs.shape
+    red = {k: np.full(shape, np.nan) for k, shape in
+           (("td", (bsz, n - 1)), ("te", (bsz, n)), ("tf", (bsz, n - 1)), ("tr", (bsz, n)))}
+    ops = np.zeros((bsz, 3), dtype=np.int64)       # muls, subs, divs of the reduction
+    x = np.full((bsz, n), np.nan)
+    res = np.full(bsz, np.nan)
+    tot = np.zeros(bsz, dtype=np.int64)            # solve report ops.total
+    status = np.zeros(bsz, dtype=np.int32)
+    index = np.full(bsz, -1, dtype=np.int32)
+    for s in range(bsz):
+        a = core.PentaMatrix.from_diagonals(sub2[s], sub1[s], main[s], sup1[s], sup2[s])
+        try:
+            t, r, c = direct.pd_to_td(a, rhs[s])
+            red["td"][s], red["te"][s], red["tf"][s] = t.sub1, t.main, t.sup1
+            red["tr"][s] = r
+            ops[s] = (c.muls, c.subs, c.divs)
+        except ReductionPivotZero as e:
+            status[s], index[s] = 8, e.index
+            continue
+        try:
+            rep = direct.solve_pd2td_ntdm(a, rhs[s])
+            x[s], res[s], tot[s] = rep.x, rep.residual_inf, rep.ops.total
+        except ZeroPivot as zp:
+            status[s], index[s] = 1, zp.index
+    return red, ops, x, res, tot, status, index
+
+
+def golden_pd2td():
+    out = {}
+    keys = ("sub2", "sub1", "main", "sup1", "sup2", "rhs")
+    cases = {
+        "dense": W.pd_dominant(6, 96, seed=41),
+        "sparse": W.pd_dominant(6, 96, seed=42, sparse_outer=True),
+        "n3": W.pd_dominant(3, 3, seed=43),
+        "n4": W.pd_dominant(3, 4, seed=44),
+        "n5": W.pd_dominant(3, 5, seed=45, sparse_outer=True),
+    }
+    # failure cases on one batch of order 24:
+    #   s0: ReductionPivotZero in pass 1 (sub2 of row 2 with sub1 of row 1 zero)
+    #   s1: ReductionPivotZero in pass 2 (sup2 of row n-3 with sup1 of row n-2 zero)
+    #   s2: reduction fine, Thomas hits ZeroPivot(0) (main[0] = 0, no sub2/sup2 at row 0/2)
+    #   s3: holes: half the outer entries exactly zero (skipped eliminations)
+    f = [a.copy() for a in W.pd_dominant(4, 24, seed=46)]
+    n = 24
+    f[1][0, 0] = 0.0                        # A[1,0] = 0, A[2,0] = sub2[0] != 0
+    f[3][1, n - 2] = 0.0                    # A[n-2, n-1] = 0
+    f[0][1, n - 4] = 0.0                    # keep pass 1 from touching row n-2's sup1
+    f[2][2, 0] = 0.0; f[0][2, 0] = 0.0; f[4][2, 0] = 0.0
+    rng = np.random.default_rng(47)
+    for k in (0, 4):
+        f[k][3, rng.random(n - 2) < 0.5] = 0.0
+    cases["fail"] = tuple(f)
+    for tag, p in cases.items():
+        red, ops, x, res, tot, st, ix = _run_pd2td(p)
+        out.update({f"{tag}_{k}": v for k, v in zip(keys, p)})
+        out.update({f"{tag}_{k}": v for k, v in red.items()})
+        out.update({f"{tag}_ops": ops, f"{tag}_x": x, f"{tag}_res": res, f"{tag}_tot": tot,
+                    f"{tag}_status": st, f"{tag}_index": ix})
+        print(tag, "status", st.tolist(), "index", ix.tolist())
+    _save("pd2td", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["direct", "iterative", "inverse", "exact"]
+    which = sys.argv[1:] or ["direct", "iterative", "inverse", "exact", "pd2td"]
     for w in which:
         globals()["golden_" + w]()

@@ -105,3 +105,28 @@ def test_hb_dense(golden):
     assert np.abs(r["x"] - g["hb_x"]).max() <= 1e-12 * np.abs(g["hb_x"]).max()
     x, it, res, hist, st = H.hb_invert_dense(np.array([[1.0, 0.0], [3.0, 1.0]]))
     assert it == g["hb_spec_iters"] == 1 and eq(x, g["hb_spec_inv"])
+
+
+PD2TD_TAGS = ["dense", "sparse", "n3", "n4", "n5", "fail"]
+
+
+@pytest.mark.parametrize("tag", PD2TD_TAGS)
+def test_pd2td_restatement(golden, tag):
+    """pd_to_td + solve_pd2td_ntdm restatement == the reference, bit for bit
+    (reduced diagonals, rhs, per-system op tallies, x, ReductionPivotZero /
+    ZeroPivot rows)."""
+    from oracle import direct as D
+    g = golden("pd2td")
+    p = [g[f"{tag}_{k}"] for k in ("sub2", "sub1", "main", "sup1", "sup2", "rhs")]
+    d, e, f, r, ops, st, ix = D.pd_to_td(*p)
+    red_ok = g[f"{tag}_status"] != 8
+    for a, k in ((d, "td"), (e, "te"), (f, "tf"), (r, "tr")):
+        assert np.array_equal(a[red_ok], g[f"{tag}_{k}"][red_ok])
+    assert np.array_equal(ops[red_ok], g[f"{tag}_ops"][red_ok])
+    x, st2, ix2, _ = D.pd2td_ntdm(*p)
+    assert np.array_equal(x, g[f"{tag}_x"], equal_nan=True)
+    assert np.array_equal(st2, g[f"{tag}_status"]) and np.array_equal(ix2, g[f"{tag}_index"])
+    ok = st2 == 0
+    n = p[2].shape[1]
+    # report op total = reduction + NTDM 9N-7 (direct.py:176)
+    assert np.array_equal(ops[ok].sum(axis=1) + 9 * n - 7, g[f"{tag}_tot"][ok])
