@@ -329,8 +329,18 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
   // producer: wait until the consumers released the stage, then queue one
   // contiguous group block (lane 0) and one full-stride row's valid range
   // (lane 1) for the step; both complete on the stage's full barrier
+#ifdef BX_SIP_TRACE
+  long long tr_wait = 0, tr_issue = 0;
+#endif
   auto produce = [&](const double *gsrc, unsigned gbytes, const double *rowp, int rslice) {
+#ifdef BX_SIP_TRACE
+    const long long c0 = clock64();
+#endif
     mbar_wait(empty + p_stg, p_par ^ 1u);  // first round passes (fresh barrier)
+#ifdef BX_SIP_TRACE
+    const long long c1 = clock64();
+    tr_wait += c1 - c0;
+#endif
     unsigned rb_ = 0;
     int a0 = 0;
     if (rowp != nullptr && rslice >= 0 && rslice < (int)T) {
@@ -346,6 +356,9 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
     }
     __syncwarp();
     if (++p_stg == nst) { p_stg = 0; p_par ^= 1u; }
+#ifdef BX_SIP_TRACE
+    tr_issue += clock64() - c1;
+#endif
   };
   auto consume_wait = [&]() -> int {
     const int stg = c_stg;
@@ -558,6 +571,9 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
     if (r < best) { best = r; best_loc = cur; }
     if (r0 > 0 && r > 1e6 * r0) { st = BX_STATUS_DIVERGED; break; }
   }
+#ifdef BX_SIP_TRACE
+  if (producer && lane == 0 && blockIdx.x < 64) { g_sip_trace[blockIdx.x][37] = tr_wait; g_sip_trace[blockIdx.x][38] = tr_issue; }
+#endif
   SIP_TR(39);
   // ---- outputs in the caller's layout
   for (int64_t t = 0; t < T; ++t) {
