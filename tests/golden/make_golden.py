@@ -298,7 +298,50 @@ def golden_pd2td():
     _save("pd2td", **out)
 
 
+MATRIXIO_TEXTS = [
+    "tri 3\n-1 -1\n2 2 2\n-1 -1\nrhs 1 0 1\n",
+    "penta 5\n1 2 3\n4 5 6 7\n10 11 12 13 14\n1/2 -3/4 5 6\n7 8 9\n",
+    "penta 4 # header\n0.5 1\n1 2 3\n4 5 6 7\n1 1 1\n2e-3 -1\nrhs 1 2\n 3 4\n",
+    "tri 2\n1\n2 3\n4\n",
+    "tri 3\n1 2\n3 4 5\n6 7\nrhs 1 2 3 4\n",
+    "quad 3\n1\n",
+    "penta 2\n1\n",
+    "tri 3\n1 2\n3 x 5\n6 7\n",
+    "tri 3\n1 2\n3 4 5\n6\n",
+    "tri three\n",
+    "tri 3\n1/0 2\n3 4 5\n6 7\n",
+    "tri 3\n1 2\n3 4 5\n6 7\nfoo 1 2 3\n",
+    "# only a comment\n",
+    "TRI 2\n+1\n-2 +3\n4\nrhs 1/3 2\n",
+]
+
+
+def golden_matrixio():
+    """Reference parser/serializer outputs (matrixio.py) for hand texts -> JSON."""
+    import json
+    from bandix import matrixio as M
+    from bandix.errors import InvalidInput
+
+    def enc(v):
+        return ["F", v.numerator, v.denominator] if isinstance(v, Fraction) else ["f", float(v).hex()]
+    cases = []
+    for t in MATRIXIO_TEXTS:
+        try:
+            m, rhs = M.parse_matrix_text(t)
+            kind = "penta" if isinstance(m, core.PentaMatrix) else "tri"
+            cases.append({"text": t, "kind": kind, "n": m.n, "exact": bool(m.exact),
+                          "diags": [[enc(v) for v in d] for d in m.diagonals()],
+                          "rhs": None if rhs is None else [enc(v) for v in rhs],
+                          "serialized": M.serialize_matrix(m, rhs)})
+        except InvalidInput as e:
+            cases.append({"text": t, "error": type(e).__name__, "message": str(e)})
+    path = os.path.join(HERE, "matrixio.json")
+    with open(path, "w") as f:
+        json.dump(cases, f, indent=1)
+    print(f"wrote {path}")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["direct", "iterative", "inverse", "exact", "pd2td"]
+    which = sys.argv[1:] or ["direct", "iterative", "inverse", "exact", "pd2td", "matrixio"]
     for w in which:
         globals()["golden_" + w]()
