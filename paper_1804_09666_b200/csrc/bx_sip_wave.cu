@@ -132,7 +132,7 @@ __device__ __forceinline__ double nan_max(double a, double b) {
 
 constexpr int NPL = 11;  // plane rows per ring stage
 
-template <class Lay>
+template <class Lay, bool M2>
 __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
                                 const double *__restrict__ ep, const double *__restrict__ c1p,
                                 const double *__restrict__ c2p, const double *__restrict__ bp,
@@ -474,47 +474,52 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
         F += 10 * Wt;
       }
     } else {
+      // lean per-step loop: rotating window pointers, incremental slice
+      // geometry, grid-form boundary tests (i = p m + q), 32-bit indices
       const bool live = q < m;
       double *py = S.at(PY, s, 0) + q;
       if (live) xs[q] = valid_cell(0) ? *(S.at(xo, s, 0) + q) : 0.0;
       double y_u = 0.0;  // own column, previous cell
-      for (int t = 0; t < Ti; ++t) {
+      const bool qge1 = q >= 1, qlem2 = q <= mi_ - 2, qlast = q == mi_ - 1, qfirst = q == 0;
+      double *wm1 = xs + 3 * mi_, *w0 = xs, *wp1 = xs + mi_, *wp2 = xs + 2 * mi_;  // slices t-1..t+2
+      double *yprev = ys + mi_, *ycur = ys;                                       // slices t-1, t
+      const int stage_d = NPL * mp;
+      for (int t = 0; t < Ti; ++t, py += mp) {
         const int stg = consume_wait();
+        const double *stage = ring + stg * stage_d;
         const int Wt = S.width(t);
-        const double *rb = R_(stg, 0) + (q - S.qlo(t));  // group rows (valid cells only)
-        if (live && t + 1 < Ti) {
-          const int p1 = t + 1 - q;
-          xs[((t + 1) & 3) * mi_ + q] = (p1 >= 0 && p1 < Ri) ? R_(stg, 10)[q] : 0.0;
-        }
-        cons_sync();
         const int p = t - q;
-        if (live && p >= 0 && p < Ri) {
-          const int64_t i = (int64_t)p * m + q;
-          auto X = [&](int sl, int col) { return xs[(sl & 3) * mi_ + col]; };
-          double acc = add(0.0, mul(rb[0], X(t, q)));
-          if (i >= 1) {
-            if (q >= 1) acc = add(acc, mul(rb[Wt], X(t - 1, q - 1)));
-            else if (m == 2) acc = add(acc, mul(rb[Wt], X(t, q + 1)));
+        if (live && t + 1 < Ti) wp1[q] = ((unsigned)(p + 1) < (unsigned)Ri) ? stage[10 * mp + q] : 0.0;
+        cons_sync();
+        if (live && (unsigned)p < (unsigned)Ri) {
+          const double *rb = stage + (q - S.qlo(t));
+          const bool pge1 = p >= 1, plast = p == Ri - 1, phi_ok = p <= p_hi;
+          double acc = add(0.0, mul(rb[0], w0[q]));
+          if (pge1 || qge1) {                                   // i >= 1
+            if (qge1) acc = add(acc, mul(rb[Wt], wm1[q - 1]));
+            else if (M2) acc = add(acc, mul(rb[Wt], w0[q + 1]));
           }
-          if (i <= n - 2) {
-            if (q <= m - 2) acc = add(acc, mul(rb[2 * Wt], X(t + 1, q + 1)));
-            else if (m == 2) acc = add(acc, mul(rb[2 * Wt], X(t, q - 1)));
+          if (!(plast && qlast)) {                              // i <= n - 2
+            if (qlem2) acc = add(acc, mul(rb[2 * Wt], wp1[q + 1]));
+            else if (M2) acc = add(acc, mul(rb[2 * Wt], w0[q - 1]));
           }
-          if (p >= 1) acc = add(acc, mul(rb[3 * Wt], X(t - 1, q)));
-          if (p <= p_hi) acc = add(acc, mul(rb[4 * Wt], X(t + 1, q)));
-          if (m != 2) {
-            if (i >= m - 1 && q <= m - 2 && p >= 1) acc = add(acc, mul(rb[5 * Wt], X(t, q + 1)));
-            if (i + m - 1 <= n - 1 && q >= 1) acc = add(acc, mul(rb[6 * Wt], X(t, q - 1)));
+          if (pge1) acc = add(acc, mul(rb[3 * Wt], wm1[q]));
+          if (phi_ok) acc = add(acc, mul(rb[4 * Wt], wp1[q]));
+          if (!M2) {
+            if ((pge1 || qlast) && qlem2 && pge1) acc = add(acc, mul(rb[5 * Wt], w0[q + 1]));
+            if ((phi_ok || (plast && qfirst)) && qge1) acc = add(acc, mul(rb[6 * Wt], w0[q - 1]));
           }
           const double v = add(acc, rb[7 * Wt]);
           double y = v;
-          if (i >= 1 && q >= 1) y = sub(y, mul(rb[8 * Wt], ys[((t + 2) % 3) * mi_ + q - 1]));
-          if (p >= 1) y = sub(y, mul(rb[9 * Wt], y_u));
-          py[(int64_t)t * mp] = y;
-          ys[(t % 3) * mi_ + q] = y;
+          if ((pge1 || qge1) && qge1) y = sub(y, mul(rb[8 * Wt], yprev[q - 1]));
+          if (pge1) y = sub(y, mul(rb[9 * Wt], y_u));
+          *py = y;
+          ycur[q] = y;
           y_u = y;
         }
         consume_release();
+        double *tw = wm1; wm1 = w0; w0 = wp1; wp1 = wp2; wp2 = tw;
+        double *ty = yprev; yprev = ycur; ycur = ty;
       }
       asm volatile("fence.proxy.async.global;" ::: "memory");  // y rows -> TMA reads below
     }
@@ -533,34 +538,53 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
       }
     } else {
       const bool live = q < m;
-      double *px = S.at(xw, s, 0) + q;
+      double *px = S.at(xw, s, 0) + q + (int64_t)(Ti - 1) * mp;
       double x_d = 0.0;  // own column, next cell (p+1, q)
-      for (int j = 0; j <= Ti; ++j) {
+      const bool qge1 = q >= 1, qlem2 = q <= mi_ - 2, qlast = q == mi_ - 1;
+      // window of the new iterate: slices t, t+1, t+2 (and t+3, being retired)
+      double *n0 = xn + ((Ti - 1) & 3) * mi_, *n1 = xn + (Ti & 3) * mi_,
+             *n2 = xn + ((Ti + 1) & 3) * mi_, *n3 = xn + ((Ti + 2) & 3) * mi_;
+      const int stage_d = NPL * mp;
+      for (int j = 0; j <= Ti; ++j, px -= mp) {
         const int t = Ti - 1 - j;
         const int stg = consume_wait();
+        const double *stage = ring + stg * stage_d;
         const int Wt = S.width(t), W1 = S.width(t + 1);
-        const double *ub = R_(stg, 0) + (q - S.qlo(t));                // phi psi mu of slice t
-        const double *ab = R_(stg, 0) + 3 * Wt + (q - S.qlo(t + 1));   // A, b of slice t+1
         const int p = t - q;
         if (live && t >= 0) {
-          if (p >= 0 && p < Ri) {
-            const int64_t i = (int64_t)p * m + q;
-            double v = R_(stg, 10)[q];  // y
-            if (i <= n - 2 && q <= m - 2) v = sub(v, mul(ub[0], xn[((t + 1) & 3) * mi_ + q + 1]));
+          if ((unsigned)p < (unsigned)Ri) {
+            const double *ub = stage + (q - S.qlo(t));              // phi psi mu of slice t
+            double v = stage[10 * mp + q];                          // y
+            if (!(p == Ri - 1 && qlast) && qlem2) v = sub(v, mul(ub[0], n1[q + 1]));
             if (p <= p_hi) v = sub(v, mul(ub[Wt], x_d));
             const double xv = dvd(v, ub[2 * Wt]);
-            px[(int64_t)t * mp] = xv;
-            xn[(t & 3) * mi_ + q] = xv;
+            *px = xv;
+            n0[q] = xv;
             x_d = xv;
           } else {
-            xn[(t & 3) * mi_ + q] = 0.0;
+            n0[q] = 0.0;
           }
         }
         cons_sync();
-        if (live && t + 1 <= Ti - 1 && p + 1 >= 0 && p + 1 < Ri)
-          rloc = nan_max(rloc, residual_from(xn, t + 1, ab[0], ab[W1], ab[2 * W1], ab[3 * W1],
-                                             ab[4 * W1], ab[5 * W1]));
+        if (live && t + 1 <= Ti - 1 && (unsigned)(p + 1) < (unsigned)Ri) {
+          // residual of slice t+1 (iterative.py:213-221 order, acc from 0)
+          const double *ab = stage + 3 * Wt + (q - S.qlo(t + 1));   // A, b of slice t+1
+          const int pp = p + 1;
+          double acc = add(0.0, mul(ab[2 * W1], n1[q]));
+          if (pp >= 1 || qge1) {
+            if (qge1) acc = add(acc, mul(ab[W1], n0[q - 1]));
+            else if (M2) acc = add(acc, mul(ab[W1], n1[q + 1]));
+          }
+          if (!(pp == Ri - 1 && qlast)) {
+            if (qlem2) acc = add(acc, mul(ab[3 * W1], n2[q + 1]));
+            else if (M2) acc = add(acc, mul(ab[3 * W1], n1[q - 1]));
+          }
+          if (pp >= 1) acc = add(acc, mul(ab[0], n0[q]));
+          if (pp <= p_hi) acc = add(acc, mul(ab[4 * W1], n2[q]));
+          rloc = nan_max(rloc, fabs(sub(ab[5 * W1], acc)));
+        }
         consume_release();
+        double *tw = n3; n3 = n2; n2 = n1; n1 = n0; n0 = tw;
       }
       asm volatile("fence.proxy.async.global;" ::: "memory");  // x rows -> next forward's TMA
     }
@@ -691,13 +715,13 @@ int sip_wave(const double *a2, const double *a1, const double *e, const double *
   // consumer warps (one thread per grid column) + one TMA producer warp
   const unsigned threads = (unsigned)(((m + 31) / 32) * 32 + 32);
   if (layout == BX_LAYOUT_INTERLEAVED) {
-    auto k = sipw::sip_wave_kernel<Interleaved>;
+    auto k = m == 2 ? sipw::sip_wave_kernel<Interleaved, true> : sipw::sip_wave_kernel<Interleaved, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)batch, threads, smem, stream>>>(a2, a1, e, c1, c2, b, tol, x, best_x, iters,
                                                  res, best_res, st, ix, hist, S, n, alpha,
                                                  max_iter, use_x0, Interleaved{ld}, nst);
   } else {
-    auto k = sipw::sip_wave_kernel<SystemMajor>;
+    auto k = m == 2 ? sipw::sip_wave_kernel<SystemMajor, true> : sipw::sip_wave_kernel<SystemMajor, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)batch, threads, smem, stream>>>(a2, a1, e, c1, c2, b, tol, x, best_x, iters,
                                                  res, best_res, st, ix, hist, S, n, alpha,
