@@ -292,9 +292,12 @@ int bx_sip_f64(const double *subm, const double *sub1, const double *main, const
   BX_REQUIRE(subm && sub1 && main && sup1 && supm && rhs && tol && x,
              "bx_sip_f64: null array pointer");
   cudaStream_t st = (cudaStream_t)stream;
-  if (algo == BX_ALGO_AUTO)
-    algo = bx::sip_is_grid(sub1, sup1, batch, n, m, ld, layout, st) ? BX_ALGO_WAVEFRONT
-                                                                     : BX_ALGO_SEQUENTIAL;
+  if (algo == BX_ALGO_AUTO) {
+    BX_REQUIRE(workspace && workspace_bytes >= 4, "bx_sip_f64: workspace required");
+    algo = bx::sip_is_grid(sub1, sup1, batch, n, m, ld, layout, workspace, st)
+               ? BX_ALGO_WAVEFRONT
+               : BX_ALGO_SEQUENTIAL;
+  }
   if (algo != BX_ALGO_SEQUENTIAL && algo != BX_ALGO_WAVEFRONT) {
     set_error("bx_sip_f64: unknown algo %d", algo);
     return BX_ERR_ARG;

@@ -52,7 +52,7 @@ int sip_export(double *ws, int64_t batch, int64_t n, double *const *outs12, int6
 // bx_sip_wave.cu
 size_t sip_wave_workspace_bytes(int64_t batch, int64_t n, int64_t m);
 bool sip_is_grid(const double *a1, const double *c1, int64_t batch, int64_t n, int64_t m,
-                 int64_t ld, int layout, cudaStream_t stream);
+                 int64_t ld, int layout, void *scratch, cudaStream_t stream);
 int sip_wave(const double *a2, const double *a1, const double *e, const double *c1,
              const double *c2, const double *b, const double *tol, double *x, double *best_x,
              int64_t *iters, double *res, double *best_res, int32_t *st, int32_t *ix,

@@ -64,6 +64,7 @@ struct Skew {
   int64_t batch, m, T, mp, R;
   int64_t P;        // sum of W(t) over the slices
   int64_t per_sys;  // doubles per system
+  const int64_t *pw;  // pw[t] = sum of W(u) for u < t, t = 0..T (device table)
   __device__ __forceinline__ int width(int t) const {
     if (t < 0 || t >= (int)T) return 0;
     int nv = t + 1;
@@ -74,6 +75,9 @@ struct Skew {
   }
   __device__ __forceinline__ int qlo(int t) const { return t - (int)R + 1 > 0 ? t - (int)R + 1 : 0; }
   __device__ __forceinline__ double *fg(int64_t s) const { return ws + s * per_sys; }
+  // block offsets: FG[t] = 10 pw[t]; BG[t] = 3 pw[t] + 6 pw[t+1] (BG[-1] = 0)
+  __device__ __forceinline__ int64_t fg_off(int t) const { return 10 * pw[t]; }
+  __device__ __forceinline__ int64_t bg_off(int t) const { return t < 0 ? 0 : 3 * pw[t] + 6 * pw[t + 1]; }
   __device__ __forceinline__ double *bg(int64_t s) const { return fg(s) + 10 * P; }
   // full-stride planes only (PY, PXA, PXB, PXBEST)
   __device__ __forceinline__ double *at(int p, int64_t s, int64_t t) const {
@@ -132,6 +136,53 @@ __device__ __forceinline__ double nan_max(double a, double b) {
 
 constexpr int NPL = 11;  // plane rows per ring stage
 
+// pw[t] = sum_{u<t} W(u), t = 0..T (one thread; T is a few thousand at most)
+__global__ void sip_prefix_kernel(Skew S) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int64_t acc = 0;
+  int64_t *pw = const_cast<int64_t *>(S.pw);
+  for (int t = 0; t <= (int)S.T; ++t) {
+    pw[t] = acc;
+    acc += S.width(t);
+  }
+}
+
+// Data-parallel part of the setup, all SMs: gather A and b of every cell
+// (t-q, q) into the packed slice rows (A/b rows of BG[t-1], b row of FG[t])
+// with the reference's out-of-range zeros applied, and the initial iterate
+// plane.  Rows of the original arrays are read where they lie; consecutive
+// slices reuse the same sectors through L2.  The wavefront setup then reads
+// A/b per step as contiguous rows.
+template <class Lay>
+__global__ void __launch_bounds__(512)
+sip_pack_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
+                const double *__restrict__ ep, const double *__restrict__ c1p,
+                const double *__restrict__ c2p, const double *__restrict__ bp,
+                const double *__restrict__ x0, Skew S, int64_t n, int use_x0, Lay lay) {
+  const int t = blockIdx.x;
+  const int64_t s = blockIdx.y;
+  const int mi = (int)S.m, Ri = (int)S.R;
+  for (int q = threadIdx.x; q < mi; q += blockDim.x) {
+    const int p = t - q;
+    if ((unsigned)p >= (unsigned)Ri) continue;
+    const int64_t i = (int64_t)p * mi + q;
+    const int64_t li = lay(i, s);
+    const bool pge1 = p >= 1, ige1 = pge1 || q >= 1, ilen2 = !(p == Ri - 1 && q == mi - 1),
+               ple = p <= Ri - 2;
+    const int Wt = S.width(t), Wm = S.width(t - 1), qo = q - S.qlo(t);
+    double *ab = S.bg(s) + S.bg_off(t - 1) + 3 * Wm + qo;
+    const double bb = ldg(bp + li);
+    ab[0] = pge1 ? ldg(a2p + li) : 0.0;
+    ab[Wt] = ige1 ? ldg(a1p + li) : 0.0;
+    ab[2 * Wt] = ldg(ep + li);
+    ab[3 * Wt] = ilen2 ? ldg(c1p + li) : 0.0;
+    ab[4 * Wt] = ple ? ldg(c2p + li) : 0.0;
+    ab[5 * Wt] = bb;
+    S.fg(s)[S.fg_off(t) + 7 * Wt + qo] = bb;
+    *(S.at(PXA, s, t) + q) = use_x0 ? x0[li] : 0.0;
+  }
+}
+
 template <class Lay, bool M2>
 __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
                                 const double *__restrict__ ep, const double *__restrict__ c1p,
@@ -157,49 +208,60 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
   // per-step recurrence never waits a full global-memory round trip.
   double rb0 = 0.0;  // max |b| of the own cells (r0 when x0 = 0)
   {
+    // lean per-step loop: 32-bit grid indices, grid-form boundary tests
+    // (i = p m + q), rotating smem slots, incremental addresses
     double *smu = sh, *sphi = sh + 3 * m, *spsi = sh + 6 * m;
     double *stg_in = sh + 11 * m + (11 * m & 1);  // [DS][6][m]
     constexpr int DS = 4;
-    auto stage_cell = [&](int64_t tt) {
-      const int64_t pp = tt - q;
-      if (q < m && tt < T && pp >= 0 && pp < R) {
-        const int64_t i = pp * m + q;
-        const double *srcs[6] = {a2p, a1p, ep, c1p, c2p, bp};
-        double *d = stg_in + ((int)(tt % DS) * 6) * m + q;
+    const int mi_ = (int)m, Ri = (int)R, Ti = (int)T;
+    const bool live = q < m;
+    const bool qge1 = q >= 1, qlast = q == mi_ - 1, qfirst = q == 0;
+    // A/b of cell (tt-q, q) from the packed rows BG[tt-1] (sip_pack_kernel):
+    // the six rows of a slice are contiguous in q, so every copy is coalesced
+    auto stage_cell = [&](int tt) {
+      const int pp = tt - q;
+      if (live && tt < Ti && (unsigned)pp < (unsigned)Ri) {
+        const int W1 = S.width(tt), W0 = S.width(tt - 1);
+        const double *src = S.bg(s) + S.bg_off(tt - 1) + 3 * W0 + (q - S.qlo(tt));
+        const unsigned d = smem_u32(stg_in + ((tt % DS) * 6) * mi_ + q);
+        const unsigned dm = (unsigned)(mi_ * sizeof(double));
 #pragma unroll
         for (int a = 0; a < 6; ++a)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + a * m)),
-                       "l"(srcs[a] + lay(i, s))
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d + a * dm), "l"(src + a * W1)
                        : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    for (int64_t tt = 0; tt < DS - 1; ++tt) stage_cell(tt);
+    for (int tt = 0; tt < DS - 1; ++tt) stage_cell(tt);
     double mu_u = 0, phi_u = 0, psi_u = 0;  // own column, previous cell (p-1, q)
-    Walk W;
-    W.start(S);
-    for (int64_t t = 0; t < T; ++t) {
+    // slots of the left neighbour's factors: previous step (read) / this step (write)
+    int sl_prev = 2 * mi_, sl_cur = 0;  // (t-1) % 3 * m, t % 3 * m at t = 0
+    int64_t F = 0, Bm = 0, Bt = 6 * (int64_t)S.width(0);
+    int Wm = 0, Wt = S.width(0);
+    const bool stone = alpha != 0.0;
+    for (int t = 0; t < Ti; ++t) {
       stage_cell(t + DS - 1);
       asm volatile("cp.async.wait_group %0;" ::"n"(DS - 1) : "memory");
-      const int64_t p = t - q;
-      const bool valid = q < m && p >= 0 && p < R;
-      if (valid) {
-        const int64_t i = p * m + q;
-        const double *in = stg_in + ((int)(t % DS) * 6) * m + q;
-        const double a2 = i >= m ? in[0] : 0.0;
-        const double a1 = i >= 1 ? in[m] : 0.0;
-        const double e = in[2 * m];
-        const double c1 = i <= n - 2 ? in[3 * m] : 0.0;
-        const double c2 = i <= n - m - 1 ? in[4 * m] : 0.0;
-        if ((q == 0 && a1 != 0.0) || (q == m - 1 && c1 != 0.0)) s_notgrid = 1;
-        const int sl = (int)((t + 2) % 3);  // slot of step t-1
-        const double mu_l = q >= 1 ? smu[sl * m + q - 1] : 0.0;
-        const double phi_l = q >= 1 ? sphi[sl * m + q - 1] : 0.0;
-        const double psi_l = q >= 1 ? spsi[sl * m + q - 1] : 0.0;
-        const bool has2 = i >= m && a2 != 0.0;
-        const bool has1 = i >= 1 && a1 != 0.0;  // implies q >= 1 on a grid
+      const int p = t - q;
+      const int Wn = S.width(t + 1);
+      if (live && (unsigned)p < (unsigned)Ri) {
+        const double *in = stg_in + ((t % DS) * 6) * mi_ + q;
+        const bool pge1 = p >= 1, plast = p == Ri - 1, ple = p <= Ri - 2;
+        const bool ige1 = pge1 || qge1;                 // i >= 1
+        const bool ilen2 = !(plast && qlast);           // i <= n - 2
+        const double a2 = pge1 ? in[0] : 0.0;           // i >= m
+        const double a1 = ige1 ? in[mi_] : 0.0;
+        const double e = in[2 * mi_];
+        const double c1 = ilen2 ? in[3 * mi_] : 0.0;
+        const double c2 = ple ? in[4 * mi_] : 0.0;      // i <= n - m - 1
+        if ((qfirst && a1 != 0.0) || (qlast && c1 != 0.0)) s_notgrid = 1;
+        const double mu_l = qge1 ? smu[sl_prev + q - 1] : 0.0;
+        const double phi_l = qge1 ? sphi[sl_prev + q - 1] : 0.0;
+        const double psi_l = qge1 ? spsi[sl_prev + q - 1] : 0.0;
+        const bool has2 = pge1 && a2 != 0.0;
+        const bool has1 = ige1 && a1 != 0.0;  // implies q >= 1 on a grid
         double li2 = 0.0, li1 = 0.0, mi, ph = 0.0, ps = 0.0;
-        if (m == 2) {
+        if (M2) {
           if (has2) li2 = dvd(a2, mu_u);
           if (has1) {
             double tt = a1;
@@ -209,85 +271,80 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
           mi = e;
           if (has2) mi = sub(mi, mul(li2, psi_u));
           if (has1) mi = sub(mi, mul(li1, phi_l));
-          if (i <= n - 2) {
+          if (ilen2) {
             double fi = c1;
             if (fi != 0.0 && has1) fi = sub(fi, mul(li1, psi_l));
             ph = fi;
           }
-          ps = i <= n - 3 ? c2 : 0.0;
+          ps = ple ? c2 : 0.0;                          // i <= n - 3 (m = 2)
         } else {
-          if (has2) li2 = dvd(a2, alpha == 0.0 ? mu_u : add(mu_u, mul(alpha, phi_u)));
-          if (has1) li1 = dvd(a1, alpha == 0.0 ? mu_l : add(mu_l, mul(alpha, psi_l)));
+          if (has2) li2 = dvd(a2, stone ? add(mu_u, mul(alpha, phi_u)) : mu_u);
+          if (has1) li1 = dvd(a1, stone ? add(mu_l, mul(alpha, psi_l)) : mu_l);
           mi = e;
           if (has2) mi = sub(mi, mul(li2, psi_u));
           if (has1) mi = sub(mi, mul(li1, phi_l));
-          if (alpha != 0.0) {
+          if (stone) {
             double comp = 0.0;
             if (has2) comp = add(comp, mul(li2, phi_u));
             if (has1) comp = add(comp, mul(li1, psi_l));
             mi = add(mi, mul(alpha, comp));
           }
-          if (i <= n - 2) {
+          if (ilen2) {
             double fi = c1;
-            if (alpha != 0.0 && fi != 0.0 && has2) fi = sub(fi, mul(alpha, mul(li2, phi_u)));
+            if (stone && fi != 0.0 && has2) fi = sub(fi, mul(alpha, mul(li2, phi_u)));
             ph = fi;
           }
-          if (i <= n - m - 1) {
+          if (ple) {
             double gi = c2;
-            if (alpha != 0.0 && gi != 0.0 && has1) gi = sub(gi, mul(alpha, mul(li1, psi_l)));
+            if (stone && gi != 0.0 && has1) gi = sub(gi, mul(alpha, mul(li1, psi_l)));
             ps = gi;
           }
         }
-        if (mi == 0.0) atomicMin(&s_bad, (int)i);
+        if (mi == 0.0) atomicMin(&s_bad, p * mi_ + q);
         const double l1 = has1 ? li1 : 0.0, l2 = has2 ? li2 : 0.0;
         // defect K = LU - A (iterative.py:152-200); cross-row products are
         // structural zeros and are skipped
-        double pm = i >= m ? mul(l2, mu_u) : 0.0;
-        double p_1 = (i >= 1 && q >= 1) ? mul(l1, mu_l) : 0.0;
-        if (m == 2 && i >= 2) p_1 = add(p_1, mul(l2, phi_u));
+        const double pm = pge1 ? mul(l2, mu_u) : 0.0;
+        double p_1 = (ige1 && qge1) ? mul(l1, mu_l) : 0.0;
+        if (M2 && pge1) p_1 = add(p_1, mul(l2, phi_u));           // i >= 2
         double p0 = mi;
-        if (i >= 1 && q >= 1) p0 = add(p0, mul(l1, phi_l));
-        if (i >= m) p0 = add(p0, mul(l2, psi_u));
-        double p1 = i <= n - 2 ? ph : 0.0;
-        if (m == 2 && i >= 1 && i <= n - 2 && q >= 1) p1 = add(p1, mul(l1, psi_l));
-        const double pp = i <= n - m - 1 ? ps : 0.0;
-        {
-          const int Wt = S.width((int)t), Wm = S.width((int)t - 1);
-          double *fgp = S.fg(s) + W.F + (q - S.qlo((int)t));
-          double *up = S.bg(s) + W.Bt + (q - S.qlo((int)t));
-          double *ab = S.bg(s) + W.Bm + 3 * Wm + (q - S.qlo((int)t));
-          fgp[3 * Wt] = sub(pm, i >= m ? a2 : 0.0);              // KNM
-          fgp[1 * Wt] = sub(p_1, i >= 1 ? a1 : 0.0);             // KN1
-          fgp[0] = sub(p0, e);                                   // K0
-          fgp[2 * Wt] = sub(p1, i <= n - 2 ? c1 : 0.0);          // KP1
-          fgp[4 * Wt] = sub(pp, i <= n - m - 1 ? c2 : 0.0);      // KPM
-          if (m != 2) {
-            fgp[5 * Wt] = i >= m ? mul(l2, phi_u) : 0.0;                            // KNQ
-            fgp[6 * Wt] = (i >= 1 && i <= n - m && q >= 1) ? mul(l1, psi_l) : 0.0;  // KPQ
-          }
-          const double bb = in[5 * m];
-          rb0 = nan_max(rb0, fabs(bb));
-          fgp[7 * Wt] = bb;
-          fgp[8 * Wt] = l1;
-          fgp[9 * Wt] = l2;
-          up[0] = ph;
-          up[Wt] = ps;
-          up[2 * Wt] = mi;
-          ab[0] = a2;
-          ab[Wt] = a1;
-          ab[2 * Wt] = e;
-          ab[3 * Wt] = c1;
-          ab[4 * Wt] = c2;
-          ab[5 * Wt] = bb;
+        if (ige1 && qge1) p0 = add(p0, mul(l1, phi_l));
+        if (pge1) p0 = add(p0, mul(l2, psi_u));
+        double p1 = ilen2 ? ph : 0.0;
+        if (M2 && ige1 && ilen2 && qge1) p1 = add(p1, mul(l1, psi_l));
+        const double pp = ple ? ps : 0.0;
+        const int qo = q - S.qlo(t);
+        double *fgp = S.fg(s) + F + qo;
+        double *up = S.bg(s) + Bt + qo;
+        fgp[3 * Wt] = sub(pm, pge1 ? a2 : 0.0);                  // KNM
+        fgp[Wt] = sub(p_1, ige1 ? a1 : 0.0);                     // KN1
+        fgp[0] = sub(p0, e);                                     // K0
+        fgp[2 * Wt] = sub(p1, ilen2 ? c1 : 0.0);                 // KP1
+        fgp[4 * Wt] = sub(pp, ple ? c2 : 0.0);                   // KPM
+        if (!M2) {
+          fgp[5 * Wt] = pge1 ? mul(l2, phi_u) : 0.0;                                  // KNQ
+          fgp[6 * Wt] = ((ige1 && (ple || (plast && qfirst))) && qge1) ? mul(l1, psi_l) : 0.0;  // KPQ
         }
-        *(S.at(PXA, s, t) + q) = use_x0 ? xout[lay(i, s)] : 0.0;
-        const int ws_ = (int)(t % 3);
-        smu[ws_ * m + q] = mi;
-        sphi[ws_ * m + q] = ph;
-        spsi[ws_ * m + q] = ps;
+        const double bb = in[5 * mi_];
+        rb0 = nan_max(rb0, fabs(bb));
+        fgp[8 * Wt] = l1;   // (b row 7 and the A/b rows come from sip_pack_kernel)
+        fgp[9 * Wt] = l2;
+        up[0] = ph;
+        up[Wt] = ps;
+        up[2 * Wt] = mi;
+        smu[sl_cur + q] = mi;
+        sphi[sl_cur + q] = ph;
+        spsi[sl_cur + q] = ps;
         mu_u = mi; phi_u = ph; psi_u = ps;
       }
-      W.next(S, (int)t);
+      // slice walk: FG[t+1], BG[t] (= A/b of t+1), BG[t+1]
+      F += 10 * (int64_t)Wt;
+      Bm = Bt;
+      Bt += 3 * (int64_t)Wt + 6 * (int64_t)Wn;
+      Wm = Wt;
+      Wt = Wn;
+      sl_prev = sl_cur;
+      sl_cur = sl_cur == 2 * mi_ ? 0 : sl_cur + mi_;
       __syncthreads();
     }
     asm volatile("cp.async.wait_all;" ::: "memory");  // staging area becomes the TMA ring
@@ -636,10 +693,10 @@ __global__ void grid_check_kernel(const double *__restrict__ a1p, const double *
 }  // namespace sipw
 
 bool sip_is_grid(const double *a1, const double *c1, int64_t batch, int64_t n, int64_t m,
-                 int64_t ld, int layout, cudaStream_t stream) {
-  if (m < 2 || n % m != 0 || m > 512) return false;
-  int *flag = nullptr;
-  if (cudaMallocAsync((void **)&flag, sizeof(int), stream) != cudaSuccess) return false;
+                 int64_t ld, int layout, void *scratch, cudaStream_t stream) {
+  // scratch: >= 4 bytes of the caller's workspace (no allocation on this path)
+  if (m < 2 || n % m != 0 || m > 512 || scratch == nullptr) return false;
+  int *flag = reinterpret_cast<int *>(scratch);
   cudaMemsetAsync(flag, 0, sizeof(int), stream);
   const int64_t work = batch * (n / m) * 2;
   const unsigned grid = (unsigned)(work / 256 + 1 < 4096 ? work / 256 + 1 : 4096);
@@ -650,7 +707,6 @@ bool sip_is_grid(const double *a1, const double *c1, int64_t batch, int64_t n, i
   int h = 1;
   cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, stream);
   cudaStreamSynchronize(stream);
-  cudaFreeAsync(flag, stream);
   return h == 0;
 }
 
@@ -678,10 +734,13 @@ static sipw::Skew sipw_layout(double *base, int64_t batch, int64_t n, int64_t m)
   return S;
 }
 
+// workspace: [prefix table pw (T+1 int64, padded to 256 B)] [systems]
+static size_t sipw_pw_bytes(int64_t T) { return ((size_t)(T + 1) * sizeof(int64_t) + 255) & ~(size_t)255; }
+
 size_t sip_wave_workspace_bytes(int64_t batch, int64_t n, int64_t m) {
   if (m < 2 || n % m) return 0;
   const sipw::Skew S = sipw_layout(nullptr, batch, n, m);
-  return sizeof(double) * (size_t)batch * (size_t)S.per_sys + 256;
+  return sipw_pw_bytes(S.T) + sizeof(double) * (size_t)batch * (size_t)S.per_sys + 256;
 }
 
 int sip_wave(const double *a2, const double *a1, const double *e, const double *c1,
@@ -697,7 +756,20 @@ int sip_wave(const double *a2, const double *a1, const double *e, const double *
   const int64_t mp = sipw_mp(m);
   // workspace base 16-byte aligned for the TMA copies
   double *base = (double *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
-  const sipw::Skew S = sipw_layout(base, batch, n, m);
+  sipw::Skew S = sipw_layout(nullptr, batch, n, m);
+  S.pw = reinterpret_cast<const int64_t *>(base);
+  S.ws = reinterpret_cast<double *>(reinterpret_cast<char *>(base) + sipw_pw_bytes(S.T));
+  sipw::sip_prefix_kernel<<<1, 32, 0, stream>>>(S);
+  {
+    const unsigned pthreads = (unsigned)(m < 512 ? ((m + 31) / 32) * 32 : 512);
+    const dim3 pgrid((unsigned)S.T, (unsigned)batch);
+    if (layout == BX_LAYOUT_INTERLEAVED)
+      sipw::sip_pack_kernel<<<pgrid, pthreads, 0, stream>>>(a2, a1, e, c1, c2, b, x, S, n, use_x0,
+                                                           Interleaved{ld});
+    else
+      sipw::sip_pack_kernel<<<pgrid, pthreads, 0, stream>>>(a2, a1, e, c1, c2, b, x, S, n, use_x0,
+                                                           SystemMajor{ld});
+  }
   // ring stages: as many as fit next to the 11 m window doubles (<= 4)
   const size_t win = sizeof(double) * (size_t)(11 * m + 1);
   const size_t stage = sizeof(double) * (size_t)sipw::NPL * (size_t)mp;
