@@ -129,6 +129,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_u32(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
 __device__ __forceinline__ double nan_max(double a, double b) {
   if (a != a || b != b) return __longlong_as_double(0x7ff8000000000000LL);
   return a > b ? a : b;
@@ -417,16 +430,18 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
     tr_issue += clock64() - c1;
 #endif
   };
+  const unsigned full_u = smem_u32(full), empty_u = smem_u32(empty);
   auto consume_wait = [&]() -> int {
     const int stg = c_stg;
-    mbar_wait(full + stg, c_par);
+    mbar_wait_u32(full_u + 8u * (unsigned)stg, c_par);
     return stg;
   };
   auto consume_release = [&]() {
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty + c_stg);
+    if (lane == 0) mbar_arrive_u32(empty_u + 8u * (unsigned)c_stg);
     if (++c_stg == nst) { c_stg = 0; c_par ^= 1u; }
   };
+
   // consumer-only barrier (named barrier 1): the producer warp runs ahead
   auto cons_sync = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(NCT) : "memory"); };
 
@@ -541,15 +556,15 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
       double *wm1 = xs + 3 * mi_, *w0 = xs, *wp1 = xs + mi_, *wp2 = xs + 2 * mi_;  // slices t-1..t+2
       double *yprev = ys + mi_, *ycur = ys;                                       // slices t-1, t
       const int stage_d = NPL * mp;
+      int Wt = S.width(0), qlo_t = 0;
       for (int t = 0; t < Ti; ++t, py += mp) {
         const int stg = consume_wait();
         const double *stage = ring + stg * stage_d;
-        const int Wt = S.width(t);
         const int p = t - q;
         if (live && t + 1 < Ti) wp1[q] = ((unsigned)(p + 1) < (unsigned)Ri) ? stage[10 * mp + q] : 0.0;
         cons_sync();
         if (live && (unsigned)p < (unsigned)Ri) {
-          const double *rb = stage + (q - S.qlo(t));
+          const double *rb = stage + (q - qlo_t);
           const bool pge1 = p >= 1, plast = p == Ri - 1, phi_ok = p <= p_hi;
           double acc = add(0.0, mul(rb[0], w0[q]));
           if (pge1 || qge1) {                                   // i >= 1
@@ -575,6 +590,8 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
           y_u = y;
         }
         consume_release();
+        Wt = S.width(t + 1);
+        qlo_t += t + 1 >= Ri ? 1 : 0;
         double *tw = wm1; wm1 = w0; w0 = wp1; wp1 = wp2; wp2 = tw;
         double *ty = yprev; yprev = ycur; ycur = ty;
       }
@@ -602,15 +619,15 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
       double *n0 = xn + ((Ti - 1) & 3) * mi_, *n1 = xn + (Ti & 3) * mi_,
              *n2 = xn + ((Ti + 1) & 3) * mi_, *n3 = xn + ((Ti + 2) & 3) * mi_;
       const int stage_d = NPL * mp;
+      int Wt = S.width(Ti - 1), W1 = 0, qlo_t = S.qlo(Ti - 1), qlo_1 = S.qlo(Ti);
       for (int j = 0; j <= Ti; ++j, px -= mp) {
         const int t = Ti - 1 - j;
         const int stg = consume_wait();
         const double *stage = ring + stg * stage_d;
-        const int Wt = S.width(t), W1 = S.width(t + 1);
         const int p = t - q;
         if (live && t >= 0) {
           if ((unsigned)p < (unsigned)Ri) {
-            const double *ub = stage + (q - S.qlo(t));              // phi psi mu of slice t
+            const double *ub = stage + (q - qlo_t);                 // phi psi mu of slice t
             double v = stage[10 * mp + q];                          // y
             if (!(p == Ri - 1 && qlast) && qlem2) v = sub(v, mul(ub[0], n1[q + 1]));
             if (p <= p_hi) v = sub(v, mul(ub[Wt], x_d));
@@ -625,7 +642,7 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
         cons_sync();
         if (live && t + 1 <= Ti - 1 && (unsigned)(p + 1) < (unsigned)Ri) {
           // residual of slice t+1 (iterative.py:213-221 order, acc from 0)
-          const double *ab = stage + 3 * Wt + (q - S.qlo(t + 1));   // A, b of slice t+1
+          const double *ab = stage + 3 * Wt + (q - qlo_1);          // A, b of slice t+1
           const int pp = p + 1;
           double acc = add(0.0, mul(ab[2 * W1], n1[q]));
           if (pp >= 1 || qge1) {
@@ -641,6 +658,10 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
           rloc = nan_max(rloc, fabs(sub(ab[5 * W1], acc)));
         }
         consume_release();
+        W1 = Wt;
+        Wt = S.width(t - 1);
+        qlo_1 = qlo_t;
+        qlo_t -= (t - 1 >= Ri - 1 && qlo_t > 0) ? 1 : 0;
         double *tw = n3; n3 = n2; n2 = n1; n1 = n0; n0 = tw;
       }
       asm volatile("fence.proxy.async.global;" ::: "memory");  // x rows -> next forward's TMA
