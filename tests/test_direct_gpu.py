@@ -168,8 +168,30 @@ def test_config2_partitioned_full(cuda):
     assert np.all(res <= 1e-13), res.max()
 
 
-def test_partitioned_zero_pivot_flagged(cuda):
-    p = [a.copy() for a in W.pd_dominant(4, 64, seed=3)]
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("k,n", [(1, 3000), (2, 2049), (2, 5000)])
+def test_partitioned_many_systems_per_cluster(cuda, layout, k, n):
+    # batch well above the number of co-resident clusters: every cluster of
+    # the persistent solver walks several systems through its double buffer
+    bsz = 400
+    if k == 1:
+        d = W.td_dominant(bsz, n, seed=11)
+        x_ref, _, _ = D.ntdm(*d)
+        rep = solve_ntdm(TriMatrix.from_diagonals(*d[:3], layout=layout), d[3], algo="partitioned")
+    else:
+        p = W.pd_dominant(bsz, n, seed=12, sparse_outer=(n == 5000))
+        x_ref, _, _ = D.npdm(*p)
+        rep = solve_mnpdm(PentaMatrix.from_diagonals(*p[:5], layout=layout), p[5], algo="partitioned")
+        _, _, _, nz = D.mnpdm(*p)
+        assert np.array_equal(host(rep.ops.total),
+                              np.array([sum(D.ops_mnpdm(n, int(z)).values()) for z in nz]))
+    assert (host(rep.status) == 0).all()
+    assert rel_err(host(rep.x), x_ref).max() <= REL_TOL
+
+
+@pytest.mark.parametrize("n", [64, 3000])
+def test_partitioned_zero_pivot_flagged(cuda, n):
+    p = [a.copy() for a in W.pd_dominant(4, n, seed=3)]
     p[2][1, 0] = 0.0   # a zero leading pivot: the chunk-local elimination fails too
     A = PentaMatrix.from_diagonals(*p[:5], layout="system")
     rep = solve_npdm(A, p[5], algo="partitioned")
