@@ -171,6 +171,18 @@ int bx_spdm_f64(const double *sub2, const double *sub1, const double *main, cons
                 int32_t *index, int32_t *substitutions, int64_t batch, int64_t n, int64_t ld,
                 int32_t layout, void *workspace, size_t workspace_bytes, void *stream);
 
+/* exact_det_band (exact.py:254-275): the determinant as the product of the
+ * same t-substituted pivots at t -> 0 (zero exactly when the substituted
+ * pivots' orders sum to > 0 -- the reference's nonsingularity gate).  One
+ * thread per system, bandwidth 1 (sub2/sup2 unused, may be NULL) or 2.
+ * det[s] = mantissa[s] * 2^exponent[s], |mantissa| in [0.5, 1) or 0, so that
+ * no product of n pivots overflows.  substitutions (may be NULL) as
+ * bx_stdm_f64; status OK or WINDOW_OVERFLOW (mantissa NaN). */
+int bx_det_band_f64(int32_t bandwidth, const double *sub2, const double *sub1, const double *main,
+                    const double *sup1, const double *sup2, double *mantissa, int64_t *exponent,
+                    int32_t *status, int32_t *index, int32_t *substitutions, int64_t batch,
+                    int64_t n, int64_t ld, int32_t layout, void *stream);
+
 /* ---- ILU(0) / SIP -------------------------------------------------------- */
 /* Stride-m five-point band: subm[i] = A[i,i-m], sub1[i] = A[i,i-1], main[i],
  * sup1[i] = A[i,i+1], supm[i] = A[i,i+m] (row-aligned, n rows each).  m = 2

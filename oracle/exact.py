@@ -58,3 +58,59 @@ def limit_solve_mp(diags, offsets, rhs, dps=50):
                     acc -= v * x[c]
             x[k] = acc / rows[k][k]
         return np.array([float(v) for v in x])
+
+
+def frexp_fraction(v):
+    """(mantissa, exponent) of an exact rational: v = m * 2**e, |m| in
+    [0.5, 1) correctly rounded to binary64 (0 -> (0.0, 0))."""
+    from fractions import Fraction
+    v = Fraction(v)
+    if v == 0:
+        return 0.0, 0
+    e = v.numerator.bit_length() - v.denominator.bit_length()
+    if abs(v) >= Fraction(2) ** e:
+        e += 1
+    if abs(v) < Fraction(2) ** (e - 1):
+        e -= 1
+    return float(v / Fraction(2) ** e), e
+
+
+def det_band_mp(diags, offsets, dps=60):
+    """det(A) by banded Gaussian elimination with partial pivoting in mpmath
+    (sign of the row permutation times the product of U's diagonal); the
+    reference's exact_det_band returns det(A) exactly (exact.py:254-275), so
+    this equals it to 10^-dps relative.  Returns (mantissa, exponent) as
+    frexp_fraction."""
+    from fractions import Fraction
+    n = max(len(d) - min(o, 0) for d, o in zip(diags, offsets)) if diags else 0
+    n = len(diags[offsets.index(0)])
+    with mpmath.workdps(dps):
+        kl = -min(offsets)
+        rows = [dict() for _ in range(n)]
+        for d, off in zip(diags, offsets):
+            for idx, v in enumerate(d):
+                i = idx - min(off, 0)
+                if v != 0.0:
+                    rows[i][i + off] = mpmath.mpf(float(v))
+        det = mpmath.mpf(1)
+        for k in range(n):
+            cand = range(k, min(n, k + kl + 1))
+            p = max(cand, key=lambda r: abs(rows[r].get(k, 0)))
+            if rows[p].get(k, 0) == 0:
+                return 0.0, 0
+            if p != k:
+                rows[k], rows[p] = rows[p], rows[k]
+                det = -det
+            piv = rows[k][k]
+            det *= piv
+            for r in range(k + 1, min(n, k + kl + 1)):
+                f = rows[r].get(k, 0)
+                if f == 0:
+                    continue
+                m = f / piv
+                for c, v in rows[k].items():
+                    if c >= k:
+                        rows[r][c] = rows[r].get(c, 0) - m * v
+                rows[r].pop(k, None)
+        m, e = mpmath.frexp(det)
+        return float(m), int(e)

@@ -39,6 +39,7 @@ _SIGS = {
     "bx_pd2td_ntdm_f64": ([_p] * 10 + [_i64, _i64, _i64, _i32, _p, _sz, _p], C.c_int),
     "bx_stdm_f64": ([_p] * 8 + [_i64, _i64, _i64, _i32, _p, _sz, _p], C.c_int),
     "bx_spdm_f64": ([_p] * 10 + [_i64, _i64, _i64, _i32, _p, _sz, _p], C.c_int),
+    "bx_det_band_f64": ([_i32] + [_p] * 10 + [_i64, _i64, _i64, _i32, _p], C.c_int),
     "bx_transpose_f64": ([_p, _p] + [_i64] * 7 + [_p], C.c_int),
     "bx_hb_workspace_bytes": ([_i64, _i64], _sz),
     "bx_hb_invert_f64": ([_p] * 12 + [_i64, _i64, _i64, C.c_double, _i64, _i64, _i32, _p, _sz, _p],

@@ -241,6 +241,21 @@ int bx_spdm_f64(const double *sub2, const double *sub1, const double *main, cons
                       substitutions, batch, n, ld, layout, workspace, workspace_bytes, stream);
 }
 
+int bx_det_band_f64(int32_t bandwidth, const double *sub2, const double *sub1, const double *main,
+                    const double *sup1, const double *sup2, double *mantissa, int64_t *exponent,
+                    int32_t *status, int32_t *index, int32_t *substitutions, int64_t batch,
+                    int64_t n, int64_t ld, int32_t layout, void *stream) {
+  BX_REQUIRE(bandwidth == 1 || bandwidth == 2, "bx_det_band_f64: bandwidth must be 1 or 2");
+  int rc = check_common("bx_det_band_f64", batch, n, bandwidth == 1 ? 2 : 3, ld, layout);
+  if (rc) return rc;
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(sub1 && main && sup1 && mantissa && exponent && (bandwidth == 1 || (sub2 && sup2)),
+             "bx_det_band_f64: null array pointer");
+  bx::det_band(bandwidth, sub2, sub1, main, sup1, sup2, mantissa, exponent, status, index,
+               substitutions, batch, n, ld, layout, (cudaStream_t)stream);
+  return bxh::check_launch("bx_det_band_f64");
+}
+
 static int check_sip_args(const char *fn, int64_t batch, int64_t n, int64_t m, double alpha,
                           int64_t ld, int32_t layout) {
   int rc = check_common(fn, batch, n, 3, ld, layout);

@@ -152,10 +152,27 @@ __device__ __forceinline__ int ls_zero(const LS &a) {
   return (a.top >= EXACT || a.top >= HI) ? 1 : -1;
 }
 
+// leading coefficient of a (nonzero) series: the value of t^-ord * a at t = 0
+__device__ __forceinline__ double ls_lead(const LS &a) {
+  const int o = ls_ord(a);
+  return o <= HI ? a.c[o - LO] : 0.0;
+}
+// det accumulator: mantissa in [0.5, 1) (or 0) times 2^exponent, so that the
+// product of n pivots neither overflows nor underflows
+struct Det {
+  double m = 1.0;
+  int64_t e = 0;
+  __device__ __forceinline__ void mul(double v) {
+    int ex;
+    m = frexp(m * v, &ex);
+    e += ex;
+  }
+};
+
 // ---- pass 1: the reference pivot recurrence with t-substitution ----------
 template <class Lay>
 __device__ void tri_pivots(const double *dp, const double *ep, const double *fp, int64_t s,
-                           int64_t n, Lay lay, int &nsub, int &ordsum, bool &ovf) {
+                           int64_t n, Lay lay, int &nsub, int &ordsum, bool &ovf, Det *det = nullptr) {
   LS rec = ls_const(0.0);
   for (int64_t i = 0; i < n; ++i) {
     const double e = ldg(ep + lay(i, s));
@@ -171,6 +188,7 @@ __device__ void tri_pivots(const double *dp, const double *ep, const double *fp,
     if (z < 0) ovf = true;
     if (z > 0) { mu = ls_t(); ++nsub; }                                // _Substituter
     ordsum += ls_ord(mu);
+    if (det) det->mul(ls_lead(mu));                                    // exact_det_band: prod mu
     rec = ls_inv(mu, &ovf);                                            // rec = 1/mu
   }
 }
@@ -178,7 +196,7 @@ __device__ void tri_pivots(const double *dp, const double *ep, const double *fp,
 template <class Lay>
 __device__ void penta_pivots(const double *cp, const double *dp, const double *ep,
                              const double *fp, const double *gp, int64_t s, int64_t n, Lay lay,
-                             int &nsub, int &ordsum, bool &ovf) {
+                             int &nsub, int &ordsum, bool &ovf, Det *det = nullptr) {
   // carried: 1/mu and phi of rows i-1, i-2; psi = g (scalar)
   LS r1 = ls_const(0.0), r2 = ls_const(0.0), ph1 = ls_const(0.0), ph2 = ls_const(0.0);
   double ps1 = 0.0, ps2 = 0.0;
@@ -206,6 +224,7 @@ __device__ void penta_pivots(const double *cp, const double *dp, const double *e
     if (z < 0) ovf = true;
     if (z > 0) { mu = ls_t(); ++nsub; }
     ordsum += ls_ord(mu);
+    if (det) det->mul(ls_lead(mu));
     r2 = r1;
     r1 = ls_inv(mu, &ovf);
     ph2 = ph1; ph1 = ph;
@@ -335,7 +354,59 @@ __global__ void exact_kernel(const double *__restrict__ cp, const double *__rest
   set_status(status, index, s, ok ? BX_STATUS_OK : BX_STATUS_SINGULAR, -1);
 }
 
+// exact_det_band (exact.py:254-275): det(A) = lim_{t->0} prod mu_i(t).  The
+// leading minors are polynomials in t, so sum ord(mu_i) >= 0; the limit is 0
+// when it is > 0 and the product of the leading coefficients when it is 0.
+template <int K, class Lay>
+__global__ void det_kernel(const double *__restrict__ cp, const double *__restrict__ dp,
+                           const double *__restrict__ ep, const double *__restrict__ fp,
+                           const double *__restrict__ gp, double *mant, int64_t *expo,
+                           int32_t *status, int32_t *index, int32_t *subs, int64_t batch,
+                           int64_t n, Lay lay) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= batch) return;
+  int nsub = 0, ordsum = 0;
+  bool ovf = false;
+  Det det;
+  if (K == 1) tri_pivots(dp, ep, fp, s, n, lay, nsub, ordsum, ovf, &det);
+  else penta_pivots(cp, dp, ep, fp, gp, s, n, lay, nsub, ordsum, ovf, &det);
+  if (subs) subs[s] = nsub;
+  if (ovf) {
+    mant[s] = __longlong_as_double(0x7ff8000000000000LL);
+    expo[s] = 0;
+    set_status(status, index, s, BX_STATUS_WINDOW_OVERFLOW, -1);
+    return;
+  }
+  mant[s] = ordsum > 0 ? 0.0 : det.m;
+  expo[s] = ordsum > 0 ? 0 : det.e;
+  set_status(status, index, s, BX_STATUS_OK, -1);
+}
+
 }  // namespace ex
+
+int det_band(int kind, const double *c, const double *d, const double *e, const double *f,
+             const double *g, double *mant, int64_t *expo, int32_t *st, int32_t *ix,
+             int32_t *subs, int64_t batch, int64_t n, int64_t ld, int layout,
+             cudaStream_t stream) {
+  const int threads = 32;
+  const dim3 grid((unsigned)((batch + threads - 1) / threads));
+  if (kind == 1) {
+    if (layout == BX_LAYOUT_INTERLEAVED)
+      ex::det_kernel<1><<<grid, threads, 0, stream>>>(c, d, e, f, g, mant, expo, st, ix, subs,
+                                                     batch, n, Interleaved{ld});
+    else
+      ex::det_kernel<1><<<grid, threads, 0, stream>>>(c, d, e, f, g, mant, expo, st, ix, subs,
+                                                     batch, n, SystemMajor{ld});
+  } else {
+    if (layout == BX_LAYOUT_INTERLEAVED)
+      ex::det_kernel<2><<<grid, threads, 0, stream>>>(c, d, e, f, g, mant, expo, st, ix, subs,
+                                                     batch, n, Interleaved{ld});
+    else
+      ex::det_kernel<2><<<grid, threads, 0, stream>>>(c, d, e, f, g, mant, expo, st, ix, subs,
+                                                     batch, n, SystemMajor{ld});
+  }
+  return BX_OK;
+}
 
 size_t exact_workspace_bytes(int kind, int64_t batch, int64_t n) {
   const int planes = kind == 1 ? 4 : 6;  // U row (2K+1) + y

@@ -66,6 +66,11 @@ int exact_solve(int kind, const double *c, const double *d, const double *e, con
                 int32_t *subs, double *ws, int64_t batch, int64_t n, int64_t ld, int layout,
                 cudaStream_t stream);
 
+int det_band(int kind, const double *c, const double *d, const double *e, const double *f,
+             const double *g, double *mant, int64_t *expo, int32_t *st, int32_t *ix,
+             int32_t *subs, int64_t batch, int64_t n, int64_t ld, int layout,
+             cudaStream_t stream);
+
 // bx_hb.cu / bx_hb_host.cu
 size_t hb_dense_bytes(int64_t batch, int64_t n);
 int64_t hb_padded(int64_t n);

@@ -18,14 +18,15 @@ by design:
 from __future__ import annotations
 
 from dataclasses import dataclass
+from fractions import Fraction
 from typing import Any
 
 import numpy as np
 import torch
 
 from . import _lib
-from .core import PentaMatrix, TriMatrix, _as_batch, ptr, stream_handle, vector_from_layout, \
-    vector_to_layout, workspace
+from .core import OpCounter, PentaMatrix, TriMatrix, _as_batch, ptr, stream_handle, \
+    vector_from_layout, vector_to_layout, workspace
 from .errors import InvalidInput, STATUS_OK, exception_for
 
 
@@ -91,3 +92,73 @@ def exact_solve_spdm(a: PentaMatrix, b) -> ExactSolveResult:
     if not isinstance(a, PentaMatrix):
         raise TypeError("expected a PentaMatrix")
     return _solve(2, a, b)
+
+
+@dataclass
+class BandDeterminant:
+    """Batched exact_det_band result: det[s] = mantissa[s] * 2**exponent[s]
+    (|mantissa| in [0.5, 1) or 0: products of thousands of pivots leave the
+    binary64 range), plus the substitution count and status per system."""
+
+    mantissa: Any
+    exponent: Any
+    pivot_substitutions: Any
+    status: Any
+    index: Any
+
+    def sign(self):
+        return torch.sign(self.mantissa)
+
+    def log2abs(self):
+        """log2 |det| (-inf for a zero determinant)."""
+        return torch.log2(self.mantissa.abs()) + self.exponent.to(self.mantissa.dtype)
+
+    def to_fraction(self, s: int = 0) -> Fraction:
+        """det of system s as the exact rational value of the binary64 result."""
+        m = float(self.mantissa[s])
+        e = int(self.exponent[s])
+        return Fraction(m) * (Fraction(2) ** e)
+
+
+def _det_ops(a) -> OpCounter:
+    """Closed-form op count of exact_det_band (exact.py:266-272)."""
+    n = a.n
+    if isinstance(a, PentaMatrix):
+        return OpCounter(muls=4 * n - 7 + (n - 1), subs=4 * n - 7, divs=2 * n - 3)
+    return OpCounter(muls=2 * n - 2 + (n - 1), subs=n - 1, divs=n)
+
+
+def exact_det_band(a, counter=None):
+    """Determinant of a band matrix from the t-substituted pivots at t -> 0
+    (exact.py:254-275).  Zero is a valid return: the nonsingularity test of
+    the symbolic solvers is det != 0.
+
+    Single system (1-D diagonals): a ``Fraction`` like the reference -- the
+    exact rational value of the binary64 determinant (inputs are binary64,
+    the module's convention).  Batched: a :class:`BandDeterminant`.
+    ``counter`` (an object with ``add(**ops)``, e.g. the reference's
+    CounterBox) receives the reference's closed-form op counts."""
+    if isinstance(a, TriMatrix):
+        bw, diags = 1, (None,) + tuple(a.rowaligned()) + (None,)
+    elif isinstance(a, PentaMatrix):
+        bw, diags = 2, tuple(a.rowaligned())
+    else:
+        raise TypeError("expected a TriMatrix or PentaMatrix")
+    dev = a.device
+    mant = torch.empty(a.batch, dtype=torch.float64, device=dev)
+    expo = torch.empty(a.batch, dtype=torch.int64, device=dev)
+    status = torch.empty(a.batch, dtype=torch.int32, device=dev)
+    index = torch.empty(a.batch, dtype=torch.int32, device=dev)
+    subs = torch.empty(a.batch, dtype=torch.int32, device=dev)
+    _lib.call("bx_det_band_f64", bw, *(ptr(d) for d in diags), ptr(mant), ptr(expo), ptr(status),
+              ptr(index), ptr(subs), a.batch, a.n, a.ld, a.layout, stream_handle())
+    if counter is not None:
+        ops = _det_ops(a)
+        counter.add(muls=ops.muls * a.batch, subs=ops.subs * a.batch, divs=ops.divs * a.batch)
+    res = BandDeterminant(mant, expo, subs, status, index)
+    if a.single:
+        st = int(status[0])
+        if st != STATUS_OK:
+            raise exception_for(st, int(index[0]))
+        return res.to_fraction(0)
+    return res

@@ -233,6 +233,53 @@ def golden_exact():
     _save("exact", **out)
 
 
+def _frexp_fraction(v):
+    e = v.numerator.bit_length() - v.denominator.bit_length() if v != 0 else 0
+    if v == 0:
+        return 0.0, 0
+    if abs(v) >= Fraction(2) ** e:
+        e += 1
+    if abs(v) < Fraction(2) ** (e - 1):
+        e -= 1
+    return float(v / Fraction(2) ** e), e
+
+
+def golden_det():
+    """exact_det_band (exact.py:254-275) through the reference on small seeded
+    systems (with and without substituted zero pivots, and singular ones);
+    the exact rational det is stored as (mantissa, exponent), det = m * 2**e."""
+    out = {}
+    t0 = time.time()
+    cases = {
+        "tds": W.td_symbolic(3, 40, seed=2, zeros=2)[:3],          # 2 zero pivots each
+        "td0": W.td_symbolic(3, 200, seed=5, zeros=0)[:3],          # non-dominant, no zeros
+        "tdd": W.td_dominant(3, 300, seed=6)[:3],                   # dominant
+        "pds": W.pd_symbolic(2, 24, seed=2, zeros=2)[:5],
+        "pd0": W.pd_symbolic(2, 120, seed=5, zeros=0)[:5],
+        "pdd": W.pd_dominant(2, 160, seed=6)[:5],
+    }
+    for name, diags in cases.items():
+        bsz = diags[0].shape[0]
+        mant = np.zeros(bsz); expo = np.zeros(bsz, np.int64); ops = np.zeros(bsz, np.int64)
+        for s in range(bsz):
+            cols = [[core.to_exact(v) for v in d[s]] for d in diags]
+            a = (core.TriMatrix if len(diags) == 3 else core.PentaMatrix).from_diagonals(*cols)
+            box = core.CounterBox()
+            det = exact.exact_det_band(a, box)
+            mant[s], expo[s] = _frexp_fraction(det)
+            ops[s] = box.counter.total
+        out.update({f"{name}_d{k}": d for k, d in enumerate(diags)})
+        out.update({f"{name}_mant": mant, f"{name}_expo": expo, f"{name}_ops": ops})
+        print(f"det {name} {time.time()-t0:.1f}s")
+    # singular: a zero determinant with a substituted pivot (rows 0, 1 equal)
+    F = Fraction
+    t = core.TriMatrix.from_diagonals([F(1), F(1)], [F(1), F(1), F(1)], [F(1), F(0)])
+    out.update(sing_d0=np.array([1.0, 1.0]), sing_d1=np.array([1.0, 1.0, 1.0]),
+               sing_d2=np.array([1.0, 0.0]),
+               sing_mant=np.float64(_frexp_fraction(exact.exact_det_band(t))[0]))
+    _save("det", **out)
+
+
 def _run_pd2td(p):
     """Reference pd_to_td + solve_pd2td_ntdm per system (direct.py:116-177)."""
     sub2, sub1, main, sup1, sup2, rhs = p
@@ -342,6 +389,6 @@ def golden_matrixio():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["direct", "iterative", "inverse", "exact", "pd2td", "matrixio"]
+    which = sys.argv[1:] or ["direct", "iterative", "inverse", "exact", "pd2td", "matrixio", "det"]
     for w in which:
         globals()["golden_" + w]()

@@ -130,3 +130,26 @@ def test_pd2td_restatement(golden, tag):
     n = p[2].shape[1]
     # report op total = reduction + NTDM 9N-7 (direct.py:176)
     assert np.array_equal(ops[ok].sum(axis=1) + 9 * n - 7, g[f"{tag}_tot"][ok])
+
+
+DET_CASES = [("tds", 3), ("td0", 3), ("tdd", 3), ("pds", 5), ("pd0", 5), ("pdd", 5)]
+
+
+@pytest.mark.parametrize("tag,nd", DET_CASES)
+def test_det_band_oracle(golden, tag, nd):
+    """oracle det_band_mp (pivoted, 60 digits) reproduces the reference's exact
+    determinant (exact_det_band, rounded to binary64) and its op counts."""
+    from oracle.exact import det_band_mp
+    g = golden("det")
+    offs = [-1, 0, 1] if nd == 3 else [-2, -1, 0, 1, 2]
+    n = g[f"{tag}_d{nd // 2}"].shape[1]
+    for s in range(g[f"{tag}_mant"].shape[0]):
+        diags = [g[f"{tag}_d{k}"][s] for k in range(nd)]
+        # reference-length diagonals (golden stores the reference's arrays)
+        m, e = det_band_mp(diags, offs)
+        assert e == g[f"{tag}_expo"][s]
+        assert abs(m - g[f"{tag}_mant"][s]) <= 2 * np.spacing(abs(g[f"{tag}_mant"][s]))
+        ops = (4 * n - 7 + (n - 1)) + (4 * n - 7) + (2 * n - 3) if nd == 5 else \
+            (2 * n - 2 + (n - 1)) + (n - 1) + n
+        assert ops == g[f"{tag}_ops"][s]
+    assert g["sing_mant"] == 0.0
