@@ -58,6 +58,7 @@ extern "C" {
 #define BX_STATUS_WINDOW_OVERFLOW 6 /* fp64 symbolic window exceeded (no reference twin) */
 #define BX_STATUS_NOT_GRID 7        /* wavefront SIP given a system whose +-1 couplings cross grid rows */
 #define BX_STATUS_REDUCTION_PIVOT 8 /* ReductionPivotZero(index)   errors.py:37-42 */
+#define BX_STATUS_STAGNATED 9       /* Stagnated(best report)      errors.py:81-93 */
 
 /* layouts */
 #define BX_LAYOUT_INTERLEAVED 0
@@ -252,6 +253,45 @@ int bx_sip_hb_f64(const double *subm, const double *sub1, const double *main, co
                   double *inv_residual, int64_t batch, int64_t n, int64_t m, double alpha,
                   int64_t max_iter, int64_t max_inv_iter, int32_t use_x0, int64_t ld,
                   int32_t layout, void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---- banded Hotelling-Bodewig (the reference's array implementation) ------ */
+/* Workspace (bytes) of both banded entry points for bandwidths up to w_cap. */
+size_t bx_hb_banded_workspace_bytes(int64_t batch, int64_t n, int64_t w_cap);
+
+/* hb_invert_banded(factors, side, w, tol, max_iter) (inverse.py:148-195) on
+ * one triangular ILU(0) factor per system, bit-for-bit the reference's
+ * band-truncated iteration (_band_mul_tri order, inverse.py:122-137).
+ * Factor diagonals row-aligned in the call's layout: side 0 = unit-lower L
+ * (l1, l2 used), side 1 = upper U (mu, phi, psi used).  tol[batch].
+ * x_diags (batch, w+1, n): diagonal r of X at [s][r][k], k < n-r (lower:
+ * entry (k+r, k), upper: (k, k+r)).  status: OK, STAGNATED (x = best
+ * approximation, iterations/residual of it), MAX_ITER (x = best, residual
+ * = last), ZERO_DIAG (index = first zero row of U).  history (may be NULL):
+ * [batch][max_iter+1] band residuals, NaN-padded. */
+int bx_hb_invert_banded_f64(const double *mu, const double *l1, const double *l2,
+                            const double *phi, const double *psi, int32_t side, int64_t w,
+                            const double *tol, int64_t max_iter, double *x_diags,
+                            int64_t *iterations, double *residual, double *history,
+                            int32_t *status, int32_t *index, int64_t batch, int64_t n, int64_t ld,
+                            int32_t layout, void *workspace, size_t workspace_bytes, void *stream);
+
+/* sip_hb_solve(mode="banded") (inverse.py:205-302, pentadiagonal, m = 2).
+ * hb_bandwidth >= 2: the reference's explicit width (a stagnated inverse
+ * is accepted).  hb_bandwidth = 0: auto width 2, 4, 8, ... <= w_cap; a width
+ * is accepted once the TRUE residual ||I - M X||_inf is below tol (the
+ * reference widens on stagnation of the truncated iteration only, which
+ * never triggers -- SURVEY D8).  w_used / inv_iterations / inv_residual /
+ * inv_true_residual: [2*batch] (L factors, then U), may be NULL.  Other
+ * arguments and outputs as bx_sip_hb_f64. */
+int bx_sip_hb_banded_f64(const double *sub2, const double *sub1, const double *main,
+                         const double *sup1, const double *sup2, const double *rhs,
+                         const double *tol, double *x, double *best_x, int64_t *iterations,
+                         double *residual, double *best_residual, int32_t *status,
+                         int32_t *index, double *history, int64_t hb_bandwidth, int64_t w_cap,
+                         int64_t *w_used, int64_t *inv_iterations, double *inv_residual,
+                         double *inv_true_residual, int64_t batch, int64_t n, int64_t max_iter,
+                         int64_t max_inv_iter, int32_t use_x0, int64_t ld, int32_t layout,
+                         void *workspace, size_t workspace_bytes, void *stream);
 
 #ifdef __cplusplus
 }

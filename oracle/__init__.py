@@ -31,3 +31,4 @@ STATUS_ZERO_DIAG = 5
 STATUS_WINDOW_OVERFLOW = 6
 STATUS_NOT_GRID = 7
 STATUS_REDUCTION_PIVOT = 8
+STATUS_STAGNATED = 9

@@ -399,4 +399,63 @@ int bx_sip_hb_f64(const double *subm, const double *sub1, const double *main, co
                     (cudaStream_t)stream, false, nullptr, nullptr);
 }
 
+size_t bx_hb_banded_workspace_bytes(int64_t batch, int64_t n, int64_t w_cap) {
+  return bx::sip_hb_band_workspace_bytes(batch, n, w_cap);
+}
+
+int bx_hb_invert_banded_f64(const double *mu, const double *l1, const double *l2,
+                            const double *phi, const double *psi, int32_t side, int64_t w,
+                            const double *tol, int64_t max_iter, double *x_diags,
+                            int64_t *iterations, double *residual, double *history,
+                            int32_t *status, int32_t *index, int64_t batch, int64_t n, int64_t ld,
+                            int32_t layout, void *workspace, size_t workspace_bytes,
+                            void *stream) {
+  const char *fn = "bx_hb_invert_banded_f64";
+  int rc = check_common(fn, batch, n, 3, ld, layout);
+  if (rc) return rc;
+  BX_REQUIRE(side == 0 || side == 1, "%s: side must be 0 (lower) or 1 (upper)", fn);
+  BX_REQUIRE(w >= 2, "%s: banded inversion needs bandwidth w >= 2 (inverse.py:160-161)", fn);
+  BX_REQUIRE(w <= n - 1, "%s: bandwidth w=%lld exceeds n-1", fn, (long long)w);
+  BX_REQUIRE(max_iter >= 0, "%s: max_iter must be >= 0", fn);
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(tol && (side == 0 ? (l1 && l2) : (mu && phi && psi)), "%s: null pointer", fn);
+  const size_t need = bx::hb_band_invert_workspace_bytes(batch, n, w);
+  if (workspace_bytes < need || !workspace) {
+    set_error("%s: workspace %zu bytes < required %zu", fn, workspace_bytes, need);
+    return BX_ERR_WORKSPACE;
+  }
+  return bx::hb_band_invert(mu, l1, l2, phi, psi, side, w, tol, max_iter, x_diags, iterations,
+                            residual, history, status, index, batch, n, ld, layout, workspace,
+                            (cudaStream_t)stream);
+}
+
+int bx_sip_hb_banded_f64(const double *sub2, const double *sub1, const double *main,
+                         const double *sup1, const double *sup2, const double *rhs,
+                         const double *tol, double *x, double *best_x, int64_t *iterations,
+                         double *residual, double *best_residual, int32_t *status,
+                         int32_t *index, double *history, int64_t hb_bandwidth, int64_t w_cap,
+                         int64_t *w_used, int64_t *inv_iterations, double *inv_residual,
+                         double *inv_true_residual, int64_t batch, int64_t n, int64_t max_iter,
+                         int64_t max_inv_iter, int32_t use_x0, int64_t ld, int32_t layout,
+                         void *workspace, size_t workspace_bytes, void *stream) {
+  const char *fn = "bx_sip_hb_banded_f64";
+  int rc = check_sip_args(fn, batch, n, 2, 0.0, ld, layout);
+  if (rc) return rc;
+  BX_REQUIRE(max_iter >= 1, "%s: max_iter must be at least 1", fn);
+  BX_REQUIRE(hb_bandwidth == 0 || hb_bandwidth >= 2, "%s: hb_bandwidth must be 0 (auto) or >= 2", fn);
+  BX_REQUIRE(hb_bandwidth <= n - 1, "%s: hb_bandwidth exceeds n-1", fn);
+  BX_REQUIRE(w_cap >= 2 && w_cap >= hb_bandwidth, "%s: w_cap must be >= max(2, hb_bandwidth)", fn);
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(sub2 && sub1 && main && sup1 && sup2 && rhs && tol && x, "%s: null array pointer", fn);
+  const size_t need = bx::sip_hb_band_workspace_bytes(batch, n, w_cap);
+  if (workspace_bytes < need || !workspace) {
+    set_error("%s: workspace %zu bytes < required %zu", fn, workspace_bytes, need);
+    return BX_ERR_WORKSPACE;
+  }
+  return bx::sip_hb_band(sub2, sub1, main, sup1, sup2, rhs, tol, x, best_x, iterations, residual,
+                         best_residual, status, index, history, hb_bandwidth, w_cap, w_used,
+                         inv_iterations, inv_residual, inv_true_residual, batch, n, max_iter,
+                         max_inv_iter, use_x0, ld, layout, workspace, (cudaStream_t)stream);
+}
+
 }  // extern "C"

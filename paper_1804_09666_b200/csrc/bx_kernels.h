@@ -4,6 +4,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace bx {
 
 // bx_direct_seq.cu
@@ -92,6 +94,37 @@ int sip_hb(const double *a2, const double *a1, const double *e, const double *c1
            int64_t batch, int64_t n, int64_t m, double alpha, int64_t max_iter,
            int64_t max_inv_iter, int use_x0, int64_t ld, int layout, void *workspace,
            cudaStream_t st, bool invert_only, double *xl, double *xu);
+
+// bx_hb_band.cu (banded HB, inverse.py:122-195)
+size_t hb_band_bytes(int64_t batch, int64_t n, int64_t cap);
+int hb_band_invert_round(const double *fac, double *X, double *Xn, double *P, double *Best,
+                         int *dact, int *dzero, unsigned long long *rbits,
+                         const std::vector<int> &act0, const double *tol_f, int64_t batch,
+                         int64_t n, int64_t cap, int64_t w, int64_t max_iter, int64_t *iters,
+                         double *resid, int *status, int *zero_row,
+                         std::vector<std::vector<double>> *hist, cudaStream_t st);
+int hb_band_true_residual(const double *fac, const double *X, int *dact, unsigned long long *rbits,
+                          const std::vector<int> &act, int64_t batch, int64_t n, int64_t cap,
+                          int64_t w, double *out, cudaStream_t st);
+int hb_band_apply(const double *X, const int64_t *wf, const double *v, double *out, const int *act,
+                  int nact, int64_t batch, int64_t n, int64_t cap, int upper, cudaStream_t st);
+int hb_band_factor_planes(const double *mu, const double *l1, const double *l2, const double *phi,
+                          const double *psi, double *fac, int64_t batch, int64_t n, int64_t ld,
+                          int layout, cudaStream_t st);
+int hb_band_invert(const double *mu, const double *l1, const double *l2, const double *phi,
+                   const double *psi, int side, int64_t w, const double *tol, int64_t max_iter,
+                   double *xdiags, int64_t *iterations, double *residual, double *history,
+                   int32_t *status, int32_t *index, int64_t batch, int64_t n, int64_t ld,
+                   int layout, void *workspace, cudaStream_t st);
+size_t hb_band_invert_workspace_bytes(int64_t batch, int64_t n, int64_t w);
+size_t sip_hb_band_workspace_bytes(int64_t batch, int64_t n, int64_t cap);
+int sip_hb_band(const double *a2, const double *a1, const double *e, const double *c1,
+                const double *c2, const double *b, const double *tol, double *x, double *best_x,
+                int64_t *iterations, double *residual, double *best_residual, int32_t *status,
+                int32_t *index, double *history, int64_t w, int64_t cap, int64_t *w_used,
+                int64_t *inv_iterations, double *inv_residual, double *inv_true_residual,
+                int64_t batch, int64_t n, int64_t max_iter, int64_t max_inv_iter, int use_x0,
+                int64_t ld, int layout, void *workspace, cudaStream_t st);
 
 // bx_layout.cu
 int transpose(const double *src, double *dst, int64_t rows, int64_t cols, int64_t lds,

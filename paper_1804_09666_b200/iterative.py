@@ -136,6 +136,8 @@ def ilu0_penta(a, counter=None, *, alpha=0.0):
     object.__setattr__(f, "status", status)
     object.__setattr__(f, "index", index)
     object.__setattr__(f, "layout", s.layout)
+    object.__setattr__(f, "single", s.single)
+    object.__setattr__(f, "batch", s.batch)
     object.__setattr__(f, "_defect", outs[5:])
     return f
 

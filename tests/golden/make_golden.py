@@ -193,6 +193,58 @@ def golden_inverse():
     _save("inverse", **out)
 
 
+def _banded_report(fn):
+    """(diags, iterations, residual, history, status) of hb_invert_banded;
+    Stagnated / MaxIterationsExceeded carry the best approximation."""
+    from bandix.errors import Stagnated
+    try:
+        r = fn()
+        return r.inverse.diags, r.iterations, r.residual_inf, r.residual_history, 0
+    except Stagnated as e:
+        r = e.report
+        return r.inverse.diags, r.iterations, r.residual_inf, r.residual_history, 9
+    except MaxIterationsExceeded as e:
+        return e.best.diags, e.iterations, e.residual_inf, (), 3
+
+
+def golden_hbband():
+    """Banded HB (inverse.py:122-195, the paper's array implementation) on the
+    ILU(0) factors of m = 2 ladder systems, and sip_hb_solve(mode="banded")
+    with explicit widths and in the reference's auto mode."""
+    out = {}
+    p = W.five_point(2, 128, 2, seed=3)
+    out.update({f"hbb_{k}": v for k, v in zip(("sub2", "sub1", "main", "sup1", "sup2", "rhs"), p)})
+    tol = W.sip_tolerance(p[5])
+    out.update(hbb_tol=tol)
+    bsz, n = p[5].shape
+    for s in range(bsz):
+        a = core.PentaMatrix.from_diagonals(*[d[s] for d in p[:5]])
+        f = iterative.ilu0_penta(a)
+        for side in ("lower", "upper"):
+            for w in (2, 3, 6):
+                for tl in (1e-12, float(tol[s])):
+                    key = f"inv_{s}_{side}_{w}_{'t' if tl != 1e-12 else 'd'}"
+                    d, it, r, h, st = _banded_report(
+                        lambda: inverse.hb_invert_banded(f, side, w, tl, 200))
+                    dd = np.full((w + 1, n), np.nan)
+                    for j, v in enumerate(d):
+                        dd[j, :len(v)] = v
+                    out.update({key + "_x": dd, key + "_it": np.int64(it), key + "_res": np.float64(r),
+                                key + "_hist": np.asarray(h, dtype=np.float64), key + "_st": np.int32(st)})
+        for w in (3, 6, 12, None):
+            key = f"sip_{s}_{w if w else 'auto'}"
+            cfg = iterative.SipConfig(tolerance=float(tol[s]), max_iterations=60)
+            try:
+                rep = inverse.sip_hb_solve(a, p[5][s], cfg, mode="banded", hb_bandwidth=w)
+                out.update({key + "_x": np.asarray(rep.x), key + "_k": np.int64(rep.iterations),
+                            key + "_res": np.float64(rep.residual_inf), key + "_st": np.int32(0)})
+            except MaxIterationsExceeded as e:
+                out.update({key + "_x": np.asarray(e.best), key + "_k": np.int64(e.iterations),
+                            key + "_res": np.float64(e.residual_inf), key + "_st": np.int32(3)})
+            print(key, int(out[key + "_st"]), int(out[key + "_k"]), float(out[key + "_res"]))
+    _save("hbband", **out)
+
+
 def golden_exact():
     """Small-N symbolic solves through the reference's exact solvers (float
     inputs converted losslessly with to_exact, exact.py:15-16)."""
@@ -389,6 +441,6 @@ def golden_matrixio():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["direct", "iterative", "inverse", "exact", "pd2td", "matrixio", "det"]
+    which = sys.argv[1:] or ["direct", "iterative", "inverse", "exact", "pd2td", "matrixio", "det", "hbband"]
     for w in which:
         globals()["golden_" + w]()

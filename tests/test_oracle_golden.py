@@ -153,3 +153,49 @@ def test_det_band_oracle(golden, tag, nd):
             (2 * n - 2 + (n - 1)) + (n - 1) + n
         assert ops == g[f"{tag}_ops"][s]
     assert g["sing_mant"] == 0.0
+
+
+HBB = ("sub2", "sub1", "main", "sup1", "sup2", "rhs")
+
+
+def test_hb_banded_restatement(golden):
+    """oracle hb_invert_banded reproduces the reference's banded HB bit for bit
+    (inverse, iterations, residual, history, status) on both factors, widths
+    2/3/6, two tolerances."""
+    from oracle.iterative import ilu0
+    g = golden("hbband")
+    p = [g[f"hbb_{k}"] for k in HBB]
+    f, _, _ = ilu0(*p[:5], 2, 0.0)
+    for s in range(2):
+        for side in ("lower", "upper"):
+            for w in (2, 3, 6):
+                for t in ("d", "t"):
+                    tl = 1e-12 if t == "d" else float(g["hbb_tol"][s])
+                    key = f"inv_{s}_{side}_{w}_{t}"
+                    x, it, r, h, st = H.hb_invert_banded(H.factor_diags(f, s, side), side, w, tl)
+                    gx = g[key + "_x"]
+                    for j in range(w + 1):
+                        assert eq(x[j], gx[j, :len(x[j])])
+                    assert it == g[key + "_it"] and r == g[key + "_res"] and st == g[key + "_st"]
+                    assert eq(np.asarray(h), g[key + "_hist"])
+
+
+def test_sip_hb_banded_restatement(golden):
+    """explicit-width SIP-HB (mode="banded"): the reference stalls at
+    MaxIterationsExceeded; the restatement returns the same best iterate,
+    count and residual bit for bit."""
+    g = golden("hbband")
+    p = [g[f"hbb_{k}"] for k in HBB]
+    for w in (3, 6, 12):
+        o = H.sip_hb_banded(*p, g["hbb_tol"], 60, w=w)
+        for s in range(2):
+            key = f"sip_{s}_{w}"
+            assert o["status"][s] == g[key + "_st"] == STATUS_MAX_ITER
+            assert eq(o["best_x"][s], g[key + "_x"])
+            assert o["iterations"][s] == g[key + "_k"]
+            assert o["best_residual"][s] == g[key + "_res"]
+    # the reference's auto mode never widens (SURVEY D8) and stalls too
+    assert g["sip_0_auto_st"] == STATUS_MAX_ITER and g["sip_1_auto_st"] == STATUS_MAX_ITER
+    # this build's true-residual widening converges
+    o = H.sip_hb_banded(*p, g["hbb_tol"], 60, w=None)
+    assert (o["status"] == 0).all() and (o["residual"] < g["hbb_tol"]).all()
