@@ -348,7 +348,32 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   BX_TR(3);
   if ((lane & ((1 << NLW) - 1)) == 0) wport[warp * NPW + (lane >> NLW)] = port;
   __syncthreads();
-  if (warp == 0) {
+  if (NW >= 2 && warp < 2) {
+    // upper levels on warps 0 and 1 together: warp 0 computes the u half of
+    // every merge (S, u, merged E), warp 1 the mirrored v half (T, v, merged
+    // F), on two SMSPs; nodes are merged in place in wport (level l reads
+    // nodes 2k, 2k+1 and writes node k), two 64-thread named barriers a level
+    const bool isU = warp == 0;
+    int off = NW * NIW;
+#pragma unroll 1
+    for (int l = 0; (1 << l) < NU; ++l) {
+      const int nm = NU >> (l + 1);
+      const int k = lane < nm ? lane : 0;  // idle lanes redo merge 0 and discard
+      Port<K> half, out;
+      bool okm;
+      if (isU) okm = merge_u<K>(wport[2 * k].E, wport[2 * k + 1].F, wport[2 * k + 1].E, half, out);
+      else okm = merge_v<K>(wport[2 * k].E, wport[2 * k + 1].F, wport[2 * k].F, half, out);
+      ok &= okm || lane >= nm;
+      asm volatile("bar.sync 1, 64;" ::: "memory");  // level l read by both warps
+      if (lane < nm) {
+        store_port<K, T>(info, isU ? 0 : (int)(sizeof(Port<K>) / 8), off + lane, half);
+        if (isU) wport[lane].E = out;
+        else wport[lane].F = out;
+      }
+      asm volatile("bar.sync 1, 64;" ::: "memory");  // level l+1 complete
+      off += nm;
+    }
+  } else if (NW == 1) {
     TwoPort<K> wp = wport[lane & (NU - 1)];
     int off = NW * NIW;
 #pragma unroll 1

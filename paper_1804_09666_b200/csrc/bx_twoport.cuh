@@ -129,6 +129,47 @@ __device__ __forceinline__ bool merge(const TwoPort<K> &a, const TwoPort<K> &b, 
   return ok;
 }
 
+// The two halves of merge(), for two warps working one merge together:
+//   merge_u(a.E, b.F, b.E): S = (I - aE.B bF.A)^-1, u (the left child's E as a
+//     function of the merged L, R) and the merged node's E;
+//   merge_v(a.E, b.F, a.F): T = (I - bF.A aE.B)^-1, v (the right child's F)
+//     and the merged node's F -- the mirror image, same cost (78 FP64 ops
+//     each for K=2 against 130 for the whole merge).
+template <int K>
+__device__ __forceinline__ bool merge_u(const Port<K> &aE, const Port<K> &bF, const Port<K> &bE,
+                                        Port<K> &u, Port<K> &outE) {
+  Mat<K> S;
+  const bool ok = inv_i_minus<K>(mm<K>(aE.B, bF.A), S);
+  u.g = mv<K>(S, vadd<K>(aE.g, mv<K>(aE.B, bF.g)));
+  u.A = mm<K>(S, aE.A);
+  u.B = mm<K>(S, mm<K>(aE.B, bF.B));
+  outE.g = vadd<K>(bE.g, mv<K>(bE.A, u.g));
+  outE.A = mm<K>(bE.A, u.A);
+  outE.B = madd<K>(mm<K>(bE.A, u.B), bE.B);
+  return ok;
+}
+template <int K>
+__device__ __forceinline__ bool merge_v(const Port<K> &aE, const Port<K> &bF, const Port<K> &aF,
+                                        Port<K> &v, Port<K> &outF) {
+  Mat<K> Tm;
+  const bool ok = inv_i_minus<K>(mm<K>(bF.A, aE.B), Tm);
+  v.g = mv<K>(Tm, vadd<K>(bF.g, mv<K>(bF.A, aE.g)));
+  v.A = mm<K>(Tm, mm<K>(bF.A, aE.A));
+  v.B = mm<K>(Tm, bF.B);
+  outF.g = vadd<K>(aF.g, mv<K>(aF.B, v.g));
+  outF.A = madd<K>(aF.A, mm<K>(aF.B, v.A));
+  outF.B = mm<K>(aF.B, v.B);
+  return ok;
+}
+
+// one Port of a merge info (component offset c0: 0 = u, NP/2 = v), SoA
+template <int K, int T>
+__device__ __forceinline__ void store_port(double *base, int c0, int node, const Port<K> &p) {
+  const double *v = reinterpret_cast<const double *>(&p);
+#pragma unroll
+  for (int c = 0; c < (int)(sizeof(Port<K>) / 8); ++c) base[(c0 + c) * T + node] = v[c];
+}
+
 template <int K>
 __device__ __forceinline__ Vec<K> apply(const Port<K> &p, const Vec<K> &L, const Vec<K> &R) {
   return vadd<K>(p.g, vadd<K>(mv<K>(p.A, L), mv<K>(p.B, R)));
