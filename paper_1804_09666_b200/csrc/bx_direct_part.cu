@@ -54,6 +54,10 @@ extern "C" int bx_trace_read(void *host, size_t bytes) {
   } while (0)
 #endif
 
+#ifndef BX_PART_LA
+#define BX_PART_LA 1  // input groups in flight ahead of the elimination (measured: 1 > 2 > 3)
+#endif
+
 namespace bx {
 namespace part {
 
@@ -146,10 +150,21 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   else W1[0] = -1.0;
   constexpr int G = 4;
   static_assert(M % G == 0, "M must be a multiple of 4");
-  double ca2[G], ca1[G], ce[G], cc1[G], cc2[G], cb[G];  // group being eliminated
-  double na2[G], na1[G], ne[G], nc1[G], nc2[G], nb[G];  // group in flight
-  auto load_group = [&](int g, double (&A2)[G], double (&A1)[G], double (&E)[G], double (&C1)[G],
-                        double (&C2)[G], double (&Bv)[G]) {
+  // register ring of input groups, LA groups in flight ahead of the one being
+  // eliminated; the g loop is fully unrolled so the ring slots are fixed
+  // registers (a copy between loop iterations would wait for the load)
+  constexpr int LA = BX_PART_LA < M / G ? BX_PART_LA : M / G - 1 > 0 ? M / G - 1 : 1;
+  constexpr int RG = LA + 1;
+  struct Grp {
+    double a2[G], a1[G], e[G], c1[G], c2[G], b[G];
+  } ring[RG];
+  auto load_group = [&](int g, Grp &gr) {
+    double(&A2)[G] = gr.a2;
+    double(&A1)[G] = gr.a1;
+    double(&E)[G] = gr.e;
+    double(&C1)[G] = gr.c1;
+    double(&C2)[G] = gr.c2;
+    double(&Bv)[G] = gr.b;
     const int64_t i0 = base + g * G;
     if (VEC && i0 + G <= n) {
       if (K == 2) ld4(c2p + lay(i0, s), A2);
@@ -200,20 +215,22 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
                    : "memory");
     }
   }
-  load_group(0, ca2, ca1, ce, cc1, cc2, cb);
-#pragma unroll 1
+#pragma unroll
+  for (int g = 0; g < LA && g < M / G; ++g) load_group(g, ring[g]);
+#pragma unroll
   for (int g = 0; g < M / G; ++g) {
-    if (g + 1 < M / G) load_group(g + 1, na2, na1, ne, nc1, nc2, nb);
+    if (g + LA < M / G) load_group(g + LA, ring[(g + LA) % RG]);
+    const Grp &cur = ring[g % RG];
 #pragma unroll
     for (int u = 0; u < G; ++u) {
     const int j = g * G + u;
     const int64_t i = base + j;  // slots outside the matrix are never trusted
-    const double a2 = (K != 2 || i < 2) ? 0.0 : ca2[u];
-    const double a1 = i < 1 ? 0.0 : ca1[u];
-    const double e = ce[u];
-    const double c1 = i > n - 2 ? 0.0 : cc1[u];
-    const double c2 = (K != 2 || i > n - 3) ? 0.0 : cc2[u];
-    const double b = cb[u];
+    const double a2 = (K != 2 || i < 2) ? 0.0 : cur.a2[u];
+    const double a1 = i < 1 ? 0.0 : cur.a1[u];
+    const double e = cur.e[u];
+    const double c1 = i > n - 2 ? 0.0 : cur.c1[u];
+    const double c2 = (K != 2 || i > n - 3) ? 0.0 : cur.c2[u];
+    const double b = cur.b[u];
     // reciprocal form on normalised carried rows (p, q, y, w); rows -2, -1
     // are the virtual rows x_{-2} - L_0 = 0, x_{-1} - L_{K-1} = 0
     double mu, c1p, yy, ww[K];
@@ -251,10 +268,6 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     }
     f2 = f1; g2 = g1; y2 = y1;
     f1 = pn; g1 = qn; y1 = yn;
-    }
-#pragma unroll
-    for (int u = 0; u < G; ++u) {
-      ca2[u] = na2[u]; ca1[u] = na1[u]; ce[u] = ne[u]; cc1[u] = nc1[u]; cc2[u] = nc2[u]; cb[u] = nb[u];
     }
   }
 
