@@ -562,10 +562,23 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
 
   BX_TR(7);
   // ---------------- status / counters ---------------------------------------
-  // status/index were preset to OK/-1 by the launcher; failing CTAs report the
-  // smallest failing row (atomicMin on the unsigned view of index)
+  // csize == 1: this CTA owns the system and writes status/index itself (no
+  // memsets in the launch).  csize > 1: status/index were preset to OK/-1 by
+  // the launcher; failing CTAs report the smallest failing row (atomicMin on
+  // the unsigned view of index).
   if (!ok && bad < 0) bad = (int32_t)seg0;
-  if (__syncthreads_or(bad >= 0)) {
+  if (csize == 1) {
+    if (t == 0) misc[1] = 0x7fffffff;
+    const bool any_bad = __syncthreads_or(bad >= 0);
+    if (any_bad) {
+      if (bad >= 0) atomicMin(&misc[1], bad);
+      __syncthreads();
+    }
+    if (t == 0) {
+      if (status) status[s] = any_bad ? BX_STATUS_ZERO_PIVOT : BX_STATUS_OK;
+      if (index) index[s] = any_bad ? misc[1] : -1;
+    }
+  } else if (__syncthreads_or(bad >= 0)) {
     if (status) status[s] = BX_STATUS_ZERO_PIVOT;
     if (index && bad >= 0) atomicMin(reinterpret_cast<unsigned int *>(index + s), (unsigned int)bad);
   }
@@ -581,8 +594,10 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     nzc = __reduce_add_sync(0xffffffffu, nzc);
     if (lane == 0) atomicAdd(&misc[0], nzc);
     __syncthreads();
-    if (t == 0) atomicAdd(reinterpret_cast<unsigned long long *>(nz_out + s),
-                          (unsigned long long)misc[0]);
+    if (t == 0) {
+      if (csize == 1) nz_out[s] = misc[0];
+      else atomicAdd(reinterpret_cast<unsigned long long *>(nz_out + s), (unsigned long long)misc[0]);
+    }
   }
 }
 
@@ -606,9 +621,11 @@ static int launch(const double *c2, const double *c1, const double *e, const dou
 #endif
   auto kern = part_kernel<K, M, T, VEC, Lay>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (nz) cudaMemsetAsync(nz, 0, sizeof(int64_t) * (size_t)batch, stream);
-  if (st) cudaMemsetAsync(st, 0, sizeof(int32_t) * (size_t)batch, stream);       // BX_STATUS_OK
-  if (ix) cudaMemsetAsync(ix, 0xff, sizeof(int32_t) * (size_t)batch, stream);    // -1
+  if (csize > 1) {  // single-CTA systems write status/index/nz in the kernel
+    if (nz) cudaMemsetAsync(nz, 0, sizeof(int64_t) * (size_t)batch, stream);
+    if (st) cudaMemsetAsync(st, 0, sizeof(int32_t) * (size_t)batch, stream);     // BX_STATUS_OK
+    if (ix) cudaMemsetAsync(ix, 0xff, sizeof(int32_t) * (size_t)batch, stream);  // -1
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(batch * csize));
   cfg.blockDim = dim3(T);
