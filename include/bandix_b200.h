@@ -184,6 +184,19 @@ int bx_det_band_f64(int32_t bandwidth, const double *sub2, const double *sub1, c
                     int32_t *status, int32_t *index, int32_t *substitutions, int64_t batch,
                     int64_t n, int64_t ld, int32_t layout, void *stream);
 
+/* Reciprocal condition estimate in the 1-norm, LAPACK's convention
+ * (dgtcon / dgbcon, norm '1'): rcond = 1 / (||A||_1 est ||A^-1||_1), A = P L U
+ * with partial pivoting, est by Hager-Higham (dlacn2).  The condition gate
+ * of SURVEY 8f row f1 (no reference twin: the reference's exact solvers need
+ * none; SURVEY H7 asks config-3 errors to be read against it).  rcond = 0 and
+ * status SINGULAR (index = first zero pivot column) for an exactly singular
+ * U.  Workspace: bx_rcond_workspace_bytes(bandwidth, batch, n). */
+size_t bx_rcond_workspace_bytes(int32_t bandwidth, int64_t batch, int64_t n);
+int bx_rcond_band_f64(int32_t bandwidth, const double *sub2, const double *sub1,
+                      const double *main, const double *sup1, const double *sup2, double *rcond,
+                      int32_t *status, int32_t *index, int64_t batch, int64_t n, int64_t ld,
+                      int32_t layout, void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---- ILU(0) / SIP -------------------------------------------------------- */
 /* Stride-m five-point band: subm[i] = A[i,i-m], sub1[i] = A[i,i-1], main[i],
  * sup1[i] = A[i,i+1], supm[i] = A[i,i+m] (row-aligned, n rows each).  m = 2

@@ -11,7 +11,8 @@ fallback: without the built library or a GPU every solver raises.
 
 from .core import BandFactors, OpCounter, PentaMatrix, SolveReport, TriMatrix  # noqa: F401
 from .direct import pd_to_td, solve_mnpdm, solve_npdm, solve_ntdm, solve_pd2td_ntdm  # noqa: F401
-from .exact import BandDeterminant, ExactSolveResult, exact_det_band, exact_solve_spdm, exact_solve_stdm  # noqa: F401
+from .exact import (BandDeterminant, ExactSolveResult, exact_det_band, exact_solve_spdm,  # noqa: F401
+                    exact_solve_stdm, rcond_band)
 from .inverse import (BandedApproxInverse, InversionReport, hb_invert_banded,  # noqa: F401
                       hb_invert_factors, sip_hb_solve)
 from .iterative import (DefectMatrix, SipConfig, StencilMatrix, defect_matrix,  # noqa: F401

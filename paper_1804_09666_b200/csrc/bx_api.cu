@@ -256,6 +256,31 @@ int bx_det_band_f64(int32_t bandwidth, const double *sub2, const double *sub1, c
   return bxh::check_launch("bx_det_band_f64");
 }
 
+size_t bx_rcond_workspace_bytes(int32_t bandwidth, int64_t batch, int64_t n) {
+  return bx::rcond_workspace_bytes(bandwidth == 1 ? 1 : 2, batch, n);
+}
+
+int bx_rcond_band_f64(int32_t bandwidth, const double *sub2, const double *sub1,
+                      const double *main, const double *sup1, const double *sup2, double *rcond,
+                      int32_t *status, int32_t *index, int64_t batch, int64_t n, int64_t ld,
+                      int32_t layout, void *workspace, size_t workspace_bytes, void *stream) {
+  const char *fn = "bx_rcond_band_f64";
+  BX_REQUIRE(bandwidth == 1 || bandwidth == 2, "%s: bandwidth must be 1 or 2", fn);
+  int rc = check_common(fn, batch, n, bandwidth == 1 ? 2 : 3, ld, layout);
+  if (rc) return rc;
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(sub1 && main && sup1 && rcond && (bandwidth == 1 || (sub2 && sup2)),
+             "%s: null array pointer", fn);
+  const size_t need = bx::rcond_workspace_bytes(bandwidth, batch, n);
+  if (workspace_bytes < need || !workspace) {
+    set_error("%s: workspace %zu bytes < required %zu", fn, workspace_bytes, need);
+    return BX_ERR_WORKSPACE;
+  }
+  bx::rcond_band(bandwidth, sub2, sub1, main, sup1, sup2, rcond, status, index,
+                 (double *)workspace, batch, n, ld, layout, (cudaStream_t)stream);
+  return bxh::check_launch(fn);
+}
+
 static int check_sip_args(const char *fn, int64_t batch, int64_t n, int64_t m, double alpha,
                           int64_t ld, int32_t layout) {
   int rc = check_common(fn, batch, n, 3, ld, layout);

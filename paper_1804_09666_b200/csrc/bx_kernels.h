@@ -73,6 +73,12 @@ int det_band(int kind, const double *c, const double *d, const double *e, const 
              int32_t *subs, int64_t batch, int64_t n, int64_t ld, int layout,
              cudaStream_t stream);
 
+// bx_rcond.cu (kind 1 = tridiagonal, 2 = pentadiagonal)
+size_t rcond_workspace_bytes(int kind, int64_t batch, int64_t n);
+int rcond_band(int kind, const double *c, const double *d, const double *e, const double *f,
+               const double *g, double *rcond, int32_t *st, int32_t *ix, double *ws,
+               int64_t batch, int64_t n, int64_t ld, int layout, cudaStream_t stream);
+
 // bx_hb.cu / bx_hb_host.cu
 size_t hb_dense_bytes(int64_t batch, int64_t n);
 int64_t hb_padded(int64_t n);

@@ -1,0 +1,248 @@
+// Reciprocal 1-norm condition estimate of banded systems (SURVEY 8f row f1:
+// the condition gate that accompanies exact_det_band; SURVEY H7 asks for the
+// per-system error to be reported with a condition estimate).
+//
+// LAPACK convention (dgtcon / dgbcon with norm = '1'):
+//     rcond = 1 / (||A||_1 * est(||A^-1||_1)),
+// A = P L U by banded Gaussian elimination with partial pivoting (U bandwidth
+// 2K), est by Higham's modification of Hager's method (LAPACK dlacn2): at most
+// five sign-vector iterations of A^-1 x / A^-T x plus the alternating-sign
+// lower bound.  One thread per system; the factors, the iterate and the sign
+// vector live in a [plane][n][batch] workspace (coalesced across systems).
+#include <math.h>
+
+#include "bx_common.cuh"
+#include "bx_kernels.h"
+
+namespace bx {
+namespace rc {
+
+template <int K>
+struct Planes {
+  static constexpr int W = 2 * K + 1;           // U row: columns k .. k+2K
+  static constexpr int U0 = 0, L0 = W, PIV = W + K, X = W + K + 1, SG = W + K + 2;
+  static constexpr int N = W + K + 3;
+};
+
+template <int K, class Lay>
+__global__ void rcond_kernel(const double *__restrict__ cp, const double *__restrict__ dp,
+                             const double *__restrict__ ep, const double *__restrict__ fp,
+                             const double *__restrict__ gp, double *__restrict__ rcond,
+                             int32_t *status, int32_t *index, double *ws, int64_t batch,
+                             int64_t n, Lay lay) {
+  using P = Planes<K>;
+  constexpr int W = P::W;
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= batch) return;
+  const int64_t pl = batch * n;
+  auto Wsp = [&](int p, int64_t k) -> double & { return ws[(int64_t)p * pl + k * batch + s]; };
+  // coefficient of A at (i, i+o), o in -K..K (0 outside the matrix)
+  auto A = [&](int64_t i, int o) -> double {
+    if (i < 0 || i >= n || i + o < 0 || i + o >= n) return 0.0;
+    if (K == 2) {
+      const double *d = o == -2 ? cp : o == -1 ? dp : o == 0 ? ep : o == 1 ? fp : gp;
+      return ldg(d + lay(i, s));
+    }
+    const double *d = o == -1 ? dp : o == 0 ? ep : fp;
+    return ldg(d + lay(i, s));
+  };
+  // ||A||_1: max column sum
+  double anorm = 0.0;
+  for (int64_t c = 0; c < n; ++c) {
+    double cs = 0.0;
+#pragma unroll
+    for (int o = -K; o <= K; ++o) cs += fabs(A(c + o, -o));
+    anorm = cs > anorm || cs != cs ? cs : anorm;
+  }
+  // ---- P L U (window of K+1 unreduced rows, columns k .. k+2K) ------------
+  double w[K + 1][W];
+  auto load_row = [&](int64_t i, double *row, int64_t k) {
+#pragma unroll
+    for (int c = 0; c < W; ++c) row[c] = 0.0;
+    if (i >= n) return;
+#pragma unroll
+    for (int o = -K; o <= K; ++o) {
+      const int c = (int)(i + o - k);
+      if (c >= 0 && c < W) row[c] = A(i, o);
+    }
+  };
+#pragma unroll
+  for (int j = 0; j <= K; ++j) load_row(j, w[j], 0);
+  bool singular = false;
+  int64_t zrow = -1;
+  for (int64_t k = 0; k < n; ++k) {
+    int p = 0;
+    double best = fabs(w[0][0]);
+#pragma unroll
+    for (int j = 1; j <= K; ++j)
+      if (k + j < n && fabs(w[j][0]) > best) { best = fabs(w[j][0]); p = j; }
+    if (best == 0.0 && !singular) { singular = true; zrow = k; }
+#pragma unroll
+    for (int j = 1; j <= K; ++j)
+      if (j == p) {
+#pragma unroll
+        for (int c = 0; c < W; ++c) { const double tmp = w[0][c]; w[0][c] = w[j][c]; w[j][c] = tmp; }
+      }
+    const double piv = w[0][0];
+#pragma unroll
+    for (int j = 1; j <= K; ++j) {
+      const double mlt = piv != 0.0 ? w[j][0] / piv : 0.0;
+      Wsp(P::L0 + j - 1, k) = mlt;
+#pragma unroll
+      for (int c = 1; c < W; ++c) w[j][c] = fma(-mlt, w[0][c], w[j][c]);
+    }
+#pragma unroll
+    for (int c = 0; c < W; ++c) Wsp(P::U0 + c, k) = w[0][c];
+    Wsp(P::PIV, k) = (double)p;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+#pragma unroll
+      for (int c = 0; c < W - 1; ++c) w[j][c] = w[j + 1][c + 1];
+      w[j][W - 1] = 0.0;
+    }
+    load_row(k + 1 + K, w[K], k + 1);
+  }
+  if (singular || anorm == 0.0) {  // LAPACK: rcond = 0 for an exactly singular U
+    rcond[s] = 0.0;
+    set_status(status, index, s, singular ? BX_STATUS_SINGULAR : BX_STATUS_OK,
+               singular ? (int32_t)zrow : -1);
+    return;
+  }
+  // ---- x := A^-1 x (trans = 0) or A^-T x (trans = 1), in place on plane X --
+  auto solve = [&](int trans) {
+    if (!trans) {
+      for (int64_t k = 0; k < n; ++k) {  // L: row swaps + eliminations
+        const int p = (int)Wsp(P::PIV, k);
+        double xk = Wsp(P::X, k);
+        if (p) { const double t = Wsp(P::X, k + p); Wsp(P::X, k + p) = xk; xk = t; Wsp(P::X, k) = xk; }
+#pragma unroll
+        for (int j = 1; j <= K; ++j)
+          if (k + j < n) Wsp(P::X, k + j) = fma(-Wsp(P::L0 + j - 1, k), xk, Wsp(P::X, k + j));
+      }
+      for (int64_t k = n - 1; k >= 0; --k) {  // U back substitution
+        double acc = Wsp(P::X, k);
+#pragma unroll
+        for (int c = 1; c < W; ++c)
+          if (k + c < n) acc = fma(-Wsp(P::U0 + c, k), Wsp(P::X, k + c), acc);
+        Wsp(P::X, k) = acc / Wsp(P::U0, k);
+      }
+    } else {
+      for (int64_t k = 0; k < n; ++k) {  // U^T forward
+        double acc = Wsp(P::X, k);
+#pragma unroll
+        for (int c = 1; c < W; ++c)
+          if (k - c >= 0) acc = fma(-Wsp(P::U0 + c, k - c), Wsp(P::X, k - c), acc);
+        Wsp(P::X, k) = acc / Wsp(P::U0, k);
+      }
+      for (int64_t k = n - 1; k >= 0; --k) {  // L^T backward, swaps undone in reverse
+        double xk = Wsp(P::X, k);
+#pragma unroll
+        for (int j = 1; j <= K; ++j)
+          if (k + j < n) xk = fma(-Wsp(P::L0 + j - 1, k), Wsp(P::X, k + j), xk);
+        const int p = (int)Wsp(P::PIV, k);
+        if (p) { Wsp(P::X, k) = Wsp(P::X, k + p); Wsp(P::X, k + p) = xk; }
+        else Wsp(P::X, k) = xk;
+      }
+    }
+  };
+  auto asum = [&]() {
+    double a = 0.0;
+    for (int64_t k = 0; k < n; ++k) a += fabs(Wsp(P::X, k));
+    return a;
+  };
+  auto iamax = [&]() {  // first index of max |x|
+    int64_t j = 0;
+    double b = -1.0;
+    for (int64_t k = 0; k < n; ++k) {
+      const double v = fabs(Wsp(P::X, k));
+      if (v > b) { b = v; j = k; }
+    }
+    return j;
+  };
+  auto unit = [&](int64_t j) {
+    for (int64_t k = 0; k < n; ++k) Wsp(P::X, k) = k == j ? 1.0 : 0.0;
+  };
+  // ---- dlacn2 (norm '1': kase 1 = A^-1 x, kase 2 = A^-T x) ---------------
+  for (int64_t k = 0; k < n; ++k) Wsp(P::X, k) = 1.0 / (double)n;
+  solve(0);
+  double est;
+  if (n == 1) {
+    est = fabs(Wsp(P::X, 0));
+  } else {
+    est = asum();
+    for (int64_t k = 0; k < n; ++k) {
+      const double sg = Wsp(P::X, k) >= 0.0 ? 1.0 : -1.0;
+      Wsp(P::X, k) = sg;
+      Wsp(P::SG, k) = sg;
+    }
+    solve(1);
+    int64_t j = iamax();
+    int iter = 2;
+    while (true) {
+      unit(j);
+      solve(0);
+      const double estold = est;
+      est = asum();
+      bool same = true;
+      for (int64_t k = 0; k < n && same; ++k)
+        same = (Wsp(P::X, k) >= 0.0 ? 1.0 : -1.0) == Wsp(P::SG, k);
+      if (same || est <= estold) break;  // repeated sign vector / no increase (dlacn2 70-90)
+      for (int64_t k = 0; k < n; ++k) {
+        const double sg = Wsp(P::X, k) >= 0.0 ? 1.0 : -1.0;
+        Wsp(P::X, k) = sg;
+        Wsp(P::SG, k) = sg;
+      }
+      solve(1);
+      const int64_t jlast = j;
+      j = iamax();
+      if (Wsp(P::X, jlast) != fabs(Wsp(P::X, j)) && iter < 5) {
+        ++iter;
+        continue;
+      }
+      break;
+    }
+    // alternating-sign lower bound
+    double alt = 1.0;
+    for (int64_t k = 0; k < n; ++k) {
+      Wsp(P::X, k) = alt * (1.0 + (double)k / (double)(n - 1));
+      alt = -alt;
+    }
+    solve(0);
+    const double temp = 2.0 * (asum() / (double)(3 * n));
+    if (temp > est) est = temp;
+  }
+  rcond[s] = est != 0.0 ? (1.0 / est) / anorm : 0.0;
+  set_status(status, index, s, BX_STATUS_OK, -1);
+}
+
+}  // namespace rc
+
+size_t rcond_workspace_bytes(int kind, int64_t batch, int64_t n) {
+  const int planes = kind == 1 ? rc::Planes<1>::N : rc::Planes<2>::N;
+  return sizeof(double) * (size_t)planes * (size_t)batch * (size_t)n;
+}
+
+int rcond_band(int kind, const double *c, const double *d, const double *e, const double *f,
+               const double *g, double *rcond, int32_t *st, int32_t *ix, double *ws,
+               int64_t batch, int64_t n, int64_t ld, int layout, cudaStream_t stream) {
+  const int threads = 32;
+  const dim3 grid((unsigned)((batch + threads - 1) / threads));
+  if (kind == 1) {
+    if (layout == BX_LAYOUT_INTERLEAVED)
+      rc::rcond_kernel<1><<<grid, threads, 0, stream>>>(c, d, e, f, g, rcond, st, ix, ws, batch, n,
+                                                       Interleaved{ld});
+    else
+      rc::rcond_kernel<1><<<grid, threads, 0, stream>>>(c, d, e, f, g, rcond, st, ix, ws, batch, n,
+                                                       SystemMajor{ld});
+  } else {
+    if (layout == BX_LAYOUT_INTERLEAVED)
+      rc::rcond_kernel<2><<<grid, threads, 0, stream>>>(c, d, e, f, g, rcond, st, ix, ws, batch, n,
+                                                       Interleaved{ld});
+    else
+      rc::rcond_kernel<2><<<grid, threads, 0, stream>>>(c, d, e, f, g, rcond, st, ix, ws, batch, n,
+                                                       SystemMajor{ld});
+  }
+  return BX_OK;
+}
+
+}  // namespace bx

@@ -162,3 +162,27 @@ def exact_det_band(a, counter=None):
             raise exception_for(st, int(index[0]))
         return res.to_fraction(0)
     return res
+
+
+def rcond_band(a):
+    """Reciprocal 1-norm condition estimate of every system, LAPACK's
+    convention (dgtcon / dgbcon, norm '1'): the condition
+    gate next to exact_det_band, against which config-3 errors are read
+    (SURVEY H7).  Single system: a float (0.0 when exactly singular);
+    batched: (rcond (B,), status, index) device tensors."""
+    if isinstance(a, TriMatrix):
+        bw, diags = 1, (None,) + tuple(a.rowaligned()) + (None,)
+    elif isinstance(a, PentaMatrix):
+        bw, diags = 2, tuple(a.rowaligned())
+    else:
+        raise TypeError("expected a TriMatrix or PentaMatrix")
+    dev = a.device
+    rc = torch.empty(a.batch, dtype=torch.float64, device=dev)
+    status = torch.empty(a.batch, dtype=torch.int32, device=dev)
+    index = torch.empty(a.batch, dtype=torch.int32, device=dev)
+    ws = workspace(_lib.lib().bx_rcond_workspace_bytes(bw, a.batch, a.n), dev)
+    _lib.call("bx_rcond_band_f64", bw, *(ptr(d) for d in diags), ptr(rc), ptr(status), ptr(index),
+              a.batch, a.n, a.ld, a.layout, ptr(ws), ws.numel(), stream_handle())
+    if a.single:
+        return float(rc[0])
+    return rc, status, index
