@@ -677,12 +677,28 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
   if (producer && lane == 0 && blockIdx.x < 64) { g_sip_trace[blockIdx.x][37] = tr_wait; g_sip_trace[blockIdx.x][38] = tr_issue; }
 #endif
   SIP_TR(39);
-  // ---- outputs in the caller's layout
-  for (int64_t t = 0; t < T; ++t) {
-    if (!valid_cell(t)) continue;
-    const int64_t i = (t - q) * m + q;
-    xout[lay(i, s)] = *(S.at(XP[cur], s, t) + q);
-    if (best_x) best_x[lay(i, s)] = *(S.at(XP[best_loc], s, t) + q);
+  // ---- outputs in the caller's layout: column q's cells (p, q), slice p + q;
+  // eight loads in flight per thread (one at a time left the loop latency-bound)
+  if (q < m) {
+    const double *xc = S.at(XP[cur], s, 0) + q, *xb = S.at(XP[best_loc], s, 0) + q;
+    constexpr int U = 8;
+    for (int64_t p0 = 0; p0 < R; p0 += U) {
+      double v[U], w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t p = p0 + u;
+        v[u] = p < R ? xc[(p + q) * S.mp] : 0.0;
+        w[u] = (best_x && p < R) ? xb[(p + q) * S.mp] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t p = p0 + u;
+        if (p >= R) break;
+        const int64_t i = p * m + q;
+        xout[lay(i, s)] = v[u];
+        if (best_x) best_x[lay(i, s)] = w[u];
+      }
+    }
   }
   if (q == 0) {
     if (iters) iters[s] = k;
