@@ -169,19 +169,60 @@ struct Det {
   }
 };
 
+// ---- per-thread row staging: every pass walks one system's rows in order
+// with a dependent chain per row, so each row's inputs are fetched DS rows
+// ahead with cp.async into a shared-memory ring [DS][NV][32 threads] and
+// read back after cp.async.wait_group (no global latency on the chain).
+constexpr int DS = 8;
+constexpr int NVMAX = 6;
+struct Stage {
+  double *sm;  // this block's ring: DS slots x NVMAX values x 32 threads
+  int tid;
+  __device__ __forceinline__ double *slot(int64_t row, int v) const {
+    return sm + ((int)(row % DS) * NVMAX + v) * 32 + tid;
+  }
+  // value v of `row` from global address g (nullptr: the value is zero)
+  __device__ __forceinline__ void put(int64_t row, int v, const double *g) const {
+    double *d = slot(row, v);
+    if (g)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(d)),
+                   "l"(g)
+                   : "memory");
+    else
+      *d = 0.0;
+  }
+  __device__ __forceinline__ void commit() const { asm volatile("cp.async.commit_group;" ::: "memory"); }
+  __device__ __forceinline__ void wait() const {  // the oldest of DS-1 groups in flight landed
+    asm volatile("cp.async.wait_group %0;" ::"n"(DS - 1) : "memory");
+  }
+  __device__ __forceinline__ double get(int64_t row, int v) const { return *slot(row, v); }
+};
+
 // ---- pass 1: the reference pivot recurrence with t-substitution ----------
 template <class Lay>
 __device__ void tri_pivots(const double *dp, const double *ep, const double *fp, int64_t s,
-                           int64_t n, Lay lay, int &nsub, int &ordsum, bool &ovf, Det *det = nullptr) {
+                           int64_t n, Lay lay, int &nsub, int &ordsum, bool &ovf,
+                           const Stage &sg, Det *det = nullptr) {
+  auto stage = [&](int64_t i) {  // e_i, d_i, f_{i-1}
+    if (i < n) {
+      sg.put(i, 0, ep + lay(i, s));
+      sg.put(i, 1, i >= 1 ? dp + lay(i, s) : nullptr);
+      sg.put(i, 2, i >= 1 ? fp + lay(i - 1, s) : nullptr);
+    }
+    sg.commit();
+  };
+  for (int64_t i = 0; i < DS - 1; ++i) stage(i);
   LS rec = ls_const(0.0);
   for (int64_t i = 0; i < n; ++i) {
-    const double e = ldg(ep + lay(i, s));
+    stage(i + DS - 1);
+    sg.wait();
+    const double e = sg.get(i, 0);
     LS mu;
     if (i == 0) {
       mu = ls_const(e);
     } else {
-      const LS l = ls_scale(ldg(dp + lay(i, s)), rec);                 // l = d * rec (_elim.py:104)
-      mu = ls_sub(ls_const(e), ls_scale(ldg(fp + lay(i - 1, s)), l));  // e - l f    (_elim.py:105)
+      const LS l = ls_scale(sg.get(i, 1), rec);                        // l = d * rec (_elim.py:104)
+      mu = ls_sub(ls_const(e), ls_scale(sg.get(i, 2), l));             // e - l f    (_elim.py:105)
     }
     ls_clamp_below(mu, -ordsum);
     const int z = ls_zero(mu);
@@ -196,25 +237,39 @@ __device__ void tri_pivots(const double *dp, const double *ep, const double *fp,
 template <class Lay>
 __device__ void penta_pivots(const double *cp, const double *dp, const double *ep,
                              const double *fp, const double *gp, int64_t s, int64_t n, Lay lay,
-                             int &nsub, int &ordsum, bool &ovf, Det *det = nullptr) {
+                             int &nsub, int &ordsum, bool &ovf, const Stage &sg,
+                             Det *det = nullptr) {
+  auto stage = [&](int64_t i) {  // e, f, g, d, c of row i
+    if (i < n) {
+      sg.put(i, 0, ep + lay(i, s));
+      sg.put(i, 1, i <= n - 2 ? fp + lay(i, s) : nullptr);
+      sg.put(i, 2, i <= n - 3 ? gp + lay(i, s) : nullptr);
+      sg.put(i, 3, i >= 1 ? dp + lay(i, s) : nullptr);
+      sg.put(i, 4, i >= 2 ? cp + lay(i, s) : nullptr);
+    }
+    sg.commit();
+  };
+  for (int64_t i = 0; i < DS - 1; ++i) stage(i);
   // carried: 1/mu and phi of rows i-1, i-2; psi = g (scalar)
   LS r1 = ls_const(0.0), r2 = ls_const(0.0), ph1 = ls_const(0.0), ph2 = ls_const(0.0);
   double ps1 = 0.0, ps2 = 0.0;
   for (int64_t i = 0; i < n; ++i) {
-    const double e = ldg(ep + lay(i, s));
-    const double f = i <= n - 2 ? ldg(fp + lay(i, s)) : 0.0;
-    const double g = i <= n - 3 ? ldg(gp + lay(i, s)) : 0.0;
+    stage(i + DS - 1);
+    sg.wait();
+    const double e = sg.get(i, 0);
+    const double f = sg.get(i, 1);
+    const double g = sg.get(i, 2);
     LS mu, ph;
     if (i == 0) {
       mu = ls_const(e);
       ph = ls_const(f);
     } else if (i == 1) {
-      const LS l1 = ls_scale(ldg(dp + lay(i, s)), r1);                 // d0 / mu0 (_elim.py:47)
+      const LS l1 = ls_scale(sg.get(i, 3), r1);                        // d0 / mu0 (_elim.py:47)
       mu = ls_sub(ls_const(e), ls_mul(l1, ph1, &ovf));
       ph = ls_sub(ls_const(f), ls_scale(ps1, l1));
     } else {
-      const LS l2 = ls_scale(ldg(cp + lay(i, s)), r2);                 // c / mu_{i-2}   (54)
-      const LS l1 = ls_mul(ls_sub(ls_const(ldg(dp + lay(i, s))), ls_mul(l2, ph2, &ovf)), r1,
+      const LS l2 = ls_scale(sg.get(i, 4), r2);                        // c / mu_{i-2}   (54)
+      const LS l1 = ls_mul(ls_sub(ls_const(sg.get(i, 3)), ls_mul(l2, ph2, &ovf)), r1,
                            &ovf);                                       // (d - l2 phi)/mu (55)
       mu = ls_sub(ls_sub(ls_const(e), ls_scale(ps2, l2)), ls_mul(l1, ph1, &ovf));  // (56)
       ph = i <= n - 2 ? ls_sub(ls_const(f), ls_scale(ps1, l1)) : ls_const(0.0);  // (60)
@@ -240,34 +295,46 @@ __device__ void penta_pivots(const double *cp, const double *dp, const double *e
 template <int K, class Lay>
 __device__ bool gbsv(const double *cp, const double *dp, const double *ep, const double *fp,
                      const double *gp, const double *bp, double *xp, double *ws, int64_t s,
-                     int64_t batch, int64_t n, Lay lay) {
+                     int64_t batch, int64_t n, Lay lay, const Stage &sg) {
   constexpr int W = 2 * K + 1;
   double w[K + 1][W], rb[K + 1];
+  // rows are fetched in increasing order, each staged DS-1 fetches ahead
+  auto stage_row = [&](int64_t i) {  // coefficients at offsets -K..K, then the rhs
+    if (i < n) {
+      if (K == 2) {
+        sg.put(i, 0, i >= 2 ? cp + lay(i, s) : nullptr);
+        sg.put(i, 1, i >= 1 ? dp + lay(i, s) : nullptr);
+        sg.put(i, 2, ep + lay(i, s));
+        sg.put(i, 3, i <= n - 2 ? fp + lay(i, s) : nullptr);
+        sg.put(i, 4, i <= n - 3 ? gp + lay(i, s) : nullptr);
+      } else {
+        sg.put(i, 0, i >= 1 ? dp + lay(i, s) : nullptr);
+        sg.put(i, 1, ep + lay(i, s));
+        sg.put(i, 2, i <= n - 2 ? fp + lay(i, s) : nullptr);
+      }
+      sg.put(i, W, bp + lay(i, s));
+    }
+    sg.commit();
+  };
+  for (int64_t i = 0; i < DS - 1; ++i) stage_row(i);
   auto load_row = [&](int64_t i, double *row, double &rhs, int64_t k) {
     // row i, columns k .. k+2K; entries at columns i-K .. i+K
+    stage_row(i + DS - 1);
+    sg.wait();
 #pragma unroll
     for (int c = 0; c < W; ++c) row[c] = 0.0;
     rhs = 0.0;
     if (i >= n) return;
     const int sh = (int)(i - k);  // column i-K sits at offset sh - K
     double v[2 * K + 1];
-    if (K == 2) {
-      v[0] = i >= 2 ? ldg(cp + lay(i, s)) : 0.0;
-      v[1] = i >= 1 ? ldg(dp + lay(i, s)) : 0.0;
-      v[2] = ldg(ep + lay(i, s));
-      v[3] = i <= n - 2 ? ldg(fp + lay(i, s)) : 0.0;
-      v[4] = i <= n - 3 ? ldg(gp + lay(i, s)) : 0.0;
-    } else {
-      v[0] = i >= 1 ? ldg(dp + lay(i, s)) : 0.0;
-      v[1] = ldg(ep + lay(i, s));
-      v[2] = i <= n - 2 ? ldg(fp + lay(i, s)) : 0.0;
-    }
+#pragma unroll
+    for (int o = 0; o < 2 * K + 1; ++o) v[o] = sg.get(i, o);
 #pragma unroll
     for (int o = 0; o < 2 * K + 1; ++o) {
       const int c = sh - K + o;
       if (c >= 0 && c < W) row[c] = v[o];
     }
-    rhs = ldg(bp + lay(i, s));
+    rhs = sg.get(i, W);
   };
 #pragma unroll
   for (int j = 0; j <= K; ++j) load_row(j, w[j], rb[j], 0);
@@ -309,15 +376,26 @@ __device__ bool gbsv(const double *cp, const double *dp, const double *ep, const
     }
     load_row(k + 1 + K, w[K], rb[K], k + 1);
   }
-  // back substitution x_k = (y_k - sum_c U[k][c] x_{k+c}) / U[k][0]
+  // back substitution x_k = (y_k - sum_c U[k][c] x_{k+c}) / U[k][0]; the U
+  // rows + y are staged DS-1 rows ahead (descending) like the inputs
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  auto stage_back = [&](int64_t k) {
+    if (k >= 0)
+#pragma unroll
+      for (int c = 0; c <= W; ++c) sg.put(k, c, ws + (int64_t)c * plane + k * batch + s);
+    sg.commit();
+  };
+  for (int64_t j = 0; j < DS - 1; ++j) stage_back(n - 1 - j);
   double xs[W];  // x_{k+1} .. x_{k+2K} (xs[1..2K])
 #pragma unroll
   for (int c = 0; c < W; ++c) xs[c] = 0.0;
   for (int64_t k = n - 1; k >= 0; --k) {
-    double acc = ws[(int64_t)W * plane + k * batch + s];
+    stage_back(k - (DS - 1));
+    sg.wait();
+    double acc = sg.get(k, W);
 #pragma unroll
-    for (int c = 1; c < W; ++c) acc = fma(-ws[(int64_t)c * plane + k * batch + s], xs[c], acc);
-    const double xk = acc / ws[k * batch + s];
+    for (int c = 1; c < W; ++c) acc = fma(-sg.get(k, c), xs[c], acc);
+    const double xk = acc / sg.get(k, 0);
 #pragma unroll
     for (int c = W - 1; c >= 2; --c) xs[c] = xs[c - 1];
     xs[1] = xk;
@@ -326,32 +404,46 @@ __device__ bool gbsv(const double *cp, const double *dp, const double *ep, const
   return true;
 }
 
+// The pivot pass and the pivoted solve are independent until the status, so
+// they run on two thread sets of one launch (even blocks: pass 1, odd blocks:
+// pass 2 -- twice the warps, the passes overlap); exact_finish combines.
 template <int K, class Lay>
 __global__ void exact_kernel(const double *__restrict__ cp, const double *__restrict__ dp,
                              const double *__restrict__ ep, const double *__restrict__ fp,
                              const double *__restrict__ gp, const double *__restrict__ bp,
-                             double *__restrict__ xp, int32_t *status, int32_t *index,
-                             int32_t *subs, double *ws, int64_t batch, int64_t n, Lay lay) {
+                             double *__restrict__ xp, int32_t *subs, int32_t *gate,
+                             int32_t *solved, double *ws, int64_t batch, int64_t n, Lay lay) {
+  extern __shared__ double stage_sm[];
+  const Stage sg{stage_sm, (int)threadIdx.x};
+  const int role = blockIdx.x & 1;
+  const int64_t s = (int64_t)(blockIdx.x >> 1) * blockDim.x + threadIdx.x;
+  if (s >= batch) return;
+  if (role == 0) {
+    int nsub = 0, ordsum = 0;
+    bool ovf = false;
+    if (K == 1) tri_pivots(dp, ep, fp, s, n, lay, nsub, ordsum, ovf, sg);
+    else penta_pivots(cp, dp, ep, fp, gp, s, n, lay, nsub, ordsum, ovf, sg);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (subs) subs[s] = nsub;
+    // WINDOW_OVERFLOW, or exact_det_band == 0 -> SingularMatrix (exact.py:287-288, 301-302)
+    gate[s] = ovf ? BX_STATUS_WINDOW_OVERFLOW : ordsum > 0 ? BX_STATUS_SINGULAR : BX_STATUS_OK;
+  } else {
+    const bool ok = gbsv<K>(cp, dp, ep, fp, gp, bp, xp, ws, s, batch, n, lay, sg);
+    solved[s] = ok ? BX_STATUS_OK : BX_STATUS_SINGULAR;
+  }
+}
+
+template <class Lay>
+__global__ void exact_finish(const int32_t *gate, const int32_t *solved, double *xp,
+                             int32_t *status, int32_t *index, int64_t batch, int64_t n, Lay lay) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= batch) return;
-  int nsub = 0, ordsum = 0;
-  bool ovf = false;
-  if (K == 1) tri_pivots(dp, ep, fp, s, n, lay, nsub, ordsum, ovf);
-  else penta_pivots(cp, dp, ep, fp, gp, s, n, lay, nsub, ordsum, ovf);
-  if (subs) subs[s] = nsub;
-  const double nan = __longlong_as_double(0x7ff8000000000000LL);
-  if (ovf) {
-    set_status(status, index, s, BX_STATUS_WINDOW_OVERFLOW, -1);
+  const int32_t g = gate[s];
+  set_status(status, index, s, g != BX_STATUS_OK ? g : solved[s], -1);
+  if (g != BX_STATUS_OK) {
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
     for (int64_t i = 0; i < n; ++i) xp[lay(i, s)] = nan;
-    return;
   }
-  if (ordsum > 0) {  // exact_det_band == 0 -> SingularMatrix (exact.py:287-288, 301-302)
-    set_status(status, index, s, BX_STATUS_SINGULAR, -1);
-    for (int64_t i = 0; i < n; ++i) xp[lay(i, s)] = nan;
-    return;
-  }
-  const bool ok = gbsv<K>(cp, dp, ep, fp, gp, bp, xp, ws, s, batch, n, lay);
-  set_status(status, index, s, ok ? BX_STATUS_OK : BX_STATUS_SINGULAR, -1);
 }
 
 // exact_det_band (exact.py:254-275): det(A) = lim_{t->0} prod mu_i(t).  The
@@ -363,13 +455,16 @@ __global__ void det_kernel(const double *__restrict__ cp, const double *__restri
                            const double *__restrict__ gp, double *mant, int64_t *expo,
                            int32_t *status, int32_t *index, int32_t *subs, int64_t batch,
                            int64_t n, Lay lay) {
+  extern __shared__ double stage_sm[];
+  const Stage sg{stage_sm, (int)threadIdx.x};
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= batch) return;
   int nsub = 0, ordsum = 0;
   bool ovf = false;
   Det det;
-  if (K == 1) tri_pivots(dp, ep, fp, s, n, lay, nsub, ordsum, ovf, &det);
-  else penta_pivots(cp, dp, ep, fp, gp, s, n, lay, nsub, ordsum, ovf, &det);
+  if (K == 1) tri_pivots(dp, ep, fp, s, n, lay, nsub, ordsum, ovf, sg, &det);
+  else penta_pivots(cp, dp, ep, fp, gp, s, n, lay, nsub, ordsum, ovf, sg, &det);
+  asm volatile("cp.async.wait_all;" ::: "memory");
   if (subs) subs[s] = nsub;
   if (ovf) {
     mant[s] = __longlong_as_double(0x7ff8000000000000LL);
@@ -384,6 +479,8 @@ __global__ void det_kernel(const double *__restrict__ cp, const double *__restri
 
 }  // namespace ex
 
+static constexpr size_t kStageBytes = sizeof(double) * ex::DS * ex::NVMAX * 32;
+
 int det_band(int kind, const double *c, const double *d, const double *e, const double *f,
              const double *g, double *mant, int64_t *expo, int32_t *st, int32_t *ix,
              int32_t *subs, int64_t batch, int64_t n, int64_t ld, int layout,
@@ -392,17 +489,17 @@ int det_band(int kind, const double *c, const double *d, const double *e, const 
   const dim3 grid((unsigned)((batch + threads - 1) / threads));
   if (kind == 1) {
     if (layout == BX_LAYOUT_INTERLEAVED)
-      ex::det_kernel<1><<<grid, threads, 0, stream>>>(c, d, e, f, g, mant, expo, st, ix, subs,
+      ex::det_kernel<1><<<grid, threads, kStageBytes, stream>>>(c, d, e, f, g, mant, expo, st, ix, subs,
                                                      batch, n, Interleaved{ld});
     else
-      ex::det_kernel<1><<<grid, threads, 0, stream>>>(c, d, e, f, g, mant, expo, st, ix, subs,
+      ex::det_kernel<1><<<grid, threads, kStageBytes, stream>>>(c, d, e, f, g, mant, expo, st, ix, subs,
                                                      batch, n, SystemMajor{ld});
   } else {
     if (layout == BX_LAYOUT_INTERLEAVED)
-      ex::det_kernel<2><<<grid, threads, 0, stream>>>(c, d, e, f, g, mant, expo, st, ix, subs,
+      ex::det_kernel<2><<<grid, threads, kStageBytes, stream>>>(c, d, e, f, g, mant, expo, st, ix, subs,
                                                      batch, n, Interleaved{ld});
     else
-      ex::det_kernel<2><<<grid, threads, 0, stream>>>(c, d, e, f, g, mant, expo, st, ix, subs,
+      ex::det_kernel<2><<<grid, threads, kStageBytes, stream>>>(c, d, e, f, g, mant, expo, st, ix, subs,
                                                      batch, n, SystemMajor{ld});
   }
   return BX_OK;
@@ -410,7 +507,8 @@ int det_band(int kind, const double *c, const double *d, const double *e, const 
 
 size_t exact_workspace_bytes(int kind, int64_t batch, int64_t n) {
   const int planes = kind == 1 ? 4 : 6;  // U row (2K+1) + y
-  return sizeof(double) * (size_t)planes * (size_t)batch * (size_t)n;
+  // + the two per-system outcomes (pivot pass gate, pivoted solve)
+  return sizeof(double) * (size_t)planes * (size_t)batch * (size_t)n + 2 * sizeof(int32_t) * (size_t)batch;
 }
 
 int exact_solve(int kind, const double *c, const double *d, const double *e, const double *f,
@@ -418,22 +516,23 @@ int exact_solve(int kind, const double *c, const double *d, const double *e, con
                 int32_t *subs, double *ws, int64_t batch, int64_t n, int64_t ld, int layout,
                 cudaStream_t stream) {
   const int threads = 32;
-  const dim3 grid((unsigned)((batch + threads - 1) / threads));
-  if (kind == 1) {
-    if (layout == BX_LAYOUT_INTERLEAVED)
-      ex::exact_kernel<1><<<grid, threads, 0, stream>>>(c, d, e, f, g, b, x, st, ix, subs, ws,
-                                                       batch, n, Interleaved{ld});
+  const unsigned nb = (unsigned)((batch + threads - 1) / threads);
+  const dim3 grid(2 * nb);  // even blocks: pivot pass, odd blocks: pivoted solve
+  const int planes = kind == 1 ? 4 : 6;
+  int32_t *gate = reinterpret_cast<int32_t *>(ws + (size_t)planes * (size_t)batch * (size_t)n);
+  int32_t *solved = gate + batch;
+  auto go = [&](auto lay) {
+    if (kind == 1)
+      ex::exact_kernel<1><<<grid, threads, kStageBytes, stream>>>(c, d, e, f, g, b, x, subs, gate,
+                                                                   solved, ws, batch, n, lay);
     else
-      ex::exact_kernel<1><<<grid, threads, 0, stream>>>(c, d, e, f, g, b, x, st, ix, subs, ws,
-                                                       batch, n, SystemMajor{ld});
-  } else {
-    if (layout == BX_LAYOUT_INTERLEAVED)
-      ex::exact_kernel<2><<<grid, threads, 0, stream>>>(c, d, e, f, g, b, x, st, ix, subs, ws,
-                                                       batch, n, Interleaved{ld});
-    else
-      ex::exact_kernel<2><<<grid, threads, 0, stream>>>(c, d, e, f, g, b, x, st, ix, subs, ws,
-                                                       batch, n, SystemMajor{ld});
-  }
+      ex::exact_kernel<2><<<grid, threads, kStageBytes, stream>>>(c, d, e, f, g, b, x, subs, gate,
+                                                                   solved, ws, batch, n, lay);
+    ex::exact_finish<<<(unsigned)((batch + 255) / 256), 256, 0, stream>>>(gate, solved, x, st, ix,
+                                                                          batch, n, lay);
+  };
+  if (layout == BX_LAYOUT_INTERLEAVED) go(Interleaved{ld});
+  else go(SystemMajor{ld});
   return BX_OK;
 }
 
