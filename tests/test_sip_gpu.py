@@ -108,7 +108,8 @@ def test_stencil_sip_matches_c_oracle(cuda, layout, m, rows, alpha):
 @pytest.mark.parametrize("algo", ["sequential", "wavefront"])
 @pytest.mark.parametrize("layout", LAYOUTS)
 @pytest.mark.parametrize("m,rows,alpha", [(2, 64, 0.0), (3, 20, 0.5), (8, 12, 0.0), (33, 9, 0.5),
-                                          (64, 40, 0.5)])
+                                          (64, 40, 0.5), (64, 70, 0.0), (128, 20, 0.5),
+                                          (256, 6, 0.5), (128, 200, 0.5)])
 def test_algorithms_agree(cuda, algo, layout, m, rows, alpha):
     n = m * rows
     p = W.five_point(5, n, m, seed=9)
