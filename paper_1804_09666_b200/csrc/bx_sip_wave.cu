@@ -23,8 +23,6 @@
 #include <math.h>
 #include <stdlib.h>
 
-#include <algorithm>
-
 #include "bx_common.cuh"
 #include "bx_kernels.h"
 
@@ -548,42 +546,61 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
         F += 10 * Wt;
       }
     } else {
-      // lean per-step loop: rotating window pointers, incremental slice
-      // geometry, grid-form boundary tests (i = p m + q), 32-bit indices
+      // lean per-step loop: incremental slice geometry, grid-form boundary
+      // tests (i = p m + q), 32-bit indices.  The old iterate's 3x3 window
+      // (columns q-1..q+1, slices t-1..t+1) lives in registers, read from the
+      // staged plane row, so K x + b of the step is formed before the
+      // barrier; only y = v - l1 y(left) - l2 y(up) follows it.
       const bool live = q < m;
       double *py = S.at(PY, s, 0) + q;
-      if (live) xs[q] = valid_cell(0) ? *(S.at(xo, s, 0) + q) : 0.0;
+      auto x_at = [&](const double *row, int tt, int qq) -> double {  // 0 outside the grid
+        const int pp = tt - qq;
+        return (qq >= 0 && qq < mi_ && (unsigned)pp < (unsigned)Ri) ? row[qq] : 0.0;
+      };
+      const double *xrow0 = S.at(xo, s, 0);
+      double xm_l = 0.0, xm_c = 0.0;                       // slice t-1: q-1, q
+      double x0_l = x_at(xrow0, 0, q - 1), x0_c = x_at(xrow0, 0, q), x0_r = x_at(xrow0, 0, q + 1);
       double y_u = 0.0;  // own column, previous cell
       const bool qge1 = q >= 1, qlem2 = q <= mi_ - 2, qlast = q == mi_ - 1, qfirst = q == 0;
-      double *wm1 = xs + 3 * mi_, *w0 = xs, *wp1 = xs + mi_, *wp2 = xs + 2 * mi_;  // slices t-1..t+2
-      double *yprev = ys + mi_, *ycur = ys;                                       // slices t-1, t
+      double *yprev = ys + mi_, *ycur = ys;  // slices t-1, t
       const int stage_d = NPL * mp;
       int Wt = S.width(0), qlo_t = 0;
       for (int t = 0; t < Ti; ++t, py += mp) {
         const int stg = consume_wait();
         const double *stage = ring + stg * stage_d;
         const int p = t - q;
-        if (live && t + 1 < Ti) wp1[q] = ((unsigned)(p + 1) < (unsigned)Ri) ? stage[10 * mp + q] : 0.0;
-        cons_sync();
-        if (live && (unsigned)p < (unsigned)Ri) {
-          const double *rb = stage + (q - qlo_t);
-          const bool pge1 = p >= 1, plast = p == Ri - 1, phi_ok = p <= p_hi;
-          double acc = add(0.0, mul(rb[0], w0[q]));
+        double xp_l = 0.0, xp_c = 0.0, xp_r = 0.0;  // slice t+1: q-1, q, q+1
+        if (live && t + 1 < Ti) {
+          const double *xr = stage + 10 * mp;
+          xp_l = x_at(xr, t + 1, q - 1);
+          xp_c = x_at(xr, t + 1, q);
+          xp_r = x_at(xr, t + 1, q + 1);
+        }
+        const bool cell = live && (unsigned)p < (unsigned)Ri;
+        const double *rb = stage + (q - qlo_t);
+        const bool pge1 = p >= 1;
+        double v = 0.0;
+        if (cell) {
+          const bool plast = p == Ri - 1, phi_ok = p <= p_hi;
+          double acc = add(0.0, mul(rb[0], x0_c));
           if (pge1 || qge1) {                                   // i >= 1
-            if (qge1) acc = add(acc, mul(rb[Wt], wm1[q - 1]));
-            else if (M2) acc = add(acc, mul(rb[Wt], w0[q + 1]));
+            if (qge1) acc = add(acc, mul(rb[Wt], xm_l));
+            else if (M2) acc = add(acc, mul(rb[Wt], x0_r));
           }
           if (!(plast && qlast)) {                              // i <= n - 2
-            if (qlem2) acc = add(acc, mul(rb[2 * Wt], wp1[q + 1]));
-            else if (M2) acc = add(acc, mul(rb[2 * Wt], w0[q - 1]));
+            if (qlem2) acc = add(acc, mul(rb[2 * Wt], xp_r));
+            else if (M2) acc = add(acc, mul(rb[2 * Wt], x0_l));
           }
-          if (pge1) acc = add(acc, mul(rb[3 * Wt], wm1[q]));
-          if (phi_ok) acc = add(acc, mul(rb[4 * Wt], wp1[q]));
+          if (pge1) acc = add(acc, mul(rb[3 * Wt], xm_c));
+          if (phi_ok) acc = add(acc, mul(rb[4 * Wt], xp_c));
           if (!M2) {
-            if ((pge1 || qlast) && qlem2 && pge1) acc = add(acc, mul(rb[5 * Wt], w0[q + 1]));
-            if ((phi_ok || (plast && qfirst)) && qge1) acc = add(acc, mul(rb[6 * Wt], w0[q - 1]));
+            if ((pge1 || qlast) && qlem2 && pge1) acc = add(acc, mul(rb[5 * Wt], x0_r));
+            if ((phi_ok || (plast && qfirst)) && qge1) acc = add(acc, mul(rb[6 * Wt], x0_l));
           }
-          const double v = add(acc, rb[7 * Wt]);
+          v = add(acc, rb[7 * Wt]);
+        }
+        cons_sync();  // y of slice t-1 (yprev) written by the left neighbour
+        if (cell) {
           double y = v;
           if ((pge1 || qge1) && qge1) y = sub(y, mul(rb[8 * Wt], yprev[q - 1]));
           if (pge1) y = sub(y, mul(rb[9 * Wt], y_u));
@@ -594,7 +611,8 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
         consume_release();
         Wt = S.width(t + 1);
         qlo_t += t + 1 >= Ri ? 1 : 0;
-        double *tw = wm1; wm1 = w0; w0 = wp1; wp1 = wp2; wp2 = tw;
+        xm_l = x0_l; xm_c = x0_c;
+        x0_l = xp_l; x0_c = xp_c; x0_r = xp_r;
         double *ty = yprev; yprev = ycur; ycur = ty;
       }
       asm volatile("fence.proxy.async.global;" ::: "memory");  // y rows -> TMA reads below
@@ -729,685 +747,6 @@ __global__ void grid_check_kernel(const double *__restrict__ a1p, const double *
   }
 }
 
-// Per-half packed layout of the two-CTA kernel: slice t of half c holds the
-// valid cells (t-q, q) with q in [qlo(c,t), qhi(c,t)] (the half's columns),
-// rows of even width W(c,t); group blocks FG_c[t] (10 rows) and BG_c[t]
-// (3 rows of slice t, 6 rows of slice t+1) as in Skew, per half, so a CTA
-// streams one contiguous block (plus one plane row) per wavefront step.
-struct SkewH {
-  double *ws;
-  int64_t batch, m, T, mp, R, mh;
-  int64_t P0, P1;  // sum of the half widths
-  int64_t per_sys;
-  const int64_t *pw0, *pw1;  // pw_c[t] = sum of W(c, u) for u < t, t = 0..T
-  __device__ __forceinline__ int qlo(int c, int t) const {
-    const int g = t - (int)R + 1 > 0 ? t - (int)R + 1 : 0;
-    return g > c * (int)mh ? g : c * (int)mh;
-  }
-  __device__ __forceinline__ int qhi(int c, int t) const {  // inclusive
-    const int g = t < (int)m - 1 ? t : (int)m - 1;
-    const int h = c * (int)mh + (int)mh - 1;
-    return g < h ? g : h;
-  }
-  __device__ __forceinline__ int width(int c, int t) const {
-    if (t < 0 || t >= (int)T) return 0;
-    const int nv = qhi(c, t) - qlo(c, t) + 1;
-    return nv <= 0 ? 0 : nv + (nv & 1);
-  }
-  __device__ __forceinline__ const int64_t *pw(int c) const { return c ? pw1 : pw0; }
-  __device__ __forceinline__ double *fg(int64_t s, int c) const {
-    return ws + s * per_sys + (c ? 10 * P0 : 0);
-  }
-  __device__ __forceinline__ double *bg(int64_t s, int c) const {
-    return ws + s * per_sys + 10 * (P0 + P1) + (c ? 9 * P0 : 0);
-  }
-  __device__ __forceinline__ int64_t fg_off(int c, int t) const { return 10 * pw(c)[t]; }
-  __device__ __forceinline__ int64_t bg_off(int c, int t) const {
-    return t < 0 ? 0 : 3 * pw(c)[t] + 6 * pw(c)[t + 1];
-  }
-  __device__ __forceinline__ double *at(int p, int64_t s, int64_t t) const {
-    return ws + s * per_sys + 19 * (P0 + P1) + ((int64_t)(p - PY) * T + t) * mp;
-  }
-};
-
-__global__ void sip_prefix_h_kernel(SkewH S) {
-  if (threadIdx.x >= 2 || blockIdx.x != 0) return;
-  const int c = threadIdx.x;
-  int64_t acc = 0;
-  int64_t *pw = const_cast<int64_t *>(S.pw(c));
-  for (int t = 0; t <= (int)S.T; ++t) {
-    pw[t] = acc;
-    acc += S.width(c, t);
-  }
-}
-
-// sip_pack_kernel for the per-half layout
-template <class Lay>
-__global__ void __launch_bounds__(512)
-sip_pack_h_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
-                  const double *__restrict__ ep, const double *__restrict__ c1p,
-                  const double *__restrict__ c2p, const double *__restrict__ bp,
-                  const double *__restrict__ x0, SkewH S, int64_t n, int use_x0, Lay lay) {
-  const int t = blockIdx.x;
-  const int64_t s = blockIdx.y;
-  const int mi = (int)S.m, Ri = (int)S.R;
-  for (int q = threadIdx.x; q < mi; q += blockDim.x) {
-    const int p = t - q;
-    if ((unsigned)p >= (unsigned)Ri) continue;
-    const int c = q >= (int)S.mh;
-    const int64_t i = (int64_t)p * mi + q;
-    const int64_t li = lay(i, s);
-    const bool pge1 = p >= 1, ige1 = pge1 || q >= 1, ilen2 = !(p == Ri - 1 && q == mi - 1),
-               ple = p <= Ri - 2;
-    const int Wt = S.width(c, t), Wm = S.width(c, t - 1), qo = q - S.qlo(c, t);
-    double *ab = S.bg(s, c) + S.bg_off(c, t - 1) + 3 * Wm + qo;
-    const double bb = ldg(bp + li);
-    ab[0] = pge1 ? ldg(a2p + li) : 0.0;
-    ab[Wt] = ige1 ? ldg(a1p + li) : 0.0;
-    ab[2 * Wt] = ldg(ep + li);
-    ab[3 * Wt] = ilen2 ? ldg(c1p + li) : 0.0;
-    ab[4 * Wt] = ple ? ldg(c2p + li) : 0.0;
-    ab[5 * Wt] = bb;
-    S.fg(s, c)[S.fg_off(c, t) + 7 * Wt + qo] = bb;
-    *(S.at(PXA, s, t) + q) = use_x0 ? x0[li] : 0.0;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Two-CTA wavefront SIP (one cluster of two CTAs per system): CTA c owns the
-// grid columns [c*mh, (c+1)*mh), mh = m/2, so a system's wavefront steps run
-// on two SMs with half the cells, half the plane bytes and half the consumer
-// warps each (the one-CTA kernel is issue- and TMA-bound on one SM).  Same
-// per-cell operation sequence as sip_wave_kernel, so iterates, residuals and
-// iteration counts are the same bits.  The only couplings across the split
-// are single boundary values per step, sent over DSMEM through a mailbox:
-//   setup   : CTA 0 -> 1  mu, phi, psi of column mh-1 (left-neighbour factors)
-//   forward : CTA 0 -> 1  y of column mh-1
-//   backward: CTA 1 -> 0  x of columns mh, mh+1 and A, b of column mh (CTA 0
-//             also evaluates column mh's residual, whose left neighbour it owns)
-// The sending CTA never waits on the receiver except when the mailbox is full,
-// so the receiver runs a few steps behind and finds every message waiting.
-constexpr int RING2 = 16;  // mailbox slots
-constexpr int MSG = 8;     // doubles per message
-
-__device__ __forceinline__ unsigned peer_u32(const void *p, int peer) {
-  unsigned a;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(peer));
-  return a;
-}
-__device__ __forceinline__ void mbar_wait_cl(uint64_t *bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(unsigned bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-struct Mail {
-  double *box;      // [RING2][MSG] inbox, written by the peer with st.async
-  uint64_t *full;   // [RING2] inbox slot barriers (tx-counted, the receiver arms them)
-  volatile unsigned *credit;  // messages of mine the peer has consumed (it stores remotely)
-  int peer;
-  // st.async writes + complete_tx on the peer's barrier: no fences on the path;
-  // flow control by the relaxed credit the receiver stores back
-  __device__ __forceinline__ void send(unsigned seq, const double *v) const {
-    while (seq - *credit >= (unsigned)RING2) {
-    }
-    const int slot = (int)(seq % RING2);
-    const unsigned dst = peer_u32(box + slot * MSG, peer), bar = peer_u32(full + slot, peer);
-#pragma unroll
-    for (int i = 0; i < MSG; ++i)
-      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
-                       dst + 8u * (unsigned)i),
-                   "d"(v[i]), "r"(bar)
-                   : "memory");
-  }
-  __device__ __forceinline__ void recv(unsigned seq, double *v) const {
-    const int slot = (int)(seq % RING2);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(full + slot)),
-                 "r"((unsigned)(MSG * sizeof(double)))
-                 : "memory");
-    mbar_wait(full + slot, (seq / RING2) & 1u);
-    const volatile double *b = box + slot * MSG;
-#pragma unroll
-    for (int i = 0; i < MSG; ++i) v[i] = b[i];
-    const unsigned cr = peer_u32((const void *)credit, peer);
-    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cr), "r"(seq + 1) : "memory");
-  }
-};
-
-template <class Lay>
-__global__ void __launch_bounds__(288) sip_wave2_kernel(
-    const double *__restrict__ a2p, const double *__restrict__ a1p, const double *__restrict__ ep,
-    const double *__restrict__ c1p, const double *__restrict__ c2p, const double *__restrict__ bp,
-    const double *__restrict__ tol, double *__restrict__ xout, double *__restrict__ best_x,
-    int64_t *iters, double *res, double *best_res, int32_t *status, int32_t *index,
-    double *history, SkewH S, int64_t n, double alpha, int64_t max_iter, int use_x0, Lay lay,
-    int nst) {
-  extern __shared__ double sh[];
-  const int64_t m = S.m, R = n / m, T = S.T;
-  const int mi_ = (int)m, Ri = (int)R, Ti = (int)T, mh = (int)S.mh;
-  const int crank = (int)(blockIdx.x & 1), peer = crank ^ 1;
-  const int64_t s = blockIdx.x >> 1;
-  const int c0 = crank * mh;
-  const int ql = threadIdx.x;
-  const int q = c0 + ql;  // global grid column of a consumer thread
-  const int MW = mh + 4;  // window rows: 2 halo columns on each side
-  const int SW = mh + 4;  // ring stage row stride (even)
-  const bool bnd_send0 = crank == 0 && ql == mh - 1;  // CTA 0's last column
-  const bool bnd_recv1 = crank == 1 && ql == 0;       // CTA 1's first column
-  __shared__ int s_bad, s_notgrid, s_go, s_bestcopy;
-  __shared__ double s_red[32], s_xr;  // s_xr: the peer's partial maximum
-  if (ql == 0) { s_bad = 0x7fffffff; s_notgrid = 0; }
-  // mailbox behind the window + ring area
-  const size_t win = (size_t)11 * MW + 2;
-  const size_t ring_d = (size_t)nst * NPL * SW;
-  const size_t stg_d = (size_t)4 * 6 * mh;
-  double *area = sh + win;
-  double *mbox = area + (ring_d > stg_d ? ring_d : stg_d);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(mbox + RING2 * MSG);
-  __shared__ unsigned s_credit;
-  const Mail mail{mbox, bars, &s_credit, peer};
-  uint64_t *full = bars + 2 * RING2;
-  uint64_t *empty = full + nst;
-  if (ql == 0) {
-    s_credit = 0;
-    for (int i = 0; i < RING2; ++i) mbar_init(bars + i, 1);
-    for (int i = 0; i < nst; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, (mh + 31) / 32); }
-  }
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-  unsigned seq_tx = 0, seq_rx = 0;  // mailbox sequence numbers (boundary threads only)
-  auto cluster_sync = [&]() {
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-  };
-  // max over both CTAs of a block-uniform value v (all threads)
-  auto cluster_max = [&](double v) -> double {
-    if (ql == 0) {
-      const unsigned d = peer_u32(&s_xr, peer);
-      asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(d), "d"(v) : "memory");
-    }
-    cluster_sync();
-    const double o = *(volatile double *)&s_xr;
-    cluster_sync();  // s_xr may be overwritten by the next exchange only after both read
-    return nan_max(v, o);
-  };
-
-  // ---------------- setup: ILU(0)/Stone + defect on my columns ----------------
-  double rb0 = 0.0;
-  {
-    double *smu = sh + 2, *sphi = sh + 3 * MW + 2, *spsi = sh + 6 * MW + 2;  // [3][MW], halo 2
-    double *stg_in = area;  // [DS][6][mh]
-    constexpr int DS = 4;
-    const bool live = ql < mh;
-    const bool qge1 = q >= 1, qlast = q == mi_ - 1, qfirst = q == 0;
-    auto stage_cell = [&](int tt) {
-      const int pp = tt - q;
-      if (live && tt < Ti && (unsigned)pp < (unsigned)Ri) {
-        const int W1 = S.width(crank, tt), W0 = S.width(crank, tt - 1);
-        const double *src = S.bg(s, crank) + S.bg_off(crank, tt - 1) + 3 * W0 + (q - S.qlo(crank, tt));
-        const unsigned d = smem_u32(stg_in + ((tt % DS) * 6) * mh + ql);
-        const unsigned dm = (unsigned)(mh * sizeof(double));
-#pragma unroll
-        for (int a = 0; a < 6; ++a)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d + a * dm), "l"(src + a * W1)
-                       : "memory");
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    for (int tt = 0; tt < DS - 1; ++tt) stage_cell(tt);
-    double mu_u = 0, phi_u = 0, psi_u = 0;
-    int sl_prev = 2 * MW, sl_cur = 0;
-    const bool stone = alpha != 0.0;
-    for (int t = 0; t < Ti; ++t) {
-      stage_cell(t + DS - 1);
-      asm volatile("cp.async.wait_group %0;" ::"n"(DS - 1) : "memory");
-      const int p = t - q;
-      const int Wt = S.width(crank, t);
-      if (bnd_recv1 && t >= 1) {  // left neighbour's factors, slice t-1
-        double v[MSG];
-        mail.recv(seq_rx++, v);
-        smu[sl_prev - 1] = v[0];
-        sphi[sl_prev - 1] = v[1];
-        spsi[sl_prev - 1] = v[2];
-      }
-      double send_v[MSG] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (live && (unsigned)p < (unsigned)Ri) {
-        const double *in = stg_in + ((t % DS) * 6) * mh + ql;
-        const bool pge1 = p >= 1, plast = p == Ri - 1, ple = p <= Ri - 2;
-        const bool ige1 = pge1 || qge1;
-        const bool ilen2 = !(plast && qlast);
-        const double a2 = pge1 ? in[0] : 0.0;
-        const double a1 = ige1 ? in[mh] : 0.0;
-        const double e = in[2 * mh];
-        const double c1 = ilen2 ? in[3 * mh] : 0.0;
-        const double c2 = ple ? in[4 * mh] : 0.0;
-        if ((qfirst && a1 != 0.0) || (qlast && c1 != 0.0)) s_notgrid = 1;
-        const double mu_l = qge1 ? smu[sl_prev + ql - 1] : 0.0;
-        const double phi_l = qge1 ? sphi[sl_prev + ql - 1] : 0.0;
-        const double psi_l = qge1 ? spsi[sl_prev + ql - 1] : 0.0;
-        const bool has2 = pge1 && a2 != 0.0;
-        const bool has1 = ige1 && a1 != 0.0;
-        double li2 = 0.0, li1 = 0.0, mi, ph = 0.0, ps = 0.0;
-        if (has2) li2 = dvd(a2, stone ? add(mu_u, mul(alpha, phi_u)) : mu_u);
-        if (has1) li1 = dvd(a1, stone ? add(mu_l, mul(alpha, psi_l)) : mu_l);
-        mi = e;
-        if (has2) mi = sub(mi, mul(li2, psi_u));
-        if (has1) mi = sub(mi, mul(li1, phi_l));
-        if (stone) {
-          double comp = 0.0;
-          if (has2) comp = add(comp, mul(li2, phi_u));
-          if (has1) comp = add(comp, mul(li1, psi_l));
-          mi = add(mi, mul(alpha, comp));
-        }
-        if (ilen2) {
-          double fi = c1;
-          if (stone && fi != 0.0 && has2) fi = sub(fi, mul(alpha, mul(li2, phi_u)));
-          ph = fi;
-        }
-        if (ple) {
-          double gi = c2;
-          if (stone && gi != 0.0 && has1) gi = sub(gi, mul(alpha, mul(li1, psi_l)));
-          ps = gi;
-        }
-        if (mi == 0.0) atomicMin(&s_bad, p * mi_ + q);
-        const double l1 = has1 ? li1 : 0.0, l2 = has2 ? li2 : 0.0;
-        const double pm = pge1 ? mul(l2, mu_u) : 0.0;
-        const double p_1 = (ige1 && qge1) ? mul(l1, mu_l) : 0.0;
-        double p0 = mi;
-        if (ige1 && qge1) p0 = add(p0, mul(l1, phi_l));
-        if (pge1) p0 = add(p0, mul(l2, psi_u));
-        const double p1 = ilen2 ? ph : 0.0;
-        const double pp = ple ? ps : 0.0;
-        const int qo = q - S.qlo(crank, t);
-        double *fgp = S.fg(s, crank) + S.fg_off(crank, t) + qo;
-        double *up = S.bg(s, crank) + S.bg_off(crank, t) + qo;
-        fgp[3 * Wt] = sub(pm, pge1 ? a2 : 0.0);
-        fgp[Wt] = sub(p_1, ige1 ? a1 : 0.0);
-        fgp[0] = sub(p0, e);
-        fgp[2 * Wt] = sub(p1, ilen2 ? c1 : 0.0);
-        fgp[4 * Wt] = sub(pp, ple ? c2 : 0.0);
-        fgp[5 * Wt] = pge1 ? mul(l2, phi_u) : 0.0;
-        fgp[6 * Wt] = ((ige1 && (ple || (plast && qfirst))) && qge1) ? mul(l1, psi_l) : 0.0;
-        const double bb = in[5 * mh];
-        rb0 = nan_max(rb0, fabs(bb));
-        fgp[8 * Wt] = l1;
-        fgp[9 * Wt] = l2;
-        up[0] = ph;
-        up[Wt] = ps;
-        up[2 * Wt] = mi;
-        smu[sl_cur + ql] = mi;
-        sphi[sl_cur + ql] = ph;
-        spsi[sl_cur + ql] = ps;
-        mu_u = mi; phi_u = ph; psi_u = ps;
-        send_v[0] = mi; send_v[1] = ph; send_v[2] = ps;
-      }
-      if (bnd_send0 && t <= Ti - 2) mail.send(seq_tx++, send_v);
-      sl_prev = sl_cur;
-      sl_cur = sl_cur == 2 * MW ? 0 : sl_cur + MW;
-      __syncthreads();
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-  }
-  // zero pivot / not-a-grid anywhere in the system: both CTAs stop
-  {
-    const int nb = s_bad, ng = s_notgrid;
-    const double cb = cluster_max(-(double)nb), cg = cluster_max((double)ng);
-    const int bad = (int)(-cb);
-    __syncthreads();
-    if (cg > 0.0 || bad != 0x7fffffff) {
-      if (crank == 0 && ql == 0) {
-        if (cg > 0.0) set_status(status, index, s, BX_STATUS_NOT_GRID, -1);
-        else set_status(status, index, s, BX_STATUS_ZERO_PIVOT, bad);
-        if (iters) iters[s] = 0;
-      }
-      cluster_sync();
-      return;
-    }
-  }
-
-  double *xs = sh + 2;            // [4][MW] window of the previous iterate
-  double *ys = sh + 4 * MW + 2;   // [3][MW]
-  double *xn = sh + 7 * MW + 2;   // [4][MW] window of the new iterate
-  double *ring = area;
-  const int NCW = (mh + 31) / 32, NCT = NCW * 32;
-  const bool producer = ql >= NCT;
-  const int lane = ql & 31;
-  auto valid_cell = [&](int64_t t) { const int64_t p = t - q; return ql < mh && p >= 0 && p < R; };
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  __syncthreads();
-  int p_stg = 0, c_stg = 0;
-  unsigned p_par = 0, c_par = 0;
-  // producer: up to 11 bulk copies per step, one per lane (rows of my columns)
-  auto produce = [&](const double *const *src, const int *rows_dst, const unsigned *bytes, int ncopy) {
-    mbar_wait(empty + p_stg, p_par ^ 1u);
-    unsigned tot = 0;
-    for (int i = 0; i < ncopy; ++i) tot += bytes[i];
-    if (lane == 0) mbar_expect(full + p_stg, tot);
-    __syncwarp();
-    if (lane < ncopy && bytes[lane])
-      bulk_g2s(ring + ((size_t)p_stg * NPL) * SW + rows_dst[lane], src[lane], bytes[lane], full + p_stg);
-    __syncwarp();
-    if (++p_stg == nst) { p_stg = 0; p_par ^= 1u; }
-  };
-  const unsigned full_u = smem_u32(full), empty_u = smem_u32(empty);
-  auto consume_wait = [&]() -> int {
-    mbar_wait_u32(full_u + 8u * (unsigned)c_stg, c_par);
-    return c_stg;
-  };
-  auto consume_release = [&]() {
-    __syncwarp();
-    if (lane == 0) mbar_arrive_u32(empty_u + 8u * (unsigned)c_stg);
-    if (++c_stg == nst) { c_stg = 0; c_par ^= 1u; }
-  };
-  auto cons_sync = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(NCT) : "memory"); };
-  // residual of cell (p, qq) (iterative.py:213-221 order, acc from 0); the
-  // five x values are passed explicitly
-  auto resid = [&](int p, int qq, double a2, double a1, double e, double c1, double c2, double bb,
-                   double xc, double xl, double xr, double xu, double xd) -> double {
-    const int64_t i = (int64_t)p * m + qq;
-    double acc = add(0.0, mul(e, xc));
-    if (i >= 1 && qq >= 1) acc = add(acc, mul(a1, xl));
-    if (i <= n - 2 && qq <= mi_ - 2) acc = add(acc, mul(c1, xr));
-    if (p >= 1) acc = add(acc, mul(a2, xu));
-    if (p <= Ri - 2) acc = add(acc, mul(c2, xd));
-    return fabs(sub(bb, acc));
-  };
-  auto block_max = [&](double v) -> double {
-    for (int o = 16; o > 0; o >>= 1) v = nan_max(v, __shfl_xor_sync(0xffffffffu, v, o));
-    __syncthreads();
-    if ((ql & 31) == 0 && ql < NCT) s_red[ql >> 5] = v;
-    __syncthreads();
-    double r = 0.0;
-    for (int w = 0; w < NCW; ++w) r = nan_max(r, s_red[w]);
-    return r;
-  };
-
-  // initial residual of x0 over my columns (neighbours from the x0 plane)
-  double rloc = 0.0;
-  if (!use_x0) {
-    rloc = rb0;
-  } else if (ql < mh) {
-    const double *xp0 = S.at(PXA, s, 0);
-    auto X = [&](int p, int qq) -> double {
-      if (p < 0 || p >= Ri || qq < 0 || qq >= mi_) return 0.0;
-      return xp0[(int64_t)(p + qq) * S.mp + qq];
-    };
-    for (int p = 0; p < Ri; ++p) {
-      const int t = p + q;
-      const int Wt = S.width(crank, t), Wm = S.width(crank, t - 1);
-      const double *ab = S.bg(s, crank) + S.bg_off(crank, t - 1) + 3 * Wm + (q - S.qlo(crank, t));
-      rloc = nan_max(rloc, resid(p, q, ab[0], ab[Wt], ab[2 * Wt], ab[3 * Wt], ab[4 * Wt], ab[5 * Wt],
-                                 X(p, q), X(p, q - 1), X(p, q + 1), X(p - 1, q), X(p + 1, q)));
-    }
-  }
-  double r = cluster_max(block_max(rloc));
-  const double r0 = r;
-  double best = r;
-  int64_t k = 0;
-  int32_t st = BX_STATUS_OK;
-  int cur = 0, best_loc = 0;
-  const double tl = tol[s];
-  const int XP[3] = {PXA, PXB, PXBEST};
-  const int p_hi = Ri - 2;
-  const int xs0 = c0 >= 2 ? c0 - 2 : 0;                      // first staged x column
-  const int xs1 = c0 + mh + 2 <= mi_ ? c0 + mh + 2 : mi_;    // one past the last
-
-  while (true) {
-    if (ql == 0) {
-      s_go = 0;
-      s_bestcopy = 0;
-      if (r >= tl) {
-        if (k >= max_iter) st = BX_STATUS_MAX_ITER;
-        else s_go = 1;
-      }
-      if (s_go && best_loc == (cur ^ 1)) s_bestcopy = 1;
-    }
-    __syncthreads();
-    if (!s_go) break;
-    const int nxt = cur ^ 1;
-    if (s_bestcopy) {
-      for (int64_t t = 0; t < T; ++t)
-        if (valid_cell(t)) *(S.at(PXBEST, s, t) + q) = *(S.at(XP[nxt], s, t) + q);
-      best_loc = 2;
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      __syncthreads();
-    }
-    const int xo = XP[cur], xw = XP[nxt];
-    // ---- forward: newRHS = K x + b, then L y = newRHS (iterative.py:293-294)
-    if (producer) {
-      const double *xrow = S.at(xo, s, 0);
-      for (int t = 0; t < Ti; ++t) {
-        const int Wt = S.width(crank, t);
-        const double *src[2] = {S.fg(s, crank) + S.fg_off(crank, t), xrow};
-        int dst[2] = {0, 10 * SW};
-        unsigned by[2] = {(unsigned)(10 * Wt * sizeof(double)), 0u};
-        // x_old of slice t+1: columns [xs0, xs1) of its valid range (even-aligned)
-        if (t + 1 < Ti) {
-          const int g = t + 1 - Ri + 1 > 0 ? t + 1 - Ri + 1 : 0;
-          const int qlo1 = g & ~1;
-          const int qhi1 = t + 1 < mi_ - 1 ? t + 1 : mi_ - 1;
-          const int a0 = max(qlo1, xs0), a1_ = min(((qhi1 + 2) & ~1), xs1);
-          if (a1_ > a0) {
-            src[1] = xrow + (int64_t)(t + 1) * S.mp + a0;
-            dst[1] = 10 * SW + (a0 - xs0);
-            by[1] = (unsigned)((a1_ - a0) * sizeof(double));
-          }
-        }
-        produce(src, dst, by, 2);
-      }
-    } else {
-      const bool live = ql < mh;
-      double *py = S.at(PY, s, 0) + q;
-      double *wm1 = xs + 3 * MW, *w0 = xs, *wp1 = xs + MW, *wp2 = xs + 2 * MW;
-      double *yprev = ys + MW, *ycur = ys;
-      if (live) {
-        w0[ql] = valid_cell(0) ? *(S.at(xo, s, 0) + q) : 0.0;
-        if (ql == 0) w0[-1] = 0.0;
-        if (ql == mh - 1) w0[mh] = 0.0;
-        yprev[-1] = 0.0;
-      }
-      double y_u = 0.0;
-      const bool qge1 = q >= 1, qlem2 = q <= mi_ - 2, qlast = q == mi_ - 1, qfirst = q == 0;
-      const int stage_d = NPL * SW;
-      for (int t = 0; t < Ti; ++t, py += S.mp) {
-        const int stg = consume_wait();
-        const double *stage = ring + stg * stage_d;
-        const int p = t - q;
-        if (live && t + 1 < Ti) {  // x_old of slice t+1, own column and halos
-          const double *xr = stage + 10 * SW - xs0;
-          auto xv = [&](int qq) -> double {
-            const int pp = t + 1 - qq;
-            return (qq >= 0 && qq < mi_ && (unsigned)pp < (unsigned)Ri) ? xr[qq] : 0.0;
-          };
-          wp1[ql] = xv(q);
-          if (ql == 0) wp1[-1] = xv(q - 1);
-          if (ql == mh - 1) wp1[mh] = xv(q + 1);
-        }
-        if (bnd_recv1 && t >= 1) {  // y of column c0-1, slice t-1
-          double v[MSG];
-          mail.recv(seq_rx++, v);
-          yprev[-1] = v[0];
-        }
-        cons_sync();
-        double y_send = 0.0;
-        if (live && (unsigned)p < (unsigned)Ri) {
-          const int Wt = S.width(crank, t);
-          const double *rb = stage + (q - S.qlo(crank, t));
-          const bool pge1 = p >= 1, plast = p == Ri - 1, phi_ok = p <= p_hi;
-          double acc = add(0.0, mul(rb[0], w0[ql]));
-          if ((pge1 || qge1) && qge1) acc = add(acc, mul(rb[Wt], wm1[ql - 1]));
-          if (!(plast && qlast) && qlem2) acc = add(acc, mul(rb[2 * Wt], wp1[ql + 1]));
-          if (pge1) acc = add(acc, mul(rb[3 * Wt], wm1[ql]));
-          if (phi_ok) acc = add(acc, mul(rb[4 * Wt], wp1[ql]));
-          if ((pge1 || qlast) && qlem2 && pge1) acc = add(acc, mul(rb[5 * Wt], w0[ql + 1]));
-          if ((phi_ok || (plast && qfirst)) && qge1) acc = add(acc, mul(rb[6 * Wt], w0[ql - 1]));
-          const double v = add(acc, rb[7 * Wt]);
-          double y = v;
-          if ((pge1 || qge1) && qge1) y = sub(y, mul(rb[8 * Wt], yprev[ql - 1]));
-          if (pge1) y = sub(y, mul(rb[9 * Wt], y_u));
-          *py = y;
-          ycur[ql] = y;
-          y_u = y;
-          y_send = y;
-        }
-        if (bnd_send0 && t <= Ti - 2) {
-          double v[MSG] = {y_send, 0, 0, 0, 0, 0, 0, 0};
-          mail.send(seq_tx++, v);
-        }
-        consume_release();
-        double *tw = wm1; wm1 = w0; w0 = wp1; wp1 = wp2; wp2 = tw;
-        double *ty = yprev; yprev = ycur; ycur = ty;
-      }
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-    __syncthreads();
-    // ---- backward U x = y (iterative.py:295) + fused residual (296-297)
-    rloc = 0.0;
-    if (producer) {
-      const double *yrow = S.at(PY, s, 0);
-      for (int t = Ti - 1; t >= -1; --t) {
-        const int Wt = S.width(crank, t), W1 = S.width(crank, t + 1);
-        const double *src[2] = {S.bg(s, crank) + S.bg_off(crank, t), yrow};
-        int dst[2] = {0, 10 * SW};
-        unsigned by[2] = {(unsigned)((3 * Wt + 6 * W1) * sizeof(double)), 0u};
-        // y of slice t, my columns (even-aligned; the plane stride mp is even)
-        if (t >= 0) {
-          const int g = t - Ri + 1 > 0 ? t - Ri + 1 : 0;
-          const int qlo0 = g & ~1;
-          const int qhi0 = t < mi_ - 1 ? t : mi_ - 1;
-          const int a0 = max(qlo0, c0), a1_ = min((qhi0 + 2) & ~1, c0 + mh);
-          if (a1_ > a0) {
-            src[1] = yrow + (int64_t)t * S.mp + a0;
-            dst[1] = 10 * SW + (a0 - c0);
-            by[1] = (unsigned)((a1_ - a0) * sizeof(double));
-          }
-        }
-        produce(src, dst, by, 2);
-      }
-    } else {
-      const bool live = ql < mh;
-      double *px = S.at(xw, s, 0) + q + (int64_t)(Ti - 1) * S.mp;
-      double x_d = 0.0;
-      const bool qlem2 = q <= mi_ - 2, qlast = q == mi_ - 1;
-      double *n0 = xn + ((Ti - 1) & 3) * MW, *n1 = xn + (Ti & 3) * MW,
-             *n2 = xn + ((Ti + 1) & 3) * MW, *n3 = xn + ((Ti + 2) & 3) * MW;
-      if (live) {
-        n1[ql] = 0.0; n2[ql] = 0.0;
-        if (ql == mh - 1) { n1[mh] = n1[mh + 1] = n2[mh] = n2[mh + 1] = 0.0; }
-        if (ql == 0) { n1[-1] = n2[-1] = 0.0; }
-      }
-      // CTA 0's last thread: column c0+mh (peer) values for its own residual
-      // and for column c0+mh's residual (A/b of that column at slice t+1)
-      double ab_peer[6] = {0, 0, 0, 0, 0, 0};
-      const int stage_d = NPL * SW;
-      for (int j = 0; j <= Ti; ++j, px -= S.mp) {
-        const int t = Ti - 1 - j;
-        const int stg = consume_wait();
-        const double *stage = ring + stg * stage_d;
-        const int p = t - q;
-        if (bnd_send0 && t >= 0) {  // receives from CTA 1: x(mh)@t, x(mh+1)@t, A/b(mh)@t+1
-          double v[MSG];
-          mail.recv(seq_rx++, v);
-          n0[mh] = v[0];
-          n0[mh + 1] = v[1];
-#pragma unroll
-          for (int i = 0; i < 6; ++i) ab_peer[i] = v[2 + i];
-        }
-        if (live && t >= 0) {
-          if ((unsigned)p < (unsigned)Ri) {
-            const int Wt = S.width(crank, t);
-            const double *ub = stage + (q - S.qlo(crank, t));
-            double v = stage[10 * SW + ql];
-            if (!(p == Ri - 1 && qlast) && qlem2) v = sub(v, mul(ub[0], n1[ql + 1]));
-            if (p <= p_hi) v = sub(v, mul(ub[Wt], x_d));
-            const double xv = dvd(v, ub[2 * Wt]);
-            *px = xv;
-            n0[ql] = xv;
-            x_d = xv;
-          } else {
-            n0[ql] = 0.0;
-          }
-          if (ql == 0) n0[-1] = 0.0;  // never read across the left edge of CTA 0
-        }
-        cons_sync();
-        if (live && t + 1 <= Ti - 1 && (unsigned)(p + 1) < (unsigned)Ri && !(bnd_recv1)) {
-          // residual of slice t+1 (column q), acc from 0 in the reference order
-          const int Wt = S.width(crank, t), W1 = S.width(crank, t + 1);
-          const double *ab = stage + 3 * Wt + (q - S.qlo(crank, t + 1));
-          const int pp = p + 1;
-          rloc = nan_max(rloc, resid(pp, q, ab[0], ab[W1], ab[2 * W1], ab[3 * W1], ab[4 * W1],
-                                     ab[5 * W1], n1[ql], n0[ql - 1], n2[ql + 1], n0[ql], n2[ql]));
-        }
-        if (bnd_send0 && t >= 0 && t + 1 <= Ti - 1) {
-          // column c0+mh's residual of slice t+1 (its left neighbour is mine)
-          const int pp = t + 1 - (q + 1);
-          if ((unsigned)pp < (unsigned)Ri)
-            rloc = nan_max(rloc, resid(pp, q + 1, ab_peer[0], ab_peer[1], ab_peer[2], ab_peer[3],
-                                       ab_peer[4], ab_peer[5], n1[mh], n0[mh - 1], n2[mh + 1],
-                                       n0[mh], n2[mh]));
-        }
-        if (bnd_recv1 && t >= 0) {
-          // to CTA 0: x of columns c0, c0+1 at slice t, A/b of column c0 at t+1
-          double v[MSG] = {n0[0], n0[1], 0, 0, 0, 0, 0, 0};
-          const int pp = t + 1 - q;
-          if (t + 1 <= Ti - 1 && (unsigned)pp < (unsigned)Ri) {
-            const int Wt = S.width(crank, t), W1 = S.width(crank, t + 1);
-            const double *ab = stage + 3 * Wt + (q - S.qlo(crank, t + 1));
-#pragma unroll
-            for (int i = 0; i < 6; ++i) v[2 + i] = ab[i * W1];
-          }
-          mail.send(seq_tx++, v);
-        }
-        consume_release();
-        double *tw = n3; n3 = n2; n2 = n1; n1 = n0; n0 = tw;
-      }
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-    r = cluster_max(block_max(rloc));
-    cur = nxt;
-    ++k;
-    if (crank == 0 && ql == 0 && history) history[s * max_iter + (k - 1)] = r;
-    if (r < best) { best = r; best_loc = cur; }
-    if (r0 > 0 && r > 1e6 * r0) { st = BX_STATUS_DIVERGED; break; }
-  }
-  // ---- outputs in the caller's layout (my columns)
-  if (ql < mh) {
-    const double *xc = S.at(XP[cur], s, 0) + q, *xb = S.at(XP[best_loc], s, 0) + q;
-    constexpr int U = 8;
-    for (int64_t p0 = 0; p0 < R; p0 += U) {
-      double v[U], w[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t p = p0 + u;
-        v[u] = p < R ? xc[(p + q) * S.mp] : 0.0;
-        w[u] = (best_x && p < R) ? xb[(p + q) * S.mp] : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t p = p0 + u;
-        if (p >= R) break;
-        const int64_t i = p * m + q;
-        xout[lay(i, s)] = v[u];
-        if (best_x) best_x[lay(i, s)] = w[u];
-      }
-    }
-  }
-  if (crank == 0 && ql == 0) {
-    if (iters) iters[s] = k;
-    if (res) res[s] = r;
-    if (best_res) best_res[s] = best;
-    set_status(status, index, s, st, -1);
-  }
-  cluster_sync();  // no CTA leaves while its peer may still write into it
-}
-
 }  // namespace sipw
 
 bool sip_is_grid(const double *a1, const double *c1, int64_t batch, int64_t n, int64_t m,
@@ -1455,48 +794,10 @@ static sipw::Skew sipw_layout(double *base, int64_t batch, int64_t n, int64_t m)
 // workspace: [prefix table pw (T+1 int64, padded to 256 B)] [systems]
 static size_t sipw_pw_bytes(int64_t T) { return ((size_t)(T + 1) * sizeof(int64_t) + 255) & ~(size_t)255; }
 
-// per-half layout of the two-CTA kernel (SkewH); widths as SkewH::width
-static sipw::SkewH sipw_layout_h(int64_t batch, int64_t n, int64_t m) {
-  sipw::SkewH S{};
-  S.batch = batch;
-  S.m = m;
-  S.mh = m / 2;
-  S.R = n / m;
-  S.T = S.R + m - 1;
-  S.mp = sipw_mp(m);
-  int64_t P[2] = {0, 0};
-  for (int c = 0; c < 2; ++c)
-    for (int64_t t = 0; t < S.T; ++t) {
-      const int64_t lo = std::max<int64_t>(std::max<int64_t>(t - S.R + 1, 0), c * S.mh);
-      const int64_t hi = std::min<int64_t>(std::min<int64_t>(t, m - 1), c * S.mh + S.mh - 1);
-      const int64_t nv = hi - lo + 1;
-      if (nv > 0) P[c] += nv + (nv & 1);
-    }
-  S.P0 = P[0];
-  S.P1 = P[1];
-  S.per_sys = 19 * (P[0] + P[1]) + 4 * S.T * S.mp;
-  return S;
-}
-static bool sipw_split_ok(int64_t m) { return m % 4 == 0 && m >= 64; }
-static int sipw_split_mode() {
-  static int mode = -2;  // BX_SIP_SPLIT=0 forces the one-CTA kernel
-  if (mode == -2) {
-    const char *env = getenv("BX_SIP_SPLIT");
-    mode = env ? atoi(env) : 0;
-  }
-  return mode;
-}
-
 size_t sip_wave_workspace_bytes(int64_t batch, int64_t n, int64_t m) {
   if (m < 2 || n % m) return 0;
   const sipw::Skew S = sipw_layout(nullptr, batch, n, m);
-  size_t b = sipw_pw_bytes(S.T) + sizeof(double) * (size_t)batch * (size_t)S.per_sys + 256;
-  if (sipw_split_ok(m)) {  // the two-CTA layout: two prefix tables, per-half rows
-    const sipw::SkewH H = sipw_layout_h(batch, n, m);
-    const size_t bh = 2 * sipw_pw_bytes(H.T) + sizeof(double) * (size_t)batch * (size_t)H.per_sys + 256;
-    b = b > bh ? b : bh;
-  }
-  return b;
+  return sipw_pw_bytes(S.T) + sizeof(double) * (size_t)batch * (size_t)S.per_sys + 256;
 }
 
 int sip_wave(const double *a2, const double *a1, const double *e, const double *c1,
@@ -1525,66 +826,6 @@ int sip_wave(const double *a2, const double *a1, const double *e, const double *
     bxh::set_error("wavefront SIP: grid width m=%lld too large for the shared-memory ring",
                    (long long)m);
     return BX_ERR_UNSUPPORTED;
-  }
-  // two-CTA clusters (half the grid columns each) for wide grids: twice the
-  // SMs per system (BX_SIP_SPLIT=0 forces the one-CTA kernel)
-  if (sipw_split_mode() != 0 && sipw_split_ok(m)) {
-    const int mh = (int)(m / 2);
-    sipw::SkewH H = sipw_layout_h(batch, n, m);
-    H.pw0 = reinterpret_cast<const int64_t *>(base);
-    H.pw1 = reinterpret_cast<const int64_t *>(reinterpret_cast<char *>(base) + sipw_pw_bytes(H.T));
-    H.ws = reinterpret_cast<double *>(reinterpret_cast<char *>(base) + 2 * sipw_pw_bytes(H.T));
-    sipw::sip_prefix_h_kernel<<<1, 32, 0, stream>>>(H);
-    {
-      const unsigned pthreads = (unsigned)(m < 512 ? ((m + 31) / 32) * 32 : 512);
-      const dim3 pgrid((unsigned)H.T, (unsigned)batch);
-      if (layout == BX_LAYOUT_INTERLEAVED)
-        sipw::sip_pack_h_kernel<<<pgrid, pthreads, 0, stream>>>(a2, a1, e, c1, c2, b, x, H, n,
-                                                               use_x0, Interleaved{ld});
-      else
-        sipw::sip_pack_h_kernel<<<pgrid, pthreads, 0, stream>>>(a2, a1, e, c1, c2, b, x, H, n,
-                                                               use_x0, SystemMajor{ld});
-    }
-    const size_t MW = (size_t)mh + 4, SW = MW;
-    const size_t win2 = sizeof(double) * (11 * MW + 2);
-    const size_t stage2 = sizeof(double) * (size_t)sipw::NPL * SW;
-    const size_t mail = sizeof(double) * sipw::RING2 * sipw::MSG + sizeof(uint64_t) * 2 * sipw::RING2;
-    const size_t stg2 = sizeof(double) * 4 * 6 * (size_t)mh;
-    int nst2 = (int)((200 * 1024 - win2 - mail) / (stage2 + 2 * sizeof(uint64_t)));
-    if (nst2 > 8) nst2 = 8;
-    if (const char *env = getenv("BX_SIP_NST")) nst2 = nst2 < atoi(env) ? nst2 : atoi(env);
-    const size_t area = stage2 * nst2 > stg2 ? stage2 * nst2 : stg2;
-    const size_t smem2 = win2 + area + mail + sizeof(uint64_t) * 2 * nst2 + 64;
-    const unsigned threads2 = (unsigned)(((mh + 31) / 32) * 32 + 32);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * batch));
-    cfg.blockDim = dim3(threads2);
-    cfg.dynamicSmemBytes = smem2;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t err;
-    if (layout == BX_LAYOUT_INTERLEAVED) {
-      auto k = sipw::sip_wave2_kernel<Interleaved>;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-      err = cudaLaunchKernelEx(&cfg, k, a2, a1, e, c1, c2, b, tol, x, best_x, iters, res, best_res,
-                               st, ix, hist, H, n, alpha, max_iter, use_x0, Interleaved{ld}, nst2);
-    } else {
-      auto k = sipw::sip_wave2_kernel<SystemMajor>;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-      err = cudaLaunchKernelEx(&cfg, k, a2, a1, e, c1, c2, b, tol, x, best_x, iters, res, best_res,
-                               st, ix, hist, H, n, alpha, max_iter, use_x0, SystemMajor{ld}, nst2);
-    }
-    if (err != cudaSuccess) {
-      bxh::set_error("wavefront SIP (2-CTA) launch: %s", cudaGetErrorString(err));
-      return BX_ERR_CUDA;
-    }
-    return BX_OK;
   }
   sipw::sip_prefix_kernel<<<1, 32, 0, stream>>>(S);
   {
