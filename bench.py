@@ -199,7 +199,7 @@ class Direct:
     def __init__(self, args, rank, dev, name):
         import torch
         from paper_1804_09666_b200 import _lib
-        from paper_1804_09666_b200.core import workspace
+        from paper_1804_09666_b200.core import ptr, workspace
         self.args = args
         solver, batch, n, cfg, sparse, desc = DIRECT[name]
         self.solver, self.batch, self.n = solver, batch, n
@@ -218,6 +218,25 @@ class Direct:
         L = _lib.lib()
         self.ws = workspace(L.bx_workspace_bytes(_lib.SOLVER[solver], batch, n, self.lay, self.algo), dev)
         self.bytes_per_row = 40 if self.kind == "tri" else 56
+        # MNPDM on sparse outer diagonals (its purpose): the +-2 diagonals as
+        # per-system row lists, compacted once per matrix outside the timed
+        # region (PentaMatrix.sparse_outer); the solve streams 40 B/row
+        self.sparse = solver == "mnpdm" and sparse and args.algo == "partitioned"
+        self.outer_bytes = 0
+        if self.sparse:
+            cnt = torch.empty(batch, dtype=torch.int32, device=dev)
+            c2, g2 = self.d_in[0], self.d_in[4]
+            _lib.call("bx_outer_compact_f64", ptr(c2), ptr(g2), ptr(cnt), None, None, None, 0, batch, n,
+                      self.ld, self.lay, torch.cuda.current_stream().cuda_stream)
+            self.outer_k = max(int(cnt.max()), 1)
+            self.orow = torch.empty((batch, self.outer_k), dtype=torch.int32, device=dev)
+            self.os2 = torch.empty((batch, self.outer_k), dtype=torch.float64, device=dev)
+            self.op2 = torch.empty((batch, self.outer_k), dtype=torch.float64, device=dev)
+            _lib.call("bx_outer_compact_f64", ptr(c2), ptr(g2), ptr(cnt), ptr(self.orow), ptr(self.os2),
+                      ptr(self.op2), self.outer_k, batch, n, self.ld, self.lay,
+                      torch.cuda.current_stream().cuda_stream)
+            self.bytes_per_row = 40
+            self.outer_bytes = batch * self.outer_k * (4 + 8 + 8)
         self.units = batch
         gb = self.bytes_per_row * batch * n / 1e9
         # inputs that fit the 126 MB L2 (config 1: 42 MB) are flushed out of it
@@ -228,6 +247,9 @@ class Direct:
               if self.flush_l2 else f"inputs {gb:.2f} GB per step > 126 MB L2, no flush")
         self.config = {"workload": desc, "solver": solver, "algo": args.algo, "batch_per_gpu": batch,
                        "n": n, "layout": f"{args.layout} row-aligned", "l2": l2}
+        if self.sparse:
+            self.config["outer"] = (f"+-2 diagonals as per-system row lists ({self.outer_k} rows per "
+                                    "system), compacted once per matrix outside the timed region")
 
     def solve(self, ins, out):
         import torch
@@ -235,7 +257,12 @@ class Direct:
         from paper_1804_09666_b200.core import ptr
         L, s = _lib.lib(), torch.cuda.current_stream().cuda_stream
         tail = (self.batch, self.n, self.ld, self.lay, self.algo, ptr(self.ws), self.ws.numel(), s)
-        if self.solver == "ntdm":
+        if self.sparse:  # ins: sub1, main, sup1, rhs
+            rc = L.bx_mnpdm_sparse_f64(ptr(self.orow), ptr(self.os2), ptr(self.op2), self.outer_k,
+                                       *(ptr(t) for t in ins), ptr(out), ptr(self.status),
+                                       ptr(self.index), ptr(self.nz), self.batch, self.n, self.ld,
+                                       self.lay, s)
+        elif self.solver == "ntdm":
             rc = L.bx_ntdm_f64(*(ptr(t) for t in ins), ptr(out), ptr(self.status), ptr(self.index), *tail)
         elif self.solver == "npdm":
             rc = L.bx_npdm_f64(*(ptr(t) for t in ins), ptr(out), ptr(self.status), ptr(self.index), *tail)
@@ -245,7 +272,7 @@ class Direct:
         _lib.check(rc, self.solver)
 
     def step(self):
-        self.solve(self.d_in, self.x)
+        self.solve([self.d_in[i] for i in (1, 2, 3, 5)] if self.sparse else self.d_in, self.x)
 
     def check(self):
         """Sampled parity gate against the C restatement of the reference."""
@@ -266,16 +293,27 @@ class Direct:
 
     def e2e_prepare(self):
         import torch
-        self.pinned = [torch.from_numpy(h).pin_memory() for h in self.host]
+        host = self.host
+        self.host_outer = None
+        if self.sparse:  # host inputs: sub1, main, sup1, rhs + the outer row lists
+            from paper_1804_09666_b200.pipeline import outer_lists
+            host = [self.host[i] for i in (1, 2, 3, 5)]
+            lists = outer_lists(self.host[0], self.host[4])
+            self.host_outer = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in lists]
+        self.pinned = [torch.from_numpy(h).pin_memory() for h in host]
         self.x_host = torch.empty(self.host[-1].shape, dtype=torch.float64).pin_memory()
-        self.h2d = sum(h.nbytes for h in self.host)
+        self.h2d = sum(h.nbytes for h in host) + sum(t.numel() * t.element_size()
+                                                      for t in (self.host_outer or []))
         self.d2h = self.x_host.numel() * 8
         self.pipe = None
+        if self.sparse and self.args.layout != "system":
+            raise SystemExit("sparse-outer MNPDM e2e path is system-major only")
         if self.args.layout == "system":
             # chunked H2D / solve / D2H overlap on three streams (pipeline.py)
             from paper_1804_09666_b200.pipeline import HostPipeline
-            self.pipe = HostPipeline(self.solver, self.n, max(1, self.batch // 8), self.x.device,
-                                     algo=self.args.algo)
+            self.pipe = HostPipeline("mnpdm_sparse" if self.sparse else self.solver, self.n,
+                                     max(1, self.batch // 8), self.x.device, algo=self.args.algo,
+                                     outer_k=self.host_outer[0].shape[1] if self.sparse else 0)
             self.e2e_path = ("pinned host -> bx C ABI per chunk -> pinned host x (system-major: "
                              "8 chunks, H2D / solve / D2H overlapped on 3 streams, pipeline.py)")
         else:
@@ -284,7 +322,7 @@ class Direct:
 
     def e2e_step(self):
         if self.pipe is not None:
-            self.pipe.run(self.pinned, self.x_host)
+            self.pipe.run(self.pinned, self.x_host, host_outer=self.host_outer)
             return
         for h, d in zip(self.pinned, self.d_e2e):
             d.copy_(h, non_blocking=True)
@@ -292,11 +330,12 @@ class Direct:
         self.x_host.copy_(self.x_e2e, non_blocking=True)
 
     def roofline(self, mean_launch, peak):
-        alg = self.bytes_per_row * self.batch * self.n
+        alg = self.bytes_per_row * self.batch * self.n + self.outer_bytes
         ach = alg / mean_launch / 1e9
+        kern = f"bx {self.solver} ({self.args.algo}{', sparse outer diagonals' if self.sparse else ''})"
         return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": None, "kernel": f"bx {self.solver} ({self.args.algo})",
-                "algorithmic_bytes_per_launch": alg, "bytes_per_row": self.bytes_per_row}
+                "traffic": None, "kernel": kern, "algorithmic_bytes_per_launch": alg,
+                "bytes_per_row": self.bytes_per_row}
 
     def cpu_baseline(self, budget_s=5.0):
         rate0, _, _ = cpu_direct_rate(self.solver, self.arrs, min(self.batch, 128))

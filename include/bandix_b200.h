@@ -113,6 +113,24 @@ int bx_mnpdm_f64(const double *sub2, const double *sub1, const double *main,
                  int64_t ld, int32_t layout, int32_t algo, void *workspace,
                  size_t workspace_bytes, void *stream);
 
+/* MNPDM with sparse outer diagonals -- the case MNPDM exists for (_elim.py:
+ * 125-190 skips the eliminations where sub2 == 0; the paper's K outer
+ * nonzeros).  bx_outer_compact_f64 lists, per system and in row order, the
+ * rows whose sub2 (i >= 2) or sup2 (i <= n-3) is nonzero: count[batch]
+ * always; with capacity > 0 also rows[batch][capacity] (-1 pads) and the
+ * two values at those rows.  bx_mnpdm_sparse_f64 then solves from sub1 /
+ * main / sup1 / rhs plus that list (partitioned algorithm, 40 B/row of
+ * compulsory traffic instead of 56): x, status, index and nz_sub2 (may be
+ * NULL) as bx_mnpdm_f64. */
+int bx_outer_compact_f64(const double *sub2, const double *sup2, int32_t *count, int32_t *rows,
+                         double *vals_sub2, double *vals_sup2, int64_t capacity, int64_t batch,
+                         int64_t n, int64_t ld, int32_t layout, void *stream);
+int bx_mnpdm_sparse_f64(const int32_t *outer_rows, const double *outer_sub2,
+                        const double *outer_sup2, int64_t outer_k, const double *sub1,
+                        const double *main, const double *sup1, const double *rhs, double *x,
+                        int32_t *status, int32_t *index, int64_t *nz_sub2, int64_t batch,
+                        int64_t n, int64_t ld, int32_t layout, void *stream);
+
 /* pd_to_td (direct.py:116-165): Gaussian reduction of pentadiagonal systems
  * to tridiagonal ones in the reference's operation order (bit-identical).
  * Inputs as bx_npdm_f64 (layout/ld); outputs t_sub1/t_main/t_sup1/t_rhs are

@@ -9,7 +9,7 @@ by hand-written sm_100a CUDA kernels behind a C ABI
 fallback: without the built library or a GPU every solver raises.
 """
 
-from .core import BandFactors, OpCounter, PentaMatrix, SolveReport, TriMatrix  # noqa: F401
+from .core import BandFactors, OpCounter, OuterSparsePenta, PentaMatrix, SolveReport, TriMatrix  # noqa: F401
 from .direct import pd_to_td, solve_mnpdm, solve_npdm, solve_ntdm, solve_pd2td_ntdm  # noqa: F401
 from .exact import (BandDeterminant, ExactSolveResult, exact_det_band, exact_solve_spdm,  # noqa: F401
                     exact_solve_stdm, rcond_band)

@@ -47,6 +47,8 @@ _SIGS = {
                              + [_i64, _i64, _i64, _i64, _i32, _i64, _i32, _p, _sz, _p], C.c_int),
     "bx_rcond_workspace_bytes": ([_i32, _i64, _i64], _sz),
     "bx_rcond_band_f64": ([_i32] + [_p] * 8 + [_i64, _i64, _i64, _i32, _p, _sz, _p], C.c_int),
+    "bx_outer_compact_f64": ([_p] * 6 + [_i64, _i64, _i64, _i64, _i32, _p], C.c_int),
+    "bx_mnpdm_sparse_f64": ([_p] * 3 + [_i64] + [_p] * 8 + [_i64, _i64, _i64, _i32, _p], C.c_int),
     "bx_transpose_f64": ([_p, _p] + [_i64] * 7 + [_p], C.c_int),
     "bx_hb_workspace_bytes": ([_i64, _i64], _sz),
     "bx_hb_invert_f64": ([_p] * 12 + [_i64, _i64, _i64, C.c_double, _i64, _i64, _i32, _p, _sz, _p],

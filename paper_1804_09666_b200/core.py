@@ -236,6 +236,14 @@ class PentaMatrix(_Band):
         n, batch = (main.shape if lay == _lib.LAYOUT_INTERLEAVED else main.shape[::-1])
         return PentaMatrix(n, batch, [sub2, sub1, main, sup1, sup2], lay, False, main.device)
 
+    def sparse_outer(self, max_per_system=None):
+        """The same systems with the +-2 diagonals held as a row-sorted list per
+        system (MNPDM's case: only K rows carry outer entries, PAPER Remark 2,
+        _elim.py:125-190).  Built once on the device (like a factorisation
+        reused across time steps); ``solve_mnpdm`` then streams 40 B/row
+        instead of 56.  Returns ``OuterSparsePenta``."""
+        return OuterSparsePenta(self, max_per_system)
+
     @property
     def sub2(self):
         return self.diagonals()[0]
@@ -255,6 +263,45 @@ class PentaMatrix(_Band):
     @property
     def sup2(self):
         return self.diagonals()[4]
+
+
+class OuterSparsePenta:
+    """Pentadiagonal systems whose sub2/sup2 are kept as per-system lists of
+    (row, sub2, sup2) in row order (``rows`` (B, k) int32, -1 pads); sub1, main,
+    sup1 stay row-aligned (shared with the source matrix)."""
+
+    def __init__(self, a, max_per_system=None):
+        if not isinstance(a, PentaMatrix):
+            raise TypeError("sparse_outer needs a PentaMatrix")
+        self.dense = a
+        self.n, self.batch, self.layout, self.single, self.device = (a.n, a.batch, a.layout,
+                                                                    a.single, a.device)
+        self.ld = a.ld
+        c, _, _, _, g = a.rowaligned()
+        count = torch.empty(a.batch, dtype=torch.int32, device=a.device)
+        _lib.call("bx_outer_compact_f64", ptr(c), ptr(g), ptr(count), None, None, None, 0, a.batch,
+                  a.n, a.ld, a.layout, stream_handle())
+        k = int(count.max()) if a.batch else 0
+        if max_per_system is not None and k > max_per_system:
+            raise InvalidInput(f"{k} outer rows in a system exceed max_per_system={max_per_system}")
+        self.k = k
+        self.count = count
+        self.rows = torch.empty((a.batch, max(k, 1)), dtype=torch.int32, device=a.device)
+        self.vals_sub2 = torch.empty((a.batch, max(k, 1)), dtype=torch.float64, device=a.device)
+        self.vals_sup2 = torch.empty((a.batch, max(k, 1)), dtype=torch.float64, device=a.device)
+        if k:
+            _lib.call("bx_outer_compact_f64", ptr(c), ptr(g), ptr(count), ptr(self.rows),
+                      ptr(self.vals_sub2), ptr(self.vals_sup2), k, a.batch, a.n, a.ld, a.layout,
+                      stream_handle())
+
+    def rowaligned(self):
+        return self.dense.rowaligned()
+
+    def rhs(self, b):
+        return self.dense.rhs(b)
+
+    def new_vector(self):
+        return self.dense.new_vector()
 
 
 @dataclass(frozen=True)

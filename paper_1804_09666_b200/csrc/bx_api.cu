@@ -256,6 +256,39 @@ int bx_det_band_f64(int32_t bandwidth, const double *sub2, const double *sub1, c
   return bxh::check_launch("bx_det_band_f64");
 }
 
+int bx_outer_compact_f64(const double *sub2, const double *sup2, int32_t *count, int32_t *rows,
+                         double *vals_sub2, double *vals_sup2, int64_t capacity, int64_t batch,
+                         int64_t n, int64_t ld, int32_t layout, void *stream) {
+  const char *fn = "bx_outer_compact_f64";
+  int rc = check_common(fn, batch, n, 3, ld, layout);
+  if (rc) return rc;
+  BX_REQUIRE(capacity >= 0, "%s: capacity must be >= 0", fn);
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(sub2 && sup2 && count && (capacity == 0 || (rows && vals_sub2 && vals_sup2)),
+             "%s: null pointer", fn);
+  bx::outer_compact(sub2, sup2, count, rows, vals_sub2, vals_sup2, capacity, batch, n, ld, layout,
+                    (cudaStream_t)stream);
+  return bxh::check_launch(fn);
+}
+
+int bx_mnpdm_sparse_f64(const int32_t *outer_rows, const double *outer_sub2,
+                        const double *outer_sup2, int64_t outer_k, const double *sub1,
+                        const double *main, const double *sup1, const double *rhs, double *x,
+                        int32_t *status, int32_t *index, int64_t *nz_sub2, int64_t batch,
+                        int64_t n, int64_t ld, int32_t layout, void *stream) {
+  const char *fn = "bx_mnpdm_sparse_f64";
+  int rc = check_common(fn, batch, n, 3, ld, layout);
+  if (rc) return rc;
+  BX_REQUIRE(outer_k >= 0, "%s: outer_k must be >= 0", fn);
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(sub1 && main && sup1 && rhs && x && (outer_k == 0 || (outer_rows && outer_sub2 && outer_sup2)),
+             "%s: null pointer", fn);
+  rc = bx::mnpdm_sparse_part(outer_rows, outer_sub2, outer_sup2, outer_k, sub1, main, sup1, rhs, x,
+                             status, index, nz_sub2, batch, n, ld, layout, (cudaStream_t)stream);
+  if (rc) return rc;
+  return bxh::check_launch(fn);
+}
+
 size_t bx_rcond_workspace_bytes(int32_t bandwidth, int64_t batch, int64_t n) {
   return bx::rcond_workspace_bytes(bandwidth == 1 ? 1 : 2, batch, n);
 }

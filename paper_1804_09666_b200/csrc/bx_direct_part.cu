@@ -95,13 +95,21 @@ struct Smem {
       sizeof(double) * (size_t)(kState + kInfo + kWPort + kWLR + kRoots + kMisc);
 };
 
-template <int K, int M, int T, bool VEC, class Lay>
+// +-2 diagonals held sparse (MNPDM's case): per system a row-sorted list of
+// the rows where sub2 or sup2 is nonzero, k slots per system (row -1 pads)
+struct Outer {
+  const int32_t *rows;
+  const double *sub2, *sup2;
+  int64_t k;
+};
+
+template <int K, int M, int T, bool VEC, bool SP, class Lay>
 __global__ void __launch_bounds__(T)
 part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
             const double *__restrict__ ep, const double *__restrict__ f1p,
             const double *__restrict__ f2p, const double *__restrict__ bp,
             double *__restrict__ xp, int32_t *status, int32_t *index, int64_t *nz_out,
-            int64_t batch, int64_t n, Lay lay, int csize, int pf_ahead) {
+            int64_t batch, int64_t n, Lay lay, int csize, int pf_ahead, Outer outer) {
   using SM = Smem<K, M, T>;
   constexpr int NW = SM::NW;
   static_assert(T % 32 == 0 && (NW & (NW - 1)) == 0, "T must be 32 * power of two");
@@ -167,11 +175,11 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     double(&Bv)[G] = gr.b;
     const int64_t i0 = base + g * G;
     if (VEC && i0 + G <= n) {
-      if (K == 2) ld4(c2p + lay(i0, s), A2);
+      if (K == 2 && !SP) ld4(c2p + lay(i0, s), A2);
       ld4(c1p + lay(i0, s), A1);
       ld4(ep + lay(i0, s), E);
       ld4(f1p + lay(i0, s), C1);
-      if (K == 2) ld4(f2p + lay(i0, s), C2);
+      if (K == 2 && !SP) ld4(f2p + lay(i0, s), C2);
       ld4(bp + lay(i0, s), Bv);
       // (slots outside the matrix are masked where the group is consumed:
       // touching the registers here would wait for the load)
@@ -180,16 +188,52 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
       for (int u = 0; u < G; ++u) {
         const int64_t i = i0 + u;
         const bool in = i < n;
-        A2[u] = (K == 2 && in && i >= 2) ? ldg(c2p + lay(i, s)) : 0.0;
+        A2[u] = (K == 2 && !SP && in && i >= 2) ? ldg(c2p + lay(i, s)) : 0.0;
         A1[u] = (in && i >= 1) ? ldg(c1p + lay(i, s)) : 0.0;
         E[u] = in ? ldg(ep + lay(i, s)) : 1.0;  // padding rows: identity
         C1[u] = (in && i <= n - 2) ? ldg(f1p + lay(i, s)) : 0.0;
-        C2[u] = (K == 2 && in && i <= n - 3) ? ldg(f2p + lay(i, s)) : 0.0;
+        C2[u] = (K == 2 && !SP && in && i <= n - 3) ? ldg(f2p + lay(i, s)) : 0.0;
         Bv[u] = in ? ldg(bp + lay(i, s)) : 0.0;
       }
     }
   };
-  constexpr int NA = K == 2 ? 6 : 4;  // input arrays
+  constexpr int NA = K == 2 && !SP ? 6 : 4;  // input arrays streamed
+  // sparse outer diagonals: the slice [ob, oe) of this system's sorted list
+  // that falls in this thread's rows (empty for almost every thread); the
+  // first 8 list rows are fetched with independent loads (one round trip)
+  int ob = 0, oe = 0;
+  auto outer_slice = [&]() {
+    const int32_t *orow = outer.rows + s * outer.k;
+    const int k = (int)outer.k;
+    int32_t r8[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r8[q] = q < k ? __ldg(orow + q) : -1;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      ob += (r8[q] >= 0 && r8[q] < base) ? 1 : 0;
+      oe += (r8[q] >= 0 && r8[q] < base + M) ? 1 : 0;
+    }
+    if (k > 8 && oe == 8) {  // long lists: continue the walk
+      ob = min(ob, 8);
+      while (ob < k && orow[ob] >= 0 && orow[ob] < base) ++ob;
+      oe = ob;
+      while (oe < k && orow[oe] >= 0 && orow[oe] < base + M) ++oe;
+    }
+  };
+  // this thread's first 4 entries in registers (rows compared per row, no
+  // memory access on the elimination chain); more than 4 fall back to loads
+  int32_t er[4] = {-1, -1, -1, -1};
+  double es2[4] = {0, 0, 0, 0}, ep2[4] = {0, 0, 0, 0};
+  auto outer_regs = [&]() {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (ob + q < oe) {
+        const int64_t o = s * outer.k + ob + q;
+        er[q] = __ldg(outer.rows + o);
+        es2[q] = __ldg(outer.sub2 + o);
+        ep2[q] = __ldg(outer.sup2 + o);
+      }
+  };
   if (VEC && t < 2 * NA) {
     // warm L2 (TMA bulk prefetch, no registers) with one array per thread of
     // this CTA's segment (threads 0..NA-1) and of the segment of the CTA
@@ -217,6 +261,10 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   }
 #pragma unroll
   for (int g = 0; g < LA && g < M / G; ++g) load_group(g, ring[g]);
+  if (SP) {  // after the first input loads are in flight
+    outer_slice();
+    outer_regs();
+  }
 #pragma unroll
   for (int g = 0; g < M / G; ++g) {
     if (g + LA < M / G) load_group(g + LA, ring[(g + LA) % RG]);
@@ -225,11 +273,24 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     for (int u = 0; u < G; ++u) {
     const int j = g * G + u;
     const int64_t i = base + j;  // slots outside the matrix are never trusted
-    const double a2 = (K != 2 || i < 2) ? 0.0 : cur.a2[u];
+    double a2 = (K != 2 || i < 2 || SP) ? 0.0 : cur.a2[u];
     const double a1 = i < 1 ? 0.0 : cur.a1[u];
     const double e = cur.e[u];
     const double c1 = i > n - 2 ? 0.0 : cur.c1[u];
-    const double c2 = (K != 2 || i > n - 3) ? 0.0 : cur.c2[u];
+    double c2 = (K != 2 || i > n - 3 || SP) ? 0.0 : cur.c2[u];
+    if (SP && ob < oe) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (er[q] == (int32_t)i) {
+          a2 = i < 2 ? 0.0 : es2[q];
+          c2 = i > n - 3 ? 0.0 : ep2[q];
+        }
+      for (int q = ob + 4; q < oe; ++q)
+        if (outer.rows[s * outer.k + q] == (int32_t)i) {
+          a2 = i < 2 ? 0.0 : outer.sub2[s * outer.k + q];
+          c2 = i > n - 3 ? 0.0 : outer.sup2[s * outer.k + q];
+        }
+    }
     const double b = cur.b[u];
     // reciprocal form on normalised carried rows (p, q, y, w); rows -2, -1
     // are the virtual rows x_{-2} - L_0 = 0, x_{-1} - L_{K-1} = 0
@@ -604,10 +665,11 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
 // ----------------------------------------------------------------------------
 // launch configuration
 // ----------------------------------------------------------------------------
-template <int K, int M, int T, bool VEC, class Lay>
+template <int K, int M, int T, bool VEC, class Lay, bool SP = false>
 static int launch(const double *c2, const double *c1, const double *e, const double *f1,
                   const double *f2, const double *b, double *x, int32_t *st, int32_t *ix,
-                  int64_t *nz, int64_t batch, int64_t n, Lay lay, cudaStream_t stream) {
+                  int64_t *nz, int64_t batch, int64_t n, Lay lay, cudaStream_t stream,
+                  Outer outer = Outer{nullptr, nullptr, nullptr, 0}) {
   constexpr int rows = M * T;
   const int csize = (int)((n + rows - 1) / rows);
   if (csize > 8) {
@@ -619,7 +681,7 @@ static int launch(const double *c2, const double *c1, const double *e, const dou
 #ifdef BX_TRACE
   if (getenv("BX_TRACE_SMEM")) smem = (size_t)atoi(getenv("BX_TRACE_SMEM"));  // occupancy experiments
 #endif
-  auto kern = part_kernel<K, M, T, VEC, Lay>;
+  auto kern = part_kernel<K, M, T, VEC, SP, Lay>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (csize > 1) {  // single-CTA systems write status/index/nz in the kernel
     if (nz) cudaMemsetAsync(nz, 0, sizeof(int64_t) * (size_t)batch, stream);
@@ -651,7 +713,7 @@ static int launch(const double *c2, const double *c1, const double *e, const dou
   int pf_ahead = resident / csize * csize;
   if (const char *env = getenv("BX_PART_PF")) pf_ahead = atoi(env);  // dev knob (0 = off)
   cudaError_t err = cudaLaunchKernelEx(&cfg, kern, c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n,
-                                       lay, csize, pf_ahead);
+                                       lay, csize, pf_ahead, outer);
   if (err != cudaSuccess) {
     bxh::set_error("partitioned solver launch: %s", cudaGetErrorString(err));
     return BX_ERR_CUDA;
@@ -684,6 +746,66 @@ static int dispatch2(const double *c2, const double *c1, const double *e, const 
   if (n <= 512) return launch<K, 8, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
   if (n <= 1024) return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
   return launch<K, 16, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+}
+
+// sparse +-2 diagonals (MNPDM): default shapes only, K = 2
+template <bool VEC, class Lay>
+static int dispatch_sparse(const double *c1, const double *e, const double *f1, const double *b,
+                           double *x, int32_t *st, int32_t *ix, int64_t *nz, int64_t batch,
+                           int64_t n, Lay lay, cudaStream_t stream, Outer o) {
+  if (n <= 256)
+    return launch<2, 8, 32, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
+  if (n <= 512)
+    return launch<2, 8, 64, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
+  if (n <= 1024)
+    return launch<2, 16, 64, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
+  return launch<2, 16, 128, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
+}
+
+// one CTA per system: rows whose sub2 (i >= 2) or sup2 (i <= n-3) is nonzero,
+// in row order (block-wide exclusive scan of per-thread counts); count[s]
+// always, the entries only when capacity > 0 (row -1 pads the slots)
+template <class Lay>
+__global__ void __launch_bounds__(256)
+outer_compact_kernel(const double *__restrict__ c2p, const double *__restrict__ f2p,
+                     int32_t *count, int32_t *rows, double *vs2, double *vp2, int64_t cap,
+                     int64_t n, Lay lay) {
+  const int64_t s = blockIdx.x;
+  const int t = threadIdx.x;
+  const int64_t per = (n + 255) / 256, r0 = t * per, r1 = min(n, r0 + per);
+  auto nzrow = [&](int64_t i) {
+    const double a = i >= 2 ? ldg(c2p + lay(i, s)) : 0.0;
+    const double c = i <= n - 3 ? ldg(f2p + lay(i, s)) : 0.0;
+    return a != 0.0 || c != 0.0;
+  };
+  int cnt = 0;
+  for (int64_t i = r0; i < r1; ++i) cnt += nzrow(i);
+  __shared__ int wsum[8];
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((t & 31) >= o) incl += v;
+  }
+  if ((t & 31) == 31) wsum[t >> 5] = incl;
+  __syncthreads();
+  int off = incl - cnt;
+  for (int w = 0; w < (t >> 5); ++w) off += wsum[w];
+  if (t == 255) count[s] = off + cnt;
+  if (cap <= 0) return;
+  for (int64_t i = r0; i < r1 && off < cap; ++i) {
+    if (!nzrow(i)) continue;
+    rows[s * cap + off] = (int32_t)i;
+    vs2[s * cap + off] = i >= 2 ? ldg(c2p + lay(i, s)) : 0.0;
+    vp2[s * cap + off] = i <= n - 3 ? ldg(f2p + lay(i, s)) : 0.0;
+    ++off;
+  }
+  __syncthreads();
+  const int total = (int)min((int64_t)count[s], cap);
+  for (int64_t j = total + t; j < cap; j += 256) {
+    rows[s * cap + j] = -1;
+    vs2[s * cap + j] = 0.0;
+    vp2[s * cap + j] = 0.0;
+  }
 }
 
 static bool aligned32(const void *p) { return p == nullptr || ((uintptr_t)p & 31u) == 0; }
@@ -721,6 +843,33 @@ int penta_part(bool, const double *c, const double *d, const double *e, const do
                              ld % 4 == 0);
   return part::dispatch<2>(c, d, e, f, g, b, x, st, ix, nz, batch, n, Interleaved{ld}, stream,
                            false);
+}
+
+int outer_compact(const double *sub2, const double *sup2, int32_t *count, int32_t *rows,
+                  double *vsub2, double *vsup2, int64_t cap, int64_t batch, int64_t n, int64_t ld,
+                  int layout, cudaStream_t stream) {
+  if (layout == BX_LAYOUT_SYSTEM_MAJOR)
+    part::outer_compact_kernel<<<(unsigned)batch, 256, 0, stream>>>(sub2, sup2, count, rows, vsub2,
+                                                                   vsup2, cap, n, SystemMajor{ld});
+  else
+    part::outer_compact_kernel<<<(unsigned)batch, 256, 0, stream>>>(sub2, sup2, count, rows, vsub2,
+                                                                   vsup2, cap, n, Interleaved{ld});
+  return BX_OK;
+}
+
+int mnpdm_sparse_part(const int32_t *rows, const double *vsub2, const double *vsup2, int64_t k,
+                      const double *d, const double *e, const double *f, const double *b,
+                      double *x, int32_t *st, int32_t *ix, int64_t *nz, int64_t batch, int64_t n,
+                      int64_t ld, int layout, cudaStream_t stream) {
+  const part::Outer o{rows, vsub2, vsup2, k};
+  if (layout == BX_LAYOUT_SYSTEM_MAJOR) {
+    const bool vec = ld % 4 == 0 && part::aligned32(d) && part::aligned32(e) && part::aligned32(f) &&
+                     part::aligned32(b) && part::aligned32(x);
+    if (vec)
+      return part::dispatch_sparse<true>(d, e, f, b, x, st, ix, nz, batch, n, SystemMajor{ld}, stream, o);
+    return part::dispatch_sparse<false>(d, e, f, b, x, st, ix, nz, batch, n, SystemMajor{ld}, stream, o);
+  }
+  return part::dispatch_sparse<false>(d, e, f, b, x, st, ix, nz, batch, n, Interleaved{ld}, stream, o);
 }
 
 size_t other_workspace_bytes(int solver, int64_t batch, int64_t n) {

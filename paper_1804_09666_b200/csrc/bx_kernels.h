@@ -22,6 +22,13 @@ void residual_inf(int bw, const double *c, const double *d, const double *e, con
 
 // bx_direct_part.cu
 size_t part_workspace_bytes(int bandwidth, int64_t batch, int64_t n);
+int outer_compact(const double *sub2, const double *sup2, int32_t *count, int32_t *rows,
+                  double *vsub2, double *vsup2, int64_t cap, int64_t batch, int64_t n, int64_t ld,
+                  int layout, cudaStream_t stream);
+int mnpdm_sparse_part(const int32_t *rows, const double *vsub2, const double *vsup2, int64_t k,
+                      const double *d, const double *e, const double *f, const double *b,
+                      double *x, int32_t *st, int32_t *ix, int64_t *nz, int64_t batch, int64_t n,
+                      int64_t ld, int layout, cudaStream_t stream);
 // pd_to_td / solve_pd2td_ntdm (bx_pd2td.cu)
 int pd2td(const double *c, const double *d, const double *e, const double *f, const double *g,
           const double *b, double *td, double *te, double *tf, double *tr, int64_t *ops,

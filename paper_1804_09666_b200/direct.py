@@ -20,8 +20,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .core import (OpCounter, PentaMatrix, SolveReport, TriMatrix, _Timer, ptr, stream_handle,
-                   vector_from_layout, workspace)
+from .core import (OpCounter, OuterSparsePenta, PentaMatrix, SolveReport, TriMatrix, _Timer, ptr,
+                   stream_handle, vector_from_layout, workspace)
 from .errors import DimensionMismatch, STATUS_OK, exception_for
 from collections import namedtuple
 
@@ -136,7 +136,26 @@ def solve_npdm(a: PentaMatrix, b, *, algo="sequential", residual=True) -> SolveR
 
 
 def solve_mnpdm(a: PentaMatrix, b, *, algo="sequential", residual=True) -> SolveReport:
-    """Sparsity-aware pentadiagonal solve: 13N-15 + 7 nz(sub2) ops (direct.py:84-100)."""
+    """Sparsity-aware pentadiagonal solve: 13N-15 + 7 nz(sub2) ops (direct.py:84-100).
+
+    ``a`` may be ``PentaMatrix.sparse_outer()``: the partitioned algorithm then
+    streams only sub1/main/sup1/rhs plus the outer-row lists (the sequential,
+    bit-exact algorithm runs on the dense source)."""
+    if isinstance(a, OuterSparsePenta):
+        if _algo(algo) != _lib.ALGO_PARTITIONED:
+            return solve_mnpdm(a.dense, b, algo=algo, residual=residual)
+        b_store = a.rhs(b)
+        x = a.new_vector()
+        status = torch.empty(a.batch, dtype=torch.int32, device=a.device)
+        index = torch.empty(a.batch, dtype=torch.int32, device=a.device)
+        nz = torch.zeros(a.batch, dtype=torch.int64, device=a.device)
+        _, d, e, f, _ = a.rowaligned()
+        timer = _Timer()
+        _lib.call("bx_mnpdm_sparse_f64", ptr(a.rows), ptr(a.vals_sub2), ptr(a.vals_sup2), a.k,
+                  ptr(d), ptr(e), ptr(f), ptr(b_store), ptr(x), ptr(status), ptr(index), ptr(nz),
+                  a.batch, a.n, a.ld, a.layout, stream_handle())
+        timer.end()
+        return _finish(a.dense, x, status, index, timer, b_store, ops_mnpdm(a.n, nz), residual)
     a = _coerce(a, "penta")
     b_store = a.rhs(b)
     x = a.new_vector()

@@ -197,3 +197,25 @@ def test_partitioned_zero_pivot_flagged(cuda, n):
     rep = solve_npdm(A, p[5], algo="partitioned")
     st = host(rep.status)
     assert st[1] == 1 and host(rep.index)[1] == 0 and st[0] == 0 and st[2] == 0
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("n,sparse", [(5, True), (300, True), (1025, True), (4096, True),
+                                      (6000, True), (700, False)])
+def test_mnpdm_sparse_outer(cuda, layout, n, sparse):
+    """+-2 diagonals as per-system row lists (PentaMatrix.sparse_outer): same
+    solution as the oracle MNPDM (tolerance parity of the partitioned path),
+    same nz(sub2) op count; a fully populated band also works (k = n)."""
+    p = W.pd_dominant(40, n, seed=n + 3, sparse_outer=sparse)
+    A = PentaMatrix.from_diagonals(*p[:5], layout=layout)
+    S = A.sparse_outer()
+    xm, _, _, nz = D.mnpdm(*p)
+    rep = solve_mnpdm(S, p[5], algo="partitioned")
+    assert (host(rep.status) == 0).all()
+    assert rel_err(host(rep.x), xm).max() <= REL_TOL
+    assert np.array_equal(host(rep.ops.total), np.array([sum(D.ops_mnpdm(n, int(z)).values()) for z in nz]))
+    if sparse and n >= 8:
+        assert S.k == 4  # rows 0, 1 (sup2) and n-2, n-1 (sub2) -- SURVEY D6
+    # the sequential (bit-exact) algorithm runs on the dense source
+    rep = solve_mnpdm(S, p[5])
+    assert np.array_equal(host(rep.x), xm)

@@ -28,3 +28,28 @@ def test_pipeline_matches_oracle(cuda, solver):
     torch.cuda.synchronize()
     x = xh.numpy()
     assert np.max(np.abs(x - ref) / np.max(np.abs(ref), axis=1, keepdims=True)) <= 1e-10
+
+
+def test_outer_lists_host_matches_device_compaction(cuda):
+    """pipeline.outer_lists (host) == bx_outer_compact_f64 (device), and the
+    sparse-outer pipeline reproduces the device solve."""
+    import torch
+
+    from paper_1804_09666_b200 import PentaMatrix, solve_mnpdm
+    from paper_1804_09666_b200.pipeline import HostPipeline, outer_lists
+    p = W.pd_dominant(24, 1500, seed=4, sparse_outer=True)
+    A = PentaMatrix.from_diagonals(*p[:5], layout="system")
+    S = A.sparse_outer()
+    c, d, e, f, g = (t.cpu().numpy() for t in A.rowaligned())
+    rows, vs, vp = outer_lists(c, g)
+    assert np.array_equal(rows, S.rows.cpu().numpy())
+    assert np.array_equal(vs, S.vals_sub2.cpu().numpy()) and np.array_equal(vp, S.vals_sup2.cpu().numpy())
+    b = np.ascontiguousarray(p[5])
+    host = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (d, e, f, b)]
+    lists = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (rows, vs, vp)]
+    x = torch.empty((24, 1500), dtype=torch.float64).pin_memory()
+    pipe = HostPipeline("mnpdm_sparse", 1500, 5, torch.device("cuda", 0), outer_k=rows.shape[1])
+    pipe.run(host, x, host_outer=lists)
+    torch.cuda.synchronize()
+    ref = solve_mnpdm(S, p[5], algo="partitioned").x.cpu().numpy()
+    assert np.array_equal(x.numpy(), ref)
