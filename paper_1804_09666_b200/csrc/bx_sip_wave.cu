@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
   }
 
   SIP_TR(1);
-  double *xs = sh;          // [4][m] window of the previous iterate
+  // (the forward keeps the previous iterate's window in registers)
   double *ys = sh + 4 * m;  // [3][m]
   double *xn = sh + 7 * m;  // [4][m] window of the new iterate
   // ring of NST stages x NPL plane rows (padded stride mp), filled by TMA bulk
