@@ -148,16 +148,20 @@ hb_gemm_kernel(double *__restrict__ Xa, double *__restrict__ Xb, const int *__re
 
 // P = M X for active factors and r_f = max_i sum_j |delta_ij - P_ij| (inverse.py:90-91,112-113)
 // factor f < B: L (unit diagonal, l1 = L(i,i-1), l2 = L(i,i-m)); f >= B: U (mu, phi, psi)
-__global__ void hb_residual_kernel(const double *__restrict__ Xa, const double *__restrict__ Xb,
-                                   const int *__restrict__ parity, double *__restrict__ P,
-                                   const double *__restrict__ l1, const double *__restrict__ l2,
-                                   const double *__restrict__ mu, const double *__restrict__ phi,
-                                   const double *__restrict__ psi, const int *__restrict__ active_list,
-                                   unsigned long long *rnorm_bits, int64_t nr, int64_t n,
-                                   int64_t m, int64_t batch) {
-  // nr = true order; n = padded order (rows >= nr are identity)
+__global__ void __launch_bounds__(256)
+hb_residual_kernel(const double *__restrict__ Xa, const double *__restrict__ Xb,
+                   const int *__restrict__ parity, double *__restrict__ P,
+                   const double *__restrict__ l1, const double *__restrict__ l2,
+                   const double *__restrict__ mu, const double *__restrict__ phi,
+                   const double *__restrict__ psi, const int *__restrict__ active_list,
+                   unsigned long long *rnorm_bits, int64_t nr, int64_t n, int64_t m,
+                   int64_t batch) {
+  // nr = true order; n = padded order (rows >= nr are identity).  One warp
+  // per row (8 rows per block): coalesced row sweeps, shuffle reductions.
   const int f = active_list[blockIdx.y];
-  const int64_t i = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (i >= n) return;
   const bool lower = f < batch;
   const int64_t s = lower ? f : f - batch;
   const size_t off = (size_t)f * n * n;
@@ -185,9 +189,9 @@ __global__ void hb_residual_kernel(const double *__restrict__ Xa, const double *
   {
     const int64_t t0 = i & ~(int64_t)(TM - 1), t1 = t0 + TM;
     const int64_t z0 = lower ? i + 1 : t0, z1 = lower ? t1 : i;
-    for (int64_t j = z0 + threadIdx.x; j < z1; j += blockDim.x) p[i * n + j] = 0.0;
+    for (int64_t j = z0 + lane; j < z1; j += 32) p[i * n + j] = 0.0;
   }
-  for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+  for (int64_t j = j0 + lane; j < j1; j += 32) {
     // X is triangular: entries of rows k1/k2 outside the triangle are zero by
     // definition (and are never stored in the ping-pong buffers)
     double v = c0 * x[i * n + j];
@@ -198,17 +202,11 @@ __global__ void hb_residual_kernel(const double *__restrict__ Xa, const double *
     p[i * n + j] = v;
     rsum += fabs((i == j ? 1.0 : 0.0) - v);
   }
-  // block reduce the row sum, then a max over rows via the ordered bits of a
-  // non-negative double
-  __shared__ double red[32];
+  // row sum, then a max over rows via the ordered bits of a non-negative double
   for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = rsum;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double tsum = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tsum += red[w];
-    if (tsum != tsum) tsum = INFINITY;
-    atomicMax(rnorm_bits + f, (unsigned long long)__double_as_longlong(tsum));
+  if (lane == 0) {
+    if (rsum != rsum) rsum = INFINITY;
+    atomicMax(rnorm_bits + f, (unsigned long long)__double_as_longlong(rsum));
   }
 }
 
@@ -279,7 +277,7 @@ int hb_residual(const double *Xa, const double *Xb, const int *parity, double *P
                 const int *active_list, int nactive, unsigned long long *rbits, int64_t n,
                 int64_t m, int64_t batch, cudaStream_t stream) {
   const int64_t np_ = hb_pad(n);
-  hb::hb_residual_kernel<<<dim3((unsigned)np_, (unsigned)nactive), 256, 0, stream>>>(
+  hb::hb_residual_kernel<<<dim3((unsigned)((np_ + 7) / 8), (unsigned)nactive), 256, 0, stream>>>(
       Xa, Xb, parity, P, l1, l2, mu, phi, psi, active_list, rbits, n, np_, m, batch);
   return BX_OK;
 }
