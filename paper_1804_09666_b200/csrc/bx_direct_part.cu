@@ -109,7 +109,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
             const double *__restrict__ ep, const double *__restrict__ f1p,
             const double *__restrict__ f2p, const double *__restrict__ bp,
             double *__restrict__ xp, int32_t *status, int32_t *index, int64_t *nz_out,
-            int64_t batch, int64_t n, Lay lay, int csize, int pf_ahead, Outer outer) {
+            int64_t batch, int64_t n, Lay lay, int csize, Outer outer) {
   using SM = Smem<K, M, T>;
   constexpr int NW = SM::NW;
   static_assert(T % 32 == 0 && (NW & (NW - 1)) == 0, "T must be 32 * power of two");
@@ -234,31 +234,19 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
         ep2[q] = __ldg(outer.sup2 + o);
       }
   };
-  if (VEC && t < 2 * NA) {
-    // warm L2 (TMA bulk prefetch, no registers) with one array per thread of
-    // this CTA's segment (threads 0..NA-1) and of the segment of the CTA
-    // `pf_ahead` launches later (threads NA..2NA-1), which starts about one
-    // CTA lifetime from now on the SM this one frees: the HBM stream runs
-    // during the tree phases and the down pass sees L2, not HBM, latency.
-    // Every byte is still fetched from HBM once.
-    const int a = t % NA;
-    const double *arr = a == 0 ? bp : a == 1 ? ep : a == 2 ? c1p : a == 3 ? f1p : a == 4 ? c2p : f2p;
-    int64_t ss = s, sg = seg0;
-    bool go = true;
-    if (t >= NA) {
-      const int64_t b2 = (int64_t)blockIdx.x + pf_ahead;
-      go = pf_ahead > 0 && b2 < (int64_t)gridDim.x;
-      ss = b2 / csize;
-      sg = (b2 % csize) * (int64_t)(T * M);
-    }
-    const int64_t rows = min((int64_t)(T * M), n - sg) & ~(int64_t)1;
-    if (go && rows > 0) {
-      const double *src = arr + lay(sg, ss);
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src),
+  if (VEC && t < NA) {
+    // warm L2 (TMA bulk prefetch, no registers) with this CTA's segment, one
+    // array per thread: the down pass then waits on L2, not HBM, for most
+    // groups.  (Prefetching the segment of the CTA one residency later as well
+    // was measured: no gain for K=2, 2 % slower for K=1.)
+    const double *arr = t == 0 ? bp : t == 1 ? ep : t == 2 ? c1p : t == 3 ? f1p : t == 4 ? c2p : f2p;
+    const int64_t rows = min((int64_t)(T * M), n - seg0) & ~(int64_t)1;
+    if (rows > 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(arr + lay(seg0, s)),
                    "r"((unsigned)(rows * sizeof(double)))
                    : "memory");
-    }
   }
+
 #pragma unroll
   for (int g = 0; g < LA && g < M / G; ++g) load_group(g, ring[g]);
   if (SP) {  // after the first input loads are in flight
@@ -700,20 +688,8 @@ static int launch(const double *c2, const double *c1, const double *e, const dou
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  // CTAs resident at once (rounded to whole clusters): the launch distance
-  // at which a CTA's successor on the same SM slot starts
-  static int resident = -1;  // per configuration (template instance)
-  if (resident < 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
-    resident = per_sm * sms;
-  }
-  int pf_ahead = resident / csize * csize;
-  if (const char *env = getenv("BX_PART_PF")) pf_ahead = atoi(env);  // dev knob (0 = off)
   cudaError_t err = cudaLaunchKernelEx(&cfg, kern, c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n,
-                                       lay, csize, pf_ahead, outer);
+                                       lay, csize, outer);
   if (err != cudaSuccess) {
     bxh::set_error("partitioned solver launch: %s", cudaGetErrorString(err));
     return BX_ERR_CUDA;
