@@ -234,18 +234,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
         ep2[q] = __ldg(outer.sup2 + o);
       }
   };
-  if (VEC && t < NA) {
-    // warm L2 (TMA bulk prefetch, no registers) with this CTA's segment, one
-    // array per thread: the down pass then waits on L2, not HBM, for most
-    // groups.  (Prefetching the segment of the CTA one residency later as well
-    // was measured: no gain for K=2, 2 % slower for K=1.)
-    const double *arr = t == 0 ? bp : t == 1 ? ep : t == 2 ? c1p : t == 3 ? f1p : t == 4 ? c2p : f2p;
-    const int64_t rows = min((int64_t)(T * M), n - seg0) & ~(int64_t)1;
-    if (rows > 0)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(arr + lay(seg0, s)),
-                   "r"((unsigned)(rows * sizeof(double)))
-                   : "memory");
-  }
+
 
 #pragma unroll
   for (int g = 0; g < LA && g < M / G; ++g) load_group(g, ring[g]);
