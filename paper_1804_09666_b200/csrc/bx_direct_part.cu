@@ -197,7 +197,6 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
       }
     }
   };
-  constexpr int NA = K == 2 && !SP ? 6 : 4;  // input arrays streamed
   // sparse outer diagonals: the slice [ob, oe) of this system's sorted list
   // that falls in this thread's rows (empty for almost every thread); the
   // first 8 list rows are fetched with independent loads (one round trip)
