@@ -235,6 +235,8 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   };
 
 
+  const bool first = base == 0;                             // rows 0, 1 of the system
+  const int rend = (int)min(n - base, (int64_t)(M + 4));     // n - base, clamped
 #pragma unroll
   for (int g = 0; g < LA && g < M / G; ++g) load_group(g, ring[g]);
   if (SP) {  // after the first input loads are in flight
@@ -248,12 +250,18 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
 #pragma unroll
     for (int u = 0; u < G; ++u) {
     const int j = g * G + u;
-    const int64_t i = base + j;  // slots outside the matrix are never trusted
-    double a2 = (K != 2 || i < 2 || SP) ? 0.0 : cur.a2[u];
-    const double a1 = i < 1 ? 0.0 : cur.a1[u];
+    const int64_t i = base + j;  // slots outside the matrix are never trusted:
+    // chunk bases are multiples of M, so only rows j < 2 of the first chunk
+    // can fall left of the matrix; the right edge is a 32-bit test on rend
+    double a2 = (K != 2 || SP) ? 0.0 : cur.a2[u];
+    double a1 = cur.a1[u];
+    if (j < 2 && first) {
+      a2 = 0.0;
+      if (j < 1) a1 = 0.0;
+    }
     const double e = cur.e[u];
-    const double c1 = i > n - 2 ? 0.0 : cur.c1[u];
-    double c2 = (K != 2 || i > n - 3 || SP) ? 0.0 : cur.c2[u];
+    const double c1 = j > rend - 2 ? 0.0 : cur.c1[u];
+    double c2 = (K != 2 || SP || j > rend - 3) ? 0.0 : cur.c2[u];
     if (SP && ob < oe) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
