@@ -219,3 +219,23 @@ def test_mnpdm_sparse_outer(cuda, layout, n, sparse):
     # the sequential (bit-exact) algorithm runs on the dense source
     rep = solve_mnpdm(S, p[5])
     assert np.array_equal(host(rep.x), xm)
+
+
+def test_mnpdm_sparse_outer_edge_cases(cuda):
+    """zero leading pivot in the sparse-outer path; n at the minimum (3);
+    a batch whose systems have different outer-row counts (padded lists)."""
+    p = [a.copy() for a in W.pd_dominant(4, 3000, seed=8, sparse_outer=True)]
+    p[2][2, 0] = 0.0                          # system 2: zero leading pivot
+    p[0][1, 1500] = 0.7                       # system 1: one more sub2 entry (row 1502)
+    S = PentaMatrix.from_diagonals(*p[:5], layout="system").sparse_outer()
+    assert S.k == 5 and host(S.count).tolist() == [4, 5, 4, 4]
+    rep = solve_mnpdm(S, p[5], algo="partitioned")
+    st = host(rep.status)
+    assert st[2] == 1 and host(rep.index)[2] == 0 and (st[[0, 1, 3]] == 0).all()
+    ok = [0, 1, 3]
+    xm, _, _, _ = D.mnpdm(*(a[ok] for a in p))
+    assert rel_err(host(rep.x)[ok], xm).max() <= REL_TOL
+    q = W.pd_dominant(3, 3, seed=9)
+    rep = solve_mnpdm(PentaMatrix.from_diagonals(*q[:5]).sparse_outer(), q[5], algo="partitioned")
+    xm, _, _, _ = D.mnpdm(*q)
+    assert rel_err(host(rep.x), xm).max() <= REL_TOL

@@ -166,3 +166,21 @@ def test_det_band_config3(cuda, kind):
     for s in range(0, 64, 16):
         m, e = det_band_mp([q[s] for q in p[:nd]], offs)
         assert _det_rel(res, s, m, e) <= 1e-8, (s, _det_rel(res, s, m, e))
+
+
+def test_det_band_minimal_and_layouts(cuda):
+    """n = 2 (TD) / 3 (PD), against the 60-digit oracle; batched in both
+    layouts gives the same mantissa/exponent."""
+    from oracle.exact import det_band_mp
+    from paper_1804_09666_b200 import exact_det_band
+    t = W.td_symbolic(3, 2, seed=4, zeros=0)
+    for lay in ("interleaved", "system"):
+        r = exact_det_band(TriMatrix.from_diagonals(*t[:3], layout=lay))
+        for s in range(3):
+            m, e = det_band_mp([q[s] for q in t[:3]], [-1, 0, 1])
+            assert _det_rel(r, s, m, e) <= REL_TOL
+    p = W.pd_symbolic(3, 3, seed=4, zeros=0)
+    r = exact_det_band(PentaMatrix.from_diagonals(*p[:5]))
+    for s in range(3):
+        m, e = det_band_mp([q[s] for q in p[:5]], [-2, -1, 0, 1, 2])
+        assert _det_rel(r, s, m, e) <= REL_TOL
