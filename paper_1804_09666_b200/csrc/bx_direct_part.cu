@@ -693,6 +693,18 @@ static int launch(const double *c2, const double *c1, const double *e, const dou
   return BX_OK;
 }
 
+// Above 1024 rows: 1024-row CTAs (T=64) or 2048-row CTAs (T=128)?  Measured
+// on B200 (K=1,2; n = 1100..8192): the 1024-row shape wins whenever it pads
+// fewer rows (n mod 2048 in (0, 1024]: 2500 rows 0.477 vs 0.608 ms) and, at
+// equal padding, when its last CTA is at least half full (n=4096: 0.581 vs
+// 0.592 ms; n=1500: 0.577 vs 0.553 ms the other way).  8-CTA cluster limit.
+static bool use_1k_ctas(int64_t n) {
+  if (n <= 1024) return true;
+  if (n > 8192) return false;
+  const int64_t r = (n - 1) % 2048 + 1;  // rows in the last 2048-row CTA
+  return r <= 1024 || r - 1024 >= 512;
+}
+
 template <int K, bool VEC, class Lay>
 static int dispatch2(const double *c2, const double *c1, const double *e, const double *f1,
                      const double *f2, const double *b, double *x, int32_t *st, int32_t *ix,
@@ -716,7 +728,7 @@ static int dispatch2(const double *c2, const double *c1, const double *e, const 
   }
   if (n <= 256) return launch<K, 8, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
   if (n <= 512) return launch<K, 8, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
-  if (n <= 1024) return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+  if (use_1k_ctas(n)) return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
   return launch<K, 16, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
 }
 
@@ -729,7 +741,7 @@ static int dispatch_sparse(const double *c1, const double *e, const double *f1, 
     return launch<2, 8, 32, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
   if (n <= 512)
     return launch<2, 8, 64, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
-  if (n <= 1024)
+  if (n <= 1024)  // the 1024-row shape measured slower here (n=4096: 0.711 vs 0.641 ms)
     return launch<2, 16, 64, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
   return launch<2, 16, 128, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
 }
