@@ -61,18 +61,40 @@ __device__ __forceinline__ LS ls_t() {  // the indeterminate t
   r.c[1 - LO] = 1.0;
   return r;
 }
-__device__ __forceinline__ int ls_ord(const LS &a) {
-  const int lim = min(a.top, HI);
+// bit k set: coefficient k nonzero (branch-free; the early-exit scans
+// diverged and were ~14 % of the pivot pass)
+__device__ __forceinline__ unsigned ls_nzmask(const LS &a) {
+  unsigned m = 0;
 #pragma unroll
-  for (int k = 0; k < NC; ++k)
-    if (k + LO <= lim && a.c[k] != 0.0) return k + LO;
-  return HI + 1;
+  for (int k = 0; k < NC; ++k) m |= (a.c[k] != 0.0 ? 1u : 0u) << k;
+  return m;
+}
+__device__ __forceinline__ int ls_ord(const LS &a) {
+  const int nb = min(a.top, HI) - LO + 1;  // coefficients below nb are known exactly
+  const unsigned m = nb <= 0 ? 0u : ls_nzmask(a) & ((1u << nb) - 1u);
+  return m ? __ffs(m) - 1 + LO : HI + 1;
 }
 __device__ __forceinline__ int ls_deg(const LS &a) {
+  const unsigned m = ls_nzmask(a);
+  return m ? 31 - __clz(m) + LO : LO - 1;
+}
+// x[j] := x[j + s] / x[j - s] (0 outside), 0 <= s < 16, in registers: a
+// runtime-indexed coefficient array would live in local memory
+__device__ __forceinline__ void ls_shift_down(double (&x)[NC], int s) {
 #pragma unroll
-  for (int k = NC - 1; k >= 0; --k)
-    if (a.c[k] != 0.0) return k + LO;
-  return LO - 1;
+  for (int b = 1; b < NC; b <<= 1) {
+    const bool on = s & b;
+#pragma unroll
+    for (int j = 0; j < NC; ++j) x[j] = on ? (j + b < NC ? x[j + b] : 0.0) : x[j];
+  }
+}
+__device__ __forceinline__ void ls_shift_up(double (&x)[NC], int s) {
+#pragma unroll
+  for (int b = 1; b < NC; b <<= 1) {
+    const bool on = s & b;
+#pragma unroll
+    for (int j = NC - 1; j >= 0; --j) x[j] = on ? (j - b >= 0 ? x[j - b] : 0.0) : x[j];
+  }
 }
 __device__ __forceinline__ LS ls_scale(double s, const LS &a) {
   if (s == 0.0) return ls_const(0.0);  // exact zero
@@ -96,12 +118,20 @@ __device__ __forceinline__ LS ls_mul(const LS &a, const LS &b, bool *ovf) {
 #pragma unroll
   for (int k = 0; k < NC; ++k) r.c[k] = 0.0;
   if (oa + ob < LO) *ovf = true;
+  // coefficients beyond top do not take part: zeroed once here instead of a
+  // per-product test (fma(0, y, r) == r for the finite y of a series)
+  double am[NC], bm[NC];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    am[i] = i + LO <= a.top ? a.c[i] : 0.0;
+    bm[i] = i + LO <= b.top ? b.c[i] : 0.0;
+  }
 #pragma unroll
   for (int i = 0; i < NC; ++i)
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       const int k = i + j + LO;
-      if (k >= 0 && k < NC && i + LO <= a.top && j + LO <= b.top) r.c[k] = fma(a.c[i], b.c[j], r.c[k]);
+      if (k >= 0 && k < NC) r.c[k] = fma(am[i], bm[j], r.c[k]);
     }
   if (a.top >= EXACT && b.top >= EXACT)
     r.top = ls_deg(a) + ls_deg(b) <= HI ? EXACT : HI;
@@ -116,24 +146,28 @@ __device__ __forceinline__ LS ls_inv(const LS &b, bool *ovf) {
     return ls_const(0.0);
   }
   LS r;
-#pragma unroll
-  for (int k = 0; k < NC; ++k) r.c[k] = 0.0;
   if (-v < LO) *ovf = true;
-  const double ib0 = 1.0 / b.c[v - LO];
-  double d[NC];
+  double bs[NC];  // bs[j] = coefficient of t^(v+j), 0 beyond top / the window
+#pragma unroll
+  for (int j = 0; j < NC; ++j) bs[j] = b.c[j];
+  ls_shift_down(bs, v - LO);
+#pragma unroll
+  for (int j = 1; j < NC; ++j)
+    if (v + j > b.top) bs[j] = 0.0;
+  const double ib0 = 1.0 / bs[0];
+  double d[NC];  // d[k] = coefficient of t^(k-v) of 1/b
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
     double acc = 0.0;
 #pragma unroll
-    for (int j = 1; j <= k; ++j) {
-      const int bi = v + j - LO;
-      const double bj = (bi >= 0 && bi < NC && v + j <= b.top) ? b.c[bi] : 0.0;
-      acc = fma(bj, d[k - j], acc);
-    }
+    for (int j = 1; j <= k; ++j) acc = fma(bs[j], d[k - j], acc);
     d[k] = k == 0 ? ib0 : -acc * ib0;
-    const int ord = k - v;
-    if (ord >= LO && ord <= HI) r.c[ord - LO] = d[k];
   }
+  const int sh = v + LO;  // r.c[m] = d[m + sh] (orders LO..HI of the inverse)
+  ls_shift_down(d, sh > 0 ? sh : 0);
+  ls_shift_up(d, sh < 0 ? -sh : 0);
+#pragma unroll
+  for (int k = 0; k < NC; ++k) r.c[k] = d[k];
   if (b.top >= EXACT && ls_deg(b) == v)
     r.top = EXACT;  // exact monomial: exact inverse
   else
@@ -155,7 +189,10 @@ __device__ __forceinline__ int ls_zero(const LS &a) {
 // leading coefficient of a (nonzero) series: the value of t^-ord * a at t = 0
 __device__ __forceinline__ double ls_lead(const LS &a) {
   const int o = ls_ord(a);
-  return o <= HI ? a.c[o - LO] : 0.0;
+  double r = 0.0;  // select chain, not a runtime index (local memory)
+#pragma unroll
+  for (int k = 0; k < NC; ++k) r = k + LO == o ? a.c[k] : r;
+  return r;
 }
 // det accumulator: mantissa in [0.5, 1) (or 0) times 2^exponent, so that the
 // product of n pivots neither overflows nor underflows
