@@ -69,15 +69,14 @@ __device__ __forceinline__ unsigned ls_nzmask(const LS &a) {
   for (int k = 0; k < NC; ++k) m |= (a.c[k] != 0.0 ? 1u : 0u) << k;
   return m;
 }
-__device__ __forceinline__ int ls_ord(const LS &a) {
+// order / degree from a precomputed ls_nzmask (one mask per series serves
+// every test on it)
+__device__ __forceinline__ int ls_ord(const LS &a, unsigned nz) {
   const int nb = min(a.top, HI) - LO + 1;  // coefficients below nb are known exactly
-  const unsigned m = nb <= 0 ? 0u : ls_nzmask(a) & ((1u << nb) - 1u);
+  const unsigned m = nb <= 0 ? 0u : nz & ((1u << nb) - 1u);
   return m ? __ffs(m) - 1 + LO : HI + 1;
 }
-__device__ __forceinline__ int ls_deg(const LS &a) {
-  const unsigned m = ls_nzmask(a);
-  return m ? 31 - __clz(m) + LO : LO - 1;
-}
+__device__ __forceinline__ int ls_deg(unsigned nz) { return nz ? 31 - __clz(nz) + LO : LO - 1; }
 // x[j] := x[j + s] / x[j - s] (0 outside), 0 <= s < 16, in registers: a
 // runtime-indexed coefficient array would live in local memory
 __device__ __forceinline__ void ls_shift_down(double (&x)[NC], int s) {
@@ -112,7 +111,8 @@ __device__ __forceinline__ LS ls_sub(const LS &a, const LS &b) {
   return r;
 }
 __device__ __forceinline__ LS ls_mul(const LS &a, const LS &b, bool *ovf) {
-  const int oa = ls_ord(a), ob = ls_ord(b);
+  const unsigned ma = ls_nzmask(a), mb = ls_nzmask(b);
+  const int oa = ls_ord(a, ma), ob = ls_ord(b, mb);
   if ((oa > HI && a.top >= EXACT) || (ob > HI && b.top >= EXACT)) return ls_const(0.0);
   LS r;
 #pragma unroll
@@ -134,13 +134,13 @@ __device__ __forceinline__ LS ls_mul(const LS &a, const LS &b, bool *ovf) {
       if (k >= 0 && k < NC) r.c[k] = fma(am[i], bm[j], r.c[k]);
     }
   if (a.top >= EXACT && b.top >= EXACT)
-    r.top = ls_deg(a) + ls_deg(b) <= HI ? EXACT : HI;
+    r.top = ls_deg(ma) + ls_deg(mb) <= HI ? EXACT : HI;
   else
     r.top = min(min(a.top + ob, b.top + oa), HI);
   return r;
 }
-__device__ __forceinline__ LS ls_inv(const LS &b, bool *ovf) {
-  const int v = ls_ord(b);
+__device__ __forceinline__ LS ls_inv(const LS &b, unsigned nz, bool *ovf) {
+  const int v = ls_ord(b, nz);
   if (v > HI) {  // not invertible inside the window
     *ovf = true;
     return ls_const(0.0);
@@ -158,9 +158,9 @@ __device__ __forceinline__ LS ls_inv(const LS &b, bool *ovf) {
   double d[NC];  // d[k] = coefficient of t^(k-v) of 1/b
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
-    double acc = 0.0;
+    double acc = 0.0;  // newest d last: one FMA + one multiply after d[k-1]
 #pragma unroll
-    for (int j = 1; j <= k; ++j) acc = fma(bs[j], d[k - j], acc);
+    for (int j = k; j >= 1; --j) acc = fma(bs[j], d[k - j], acc);
     d[k] = k == 0 ? ib0 : -acc * ib0;
   }
   const int sh = v + LO;  // r.c[m] = d[m + sh] (orders LO..HI of the inverse)
@@ -168,7 +168,7 @@ __device__ __forceinline__ LS ls_inv(const LS &b, bool *ovf) {
   ls_shift_up(d, sh < 0 ? -sh : 0);
 #pragma unroll
   for (int k = 0; k < NC; ++k) r.c[k] = d[k];
-  if (b.top >= EXACT && ls_deg(b) == v)
+  if (b.top >= EXACT && ls_deg(nz) == v)
     r.top = EXACT;  // exact monomial: exact inverse
   else
     r.top = min(HI, b.top - 2 * v);
@@ -180,15 +180,15 @@ __device__ __forceinline__ void ls_clamp_below(LS &a, int lo) {
     if (k + LO < lo) a.c[k] = 0.0;
 }
 // identically zero?  +1: yes, 0: no, -1: undecidable inside the window
-__device__ __forceinline__ int ls_zero(const LS &a) {
-  const int o = ls_ord(a);
+__device__ __forceinline__ int ls_zero(const LS &a, unsigned nz) {
+  const int o = ls_ord(a, nz);
   if (o <= min(a.top, HI)) return 0;
   return (a.top >= EXACT || a.top >= HI) ? 1 : -1;
 }
 
 // leading coefficient of a (nonzero) series: the value of t^-ord * a at t = 0
-__device__ __forceinline__ double ls_lead(const LS &a) {
-  const int o = ls_ord(a);
+__device__ __forceinline__ double ls_lead(const LS &a, unsigned nz) {
+  const int o = ls_ord(a, nz);
   double r = 0.0;  // select chain, not a runtime index (local memory)
 #pragma unroll
   for (int k = 0; k < NC; ++k) r = k + LO == o ? a.c[k] : r;
@@ -262,12 +262,13 @@ __device__ void tri_pivots(const double *dp, const double *ep, const double *fp,
       mu = ls_sub(ls_const(e), ls_scale(sg.get(i, 2), l));             // e - l f    (_elim.py:105)
     }
     ls_clamp_below(mu, -ordsum);
-    const int z = ls_zero(mu);
+    unsigned nz = ls_nzmask(mu);
+    const int z = ls_zero(mu, nz);
     if (z < 0) ovf = true;
-    if (z > 0) { mu = ls_t(); ++nsub; }                                // _Substituter
-    ordsum += ls_ord(mu);
-    if (det) det->mul(ls_lead(mu));                                    // exact_det_band: prod mu
-    rec = ls_inv(mu, &ovf);                                            // rec = 1/mu
+    if (z > 0) { mu = ls_t(); nz = 1u << (1 - LO); ++nsub; }          // _Substituter
+    ordsum += ls_ord(mu, nz);
+    if (det) det->mul(ls_lead(mu, nz));                                // exact_det_band: prod mu
+    rec = ls_inv(mu, nz, &ovf);                                        // rec = 1/mu
   }
 }
 
@@ -312,13 +313,14 @@ __device__ void penta_pivots(const double *cp, const double *dp, const double *e
       ph = i <= n - 2 ? ls_sub(ls_const(f), ls_scale(ps1, l1)) : ls_const(0.0);  // (60)
     }
     ls_clamp_below(mu, -ordsum);
-    const int z = ls_zero(mu);
+    unsigned nz = ls_nzmask(mu);
+    const int z = ls_zero(mu, nz);
     if (z < 0) ovf = true;
-    if (z > 0) { mu = ls_t(); ++nsub; }
-    ordsum += ls_ord(mu);
-    if (det) det->mul(ls_lead(mu));
+    if (z > 0) { mu = ls_t(); nz = 1u << (1 - LO); ++nsub; }
+    ordsum += ls_ord(mu, nz);
+    if (det) det->mul(ls_lead(mu, nz));
     r2 = r1;
-    r1 = ls_inv(mu, &ovf);
+    r1 = ls_inv(mu, nz, &ovf);
     ph2 = ph1; ph1 = ph;
     ps2 = ps1; ps1 = g;
   }
