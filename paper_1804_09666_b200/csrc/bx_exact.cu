@@ -147,10 +147,18 @@ __device__ __forceinline__ LS ls_inv(const LS &b, unsigned nz, bool *ovf) {
   }
   LS r;
   if (-v < LO) *ovf = true;
+  // v = 0 on every lane of the warp (the common case: only rows next to a
+  // substituted pivot have a Laurent part) needs no runtime shifts
+  const bool v0 = __all_sync(__activemask(), v == 0);
   double bs[NC];  // bs[j] = coefficient of t^(v+j), 0 beyond top / the window
+  if (v0) {
 #pragma unroll
-  for (int j = 0; j < NC; ++j) bs[j] = b.c[j];
-  ls_shift_down(bs, v - LO);
+    for (int j = 0; j < NC; ++j) bs[j] = j - LO < NC ? b.c[j - LO] : 0.0;
+  } else {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) bs[j] = b.c[j];
+    ls_shift_down(bs, v - LO);
+  }
 #pragma unroll
   for (int j = 1; j < NC; ++j)
     if (v + j > b.top) bs[j] = 0.0;
@@ -163,11 +171,17 @@ __device__ __forceinline__ LS ls_inv(const LS &b, unsigned nz, bool *ovf) {
     for (int j = k; j >= 1; --j) acc = fma(bs[j], d[k - j], acc);
     d[k] = k == 0 ? ib0 : -acc * ib0;
   }
-  const int sh = v + LO;  // r.c[m] = d[m + sh] (orders LO..HI of the inverse)
-  ls_shift_down(d, sh > 0 ? sh : 0);
-  ls_shift_up(d, sh < 0 ? -sh : 0);
+  // r.c[m] = d[m + v + LO] (orders LO..HI of the inverse)
+  if (v0) {
 #pragma unroll
-  for (int k = 0; k < NC; ++k) r.c[k] = d[k];
+    for (int m = 0; m < NC; ++m) r.c[m] = m + LO >= 0 ? d[m + LO] : 0.0;
+  } else {
+    const int sh = v + LO;
+    ls_shift_down(d, sh > 0 ? sh : 0);
+    ls_shift_up(d, sh < 0 ? -sh : 0);
+#pragma unroll
+    for (int k = 0; k < NC; ++k) r.c[k] = d[k];
+  }
   if (b.top >= EXACT && ls_deg(nz) == v)
     r.top = EXACT;  // exact monomial: exact inverse
   else
