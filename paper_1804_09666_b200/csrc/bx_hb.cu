@@ -253,6 +253,54 @@ __global__ void hb_apply_kernel(const double *__restrict__ Xa, const double *__r
   }
 }
 
+// the same product with the system's v staged once in shared memory (the
+// interleaved v[j * batch + s] read costs a 32-byte sector per element) and
+// APPLY_R rows per CTA, 4 rows per warp in flight (X rows are contiguous)
+constexpr int APPLY_R = 32;
+__global__ void __launch_bounds__(256)
+hb_apply_smem_kernel(const double *__restrict__ Xa, const double *__restrict__ Xb,
+                     const int *__restrict__ parity, const double *__restrict__ v,
+                     double *__restrict__ y, const int *__restrict__ act, int64_t nr, int64_t n,
+                     int64_t batch, int upper) {
+  extern __shared__ double vs[];
+  const int64_t s = act[blockIdx.y];
+  const int64_t i0 = (int64_t)blockIdx.x * APPLY_R;
+  const int64_t i1 = min(i0 + APPLY_R, nr);
+  const int f = upper ? (int)(batch + s) : (int)s;
+  const double *xf = (parity[f] ? Xb : Xa) + (size_t)f * n * n;
+  // columns this row block touches: lower [0, i1), upper [i0, nr)
+  const int64_t c0 = upper ? i0 : 0, c1 = upper ? nr : i1;
+  for (int64_t j = c0 + threadIdx.x; j < c1; j += blockDim.x) vs[j - c0] = v[j * batch + s];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ib = i0 + warp * 4;
+  if (ib >= i1) return;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const double *xr[4];
+  int64_t lo[4], hi[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t i = min(ib + r, i1 - 1);
+    xr[r] = xf + (size_t)i * n;
+    lo[r] = upper ? i : 0;
+    hi[r] = ib + r < i1 ? (upper ? nr : i + 1) : lo[r];  // rows past the block: empty
+  }
+  const int64_t jlo = upper ? ib : 0;
+  const int64_t jhi = upper ? nr : min(ib + 4, i1);
+  for (int64_t j = jlo + lane; j < jhi; j += 32) {
+    const double vj = vs[j - c0];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (j >= lo[r] && j < hi[r]) acc[r] = fma(ldg(xr[r] + j), vj, acc[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    double a = acc[r];
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0 && ib + r < i1) y[(ib + r) * batch + s] = a;
+  }
+}
+
 }  // namespace hb
 
 static inline int64_t hb_pad(int64_t n) { return (n + hb::TM - 1) / hb::TM * hb::TM; }
@@ -293,8 +341,20 @@ int hb_init(double *X, const double *mu, int64_t n, int64_t batch, int32_t *zero
 int hb_apply(const double *Xa, const double *Xb, const int *parity, const double *v, double *y,
              const int *act, int nact, int64_t n, int64_t batch, int upper, cudaStream_t stream) {
   const int64_t np_ = hb_pad(n);
-  hb::hb_apply_kernel<<<dim3((unsigned)n, (unsigned)nact), 128, 0, stream>>>(
-      Xa, Xb, parity, v, y, act, n, np_, batch, upper);
+  const size_t smem = sizeof(double) * (size_t)n;
+  if (smem <= 200 * 1024) {
+    static size_t attr = 0;  // opt-in above 48 KB, set once per size class
+    if (smem > 48 * 1024 && smem > attr) {
+      cudaFuncSetAttribute(hb::hb_apply_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      attr = smem;
+    }
+    hb::hb_apply_smem_kernel<<<dim3((unsigned)((n + hb::APPLY_R - 1) / hb::APPLY_R), (unsigned)nact),
+                               256, smem, stream>>>(Xa, Xb, parity, v, y, act, n, np_, batch, upper);
+  } else {
+    hb::hb_apply_kernel<<<dim3((unsigned)n, (unsigned)nact), 128, 0, stream>>>(
+        Xa, Xb, parity, v, y, act, n, np_, batch, upper);
+  }
   return BX_OK;
 }
 
