@@ -621,7 +621,20 @@ class Hb:
                 "note": "achieved counts only the HB GEMM flops but divides by the whole step"}
 
     def cpu_baseline(self, budget_s=5.0):
-        return None
+        # the reference's dense HB is numpy matmul (BLAS); oracle.inverse.sip_hb
+        # restates it with the same numpy calls, timed on a 2-system sample
+        from oracle import inverse as OI
+        sample = 2
+        a = [x[:sample] for x in self.arrs]
+        t0 = time.perf_counter()
+        out = OI.sip_hb(*a[:5], a[5], self.tol[:sample], 500, m=self.m, alpha=self.alpha)
+        dt = time.perf_counter() - t0
+        its = int(np.asarray(out["iterations"]).sum())
+        cores = len(os.sched_getaffinity(0))
+        return {"value": its / dt, "unit": self.unit, "cores": cores, "kind": "port",
+                "sample": f"{sample} of {self.batch} systems ({its} system-iterations incl. ILU(0) and "
+                          f"both dense HB inversions, {dt:.1f} s), numpy restatement of the reference "
+                          f"(oracle/inverse.sip_hb, BLAS on up to {cores} threads)"}
 
 
 class Adi:
