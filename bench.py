@@ -312,10 +312,12 @@ class Direct:
             # chunked H2D / solve / D2H overlap on three streams (pipeline.py)
             from paper_1804_09666_b200.pipeline import HostPipeline
             self.pipe = HostPipeline("mnpdm_sparse" if self.sparse else self.solver, self.n,
-                                     max(1, self.batch // 8), self.x.device, algo=self.args.algo,
+                                     max(1, self.batch // self.args.e2e_chunks), self.x.device,
+                                     algo=self.args.algo,
                                      outer_k=self.host_outer[0].shape[1] if self.sparse else 0)
             self.e2e_path = ("pinned host -> bx C ABI per chunk -> pinned host x (system-major: "
-                             "8 chunks, H2D / solve / D2H overlapped on 3 streams, pipeline.py)")
+                             f"{self.args.e2e_chunks} chunks, H2D / solve / D2H overlapped on 3 "
+                             "streams, pipeline.py)")
         else:
             self.d_e2e = [torch.empty_like(t) for t in self.d_in]
             self.x_e2e = torch.empty_like(self.x)
@@ -907,6 +909,8 @@ def main():
     ap.add_argument("--layout", default=None, choices=["interleaved", "system"],
                     help="C-ABI storage (default: system-major for partitioned, interleaved for sequential)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=8,
+                    help="system chunks of the overlapped host pipeline (e2e leg)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.layout is None:
