@@ -154,6 +154,33 @@ def test_penta_partitioned_sizes(cuda, layout, n, sparse):
     assert np.array_equal(host(rep.ops.total), np.array([sum(D.ops_mnpdm(n, int(z)).values()) for z in nz]))
 
 
+# CTA-shape boundaries of the partitioned solver (use_1k_ctas in
+# bx_direct_part.cu): one 2048-row CTA (1500), 1024-row CTAs with a partial
+# last CTA (1800, 2500, 7000), exact fits (2048, 8192), 2048-row clusters past
+# the 8 x 1024 limit (8193, 12000) and the 16384-row maximum
+@pytest.mark.parametrize("n", [1500, 1800, 2048, 2500, 3500, 7000, 8192, 8193, 12000, 16384])
+@pytest.mark.parametrize("k", [1, 2])
+def test_partitioned_cta_shape_boundaries(cuda, k, n):
+    if k == 1:
+        d = W.td_dominant(6, n, seed=n)
+        x_ref, _, _ = D.ntdm(*d)
+        rep = solve_ntdm(TriMatrix.from_diagonals(*d[:3], layout="system"), d[3], algo="partitioned")
+        assert (host(rep.status) == 0).all()
+        assert rel_err(host(rep.x), x_ref).max() <= REL_TOL
+        return
+    p = W.pd_dominant(6, n, seed=n)
+    x_ref, _, _ = D.npdm(*p)
+    rep = solve_npdm(PentaMatrix.from_diagonals(*p[:5], layout="system"), p[5], algo="partitioned")
+    assert (host(rep.status) == 0).all()
+    assert rel_err(host(rep.x), x_ref).max() <= REL_TOL
+    ps = W.pd_dominant(6, n, seed=n + 1, sparse_outer=True)
+    A = PentaMatrix.from_diagonals(*ps[:5], layout="system")
+    xs_ref, _, _ = D.npdm(*ps)
+    rep = solve_mnpdm(A.sparse_outer(), ps[5], algo="partitioned")
+    assert (host(rep.status) == 0).all()
+    assert rel_err(host(rep.x), xs_ref).max() <= REL_TOL
+
+
 def test_config2_partitioned_full(cuda):
     p = W.pd_dominant(8192, 4096, seed=1)
     A = PentaMatrix.from_diagonals(*p[:5], layout="system")
