@@ -246,6 +246,9 @@ struct Stage {
   __device__ __forceinline__ void wait() const {  // the oldest of DS-1 groups in flight landed
     asm volatile("cp.async.wait_group %0;" ::"n"(DS - 1) : "memory");
   }
+  __device__ __forceinline__ void wait_next() const {  // ... and the row after it
+    asm volatile("cp.async.wait_group %0;" ::"n"(DS - 2) : "memory");
+  }
   __device__ __forceinline__ double get(int64_t row, int v) const { return *slot(row, v); }
 };
 
@@ -303,14 +306,24 @@ __device__ void penta_pivots(const double *cp, const double *dp, const double *e
   };
   for (int64_t i = 0; i < DS - 1; ++i) stage(i);
   // carried: 1/mu and phi of rows i-1, i-2; psi = g (scalar)
-  LS r1 = ls_const(0.0), r2 = ls_const(0.0), ph1 = ls_const(0.0), ph2 = ls_const(0.0);
-  double ps1 = 0.0, ps2 = 0.0;
+  LS r1 = ls_const(0.0), ph1 = ls_const(0.0);
+  double ps1 = 0.0;
+  // l2 = c_i / mu_{i-2}, l2 phi_{i-2} and e_i - psi_{i-2} l2 depend on rows
+  // <= i-1 only: formed one row early (iteration i-1), off the mu_{i-1} -> mu_i
+  // chain (same operations, same rounding)
+  LS t1n = ls_const(0.0), m0n = ls_const(0.0);
   for (int64_t i = 0; i < n; ++i) {
     stage(i + DS - 1);
-    sg.wait();
+    sg.wait_next();
     const double e = sg.get(i, 0);
     const double f = sg.get(i, 1);
     const double g = sg.get(i, 2);
+    const LS t1 = t1n, m0 = m0n;
+    if (i >= 1 && i + 1 < n) {
+      const LS l2n = ls_scale(sg.get(i + 1, 4), r1);                    // c / mu_{i-2}   (54)
+      t1n = ls_mul(l2n, ph1, &ovf);                                     // l2 phi_{i-2}
+      m0n = ls_sub(ls_const(sg.get(i + 1, 0)), ls_scale(ps1, l2n));    // e - psi l2     (56)
+    }
     LS mu, ph;
     if (i == 0) {
       mu = ls_const(e);
@@ -320,10 +333,8 @@ __device__ void penta_pivots(const double *cp, const double *dp, const double *e
       mu = ls_sub(ls_const(e), ls_mul(l1, ph1, &ovf));
       ph = ls_sub(ls_const(f), ls_scale(ps1, l1));
     } else {
-      const LS l2 = ls_scale(sg.get(i, 4), r2);                        // c / mu_{i-2}   (54)
-      const LS l1 = ls_mul(ls_sub(ls_const(sg.get(i, 3)), ls_mul(l2, ph2, &ovf)), r1,
-                           &ovf);                                       // (d - l2 phi)/mu (55)
-      mu = ls_sub(ls_sub(ls_const(e), ls_scale(ps2, l2)), ls_mul(l1, ph1, &ovf));  // (56)
+      const LS l1 = ls_mul(ls_sub(ls_const(sg.get(i, 3)), t1), r1, &ovf);  // (d - l2 phi)/mu (55)
+      mu = ls_sub(m0, ls_mul(l1, ph1, &ovf));                                     // (56)
       ph = i <= n - 2 ? ls_sub(ls_const(f), ls_scale(ps1, l1)) : ls_const(0.0);  // (60)
     }
     ls_clamp_below(mu, -ordsum);
@@ -333,10 +344,9 @@ __device__ void penta_pivots(const double *cp, const double *dp, const double *e
     if (z > 0) { mu = ls_t(); nz = 1u << (1 - LO); ++nsub; }
     ordsum += ls_ord(mu, nz);
     if (det) det->mul(ls_lead(mu, nz));
-    r2 = r1;
     r1 = ls_inv(mu, nz, &ovf);
-    ph2 = ph1; ph1 = ph;
-    ps2 = ps1; ps1 = g;
+    ph1 = ph;
+    ps1 = g;
   }
 }
 
