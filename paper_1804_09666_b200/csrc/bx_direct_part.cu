@@ -262,13 +262,15 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     const double e = cur.e[u];
     const double c1 = j > rend - 2 ? 0.0 : cur.c1[u];
     double c2 = (K != 2 || SP || j > rend - 3) ? 0.0 : cur.c2[u];
-    if (SP && ob < oe) {
+    if (SP) {  // branch-free for the register entries (the row loop stays one block)
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (er[q] == (int32_t)i) {
-          a2 = i < 2 ? 0.0 : es2[q];
-          c2 = i > n - 3 ? 0.0 : ep2[q];
-        }
+      for (int q = 0; q < 4; ++q) {
+        const bool h = er[q] == (int32_t)i;
+        a2 = h ? (i < 2 ? 0.0 : es2[q]) : a2;
+        c2 = h ? (i > n - 3 ? 0.0 : ep2[q]) : c2;
+      }
+    }
+    if (SP && oe - ob > 4) {
       for (int q = ob + 4; q < oe; ++q)
         if (outer.rows[s * outer.k + q] == (int32_t)i) {
           a2 = i < 2 ? 0.0 : outer.sub2[s * outer.k + q];
