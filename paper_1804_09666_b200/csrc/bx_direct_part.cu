@@ -743,7 +743,7 @@ static int dispatch_sparse(const double *c1, const double *e, const double *f1, 
     return launch<2, 8, 32, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
   if (n <= 512)
     return launch<2, 8, 64, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
-  if (n <= 1024)  // the 1024-row shape measured slower here (n=4096: 0.711 vs 0.641 ms)
+  if (n <= 1024)  // the 1024-row shape measured slower here (n=4096: 0.668 vs 0.632 ms)
     return launch<2, 16, 64, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
   return launch<2, 16, 128, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
 }
