@@ -139,6 +139,17 @@ __device__ __forceinline__ LS ls_mul(const LS &a, const LS &b, bool *ovf) {
     r.top = min(min(a.top + ob, b.top + oa), HI);
   return r;
 }
+// d[0..KM) of 1/b for bs[j] = coefficient j of b / t^ord(b), ib0 = 1/bs[0]
+template <int KM>
+__device__ __forceinline__ void ls_inv_coeffs(const double (&bs)[NC], double ib0, double (&d)[NC]) {
+#pragma unroll
+  for (int k = 0; k < KM; ++k) {
+    double acc = 0.0;  // newest d last: one FMA + one multiply after d[k-1]
+#pragma unroll
+    for (int j = k; j >= 1; --j) acc = fma(bs[j], d[k - j], acc);
+    d[k] = k == 0 ? ib0 : -acc * ib0;
+  }
+}
 __device__ __forceinline__ LS ls_inv(const LS &b, unsigned nz, bool *ovf) {
   const int v = ls_ord(b, nz);
   if (v > HI) {  // not invertible inside the window
@@ -164,18 +175,13 @@ __device__ __forceinline__ LS ls_inv(const LS &b, unsigned nz, bool *ovf) {
     if (v + j > b.top) bs[j] = 0.0;
   const double ib0 = 1.0 / bs[0];
   double d[NC];  // d[k] = coefficient of t^(k-v) of 1/b
-#pragma unroll
-  for (int k = 0; k < NC; ++k) {
-    double acc = 0.0;  // newest d last: one FMA + one multiply after d[k-1]
-#pragma unroll
-    for (int j = k; j >= 1; --j) acc = fma(bs[j], d[k - j], acc);
-    d[k] = k == 0 ? ib0 : -acc * ib0;
-  }
   // r.c[m] = d[m + v + LO] (orders LO..HI of the inverse)
-  if (v0) {
+  if (v0) {  // orders 0..HI only: d[HI+1..] would fall outside the window
+    ls_inv_coeffs<HI + 1>(bs, ib0, d);
 #pragma unroll
     for (int m = 0; m < NC; ++m) r.c[m] = m + LO >= 0 ? d[m + LO] : 0.0;
   } else {
+    ls_inv_coeffs<NC>(bs, ib0, d);
     const int sh = v + LO;
     ls_shift_down(d, sh > 0 ? sh : 0);
     ls_shift_up(d, sh < 0 ? -sh : 0);
