@@ -433,7 +433,7 @@ class Sip:
 
     def cpu_baseline(self, budget_s=5.0):
         from oracle import cport
-        sample = 8
+        sample = self.batch  # the whole batch (~1 s on 16 threads): an 8-system sample swung 800-1070
         a = [x[:sample] for x in self.arrs]
         r = cport.rowaligned_penta(*a[:5], m=self.m)
         t0 = time.perf_counter()
@@ -757,7 +757,8 @@ def cpu_reference_arm(args):
         from paper_1804_09666_b200 import workloads as W
         c = SIP_CFG
         metric, unit = "sip_system_iterations_per_s", "system-iterations/s"
-        arrs = W.five_point(4, c["n"], c["m"], rng=np.random.default_rng(c["cfg"]))
+        nsys = min(64, max(16, cport.threads()))  # at least one system per host thread
+        arrs = W.five_point(nsys, c["n"], c["m"], rng=np.random.default_rng(c["cfg"]))
         tol = W.sip_tolerance(arrs[5])
         r = cport.rowaligned_penta(*arrs[:5], m=c["m"])
         its = 0
@@ -769,7 +770,7 @@ def cpu_reference_arm(args):
                 its += int(out["iterations"].sum())
         value = its / sum(times)
         thr = cport.threads()
-        desc, samp = "config 4 SIP", "4 of 64 systems per step (full sip_solve each)"
+        desc, samp = "config 4 SIP", f"{nsys} of 64 systems per step (full sip_solve each)"
     line = {"impl": "reference", "metric": metric, "value": value, "unit": unit,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
