@@ -343,7 +343,7 @@ class Direct:
         rate0, _, _ = cpu_direct_rate(self.solver, self.arrs, min(self.batch, 128))
         sample = int(min(self.batch, max(64, rate0 * budget_s)))
         tot_s, tot_n, passes = 0.0, 0, 0
-        while tot_s < budget_s and passes < 20:
+        while tot_s < budget_s and passes < 1000:  # ~5 s of host work (tiny configs: many passes)
             rate, dt, thr = cpu_direct_rate(self.solver, self.arrs, sample)
             tot_s += dt; tot_n += sample; passes += 1
         return {"value": tot_n / tot_s, "unit": self.unit, "cores": thr, "kind": "port",
