@@ -109,40 +109,78 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
     return;
   }
   // ---- x := A^-1 x (trans = 0) or A^-T x (trans = 1), in place on plane X --
+  // Every row step depends on the rows just solved: those are carried in
+  // register windows (a global write read back one step later costs an L2
+  // round trip per row); same operations in the same order as the plain loops.
   auto solve = [&](int trans) {
     if (!trans) {
+      double win[K + 1];  // X[k .. k+K] as modified so far
+#pragma unroll
+      for (int j = 0; j <= K; ++j) win[j] = j < n ? Wsp(P::X, j) : 0.0;
       for (int64_t k = 0; k < n; ++k) {  // L: row swaps + eliminations
         const int p = (int)Wsp(P::PIV, k);
-        double xk = Wsp(P::X, k);
-        if (p) { const double t = Wsp(P::X, k + p); Wsp(P::X, k + p) = xk; xk = t; Wsp(P::X, k) = xk; }
+        double xk = win[0];
 #pragma unroll
         for (int j = 1; j <= K; ++j)
-          if (k + j < n) Wsp(P::X, k + j) = fma(-Wsp(P::L0 + j - 1, k), xk, Wsp(P::X, k + j));
+          if (p == j) { const double t = win[j]; win[j] = xk; xk = t; }
+        Wsp(P::X, k) = xk;
+#pragma unroll
+        for (int j = 1; j <= K; ++j)
+          if (k + j < n) win[j] = fma(-Wsp(P::L0 + j - 1, k), xk, win[j]);
+#pragma unroll
+        for (int j = 0; j < K; ++j) win[j] = win[j + 1];
+        win[K] = k + K + 1 < n ? Wsp(P::X, k + K + 1) : 0.0;
       }
+      double r[W];  // r[c] = solved X[k + c], c = 1 .. 2K
+#pragma unroll
+      for (int c = 0; c < W; ++c) r[c] = 0.0;
       for (int64_t k = n - 1; k >= 0; --k) {  // U back substitution
         double acc = Wsp(P::X, k);
 #pragma unroll
         for (int c = 1; c < W; ++c)
-          if (k + c < n) acc = fma(-Wsp(P::U0 + c, k), Wsp(P::X, k + c), acc);
-        Wsp(P::X, k) = acc / Wsp(P::U0, k);
+          if (k + c < n) acc = fma(-Wsp(P::U0 + c, k), r[c], acc);
+        const double xk = acc / Wsp(P::U0, k);
+        Wsp(P::X, k) = xk;
+#pragma unroll
+        for (int c = W - 1; c >= 2; --c) r[c] = r[c - 1];
+        r[1] = xk;
       }
     } else {
+      double q[W];  // q[c] = solved X[k - c]
+#pragma unroll
+      for (int c = 0; c < W; ++c) q[c] = 0.0;
       for (int64_t k = 0; k < n; ++k) {  // U^T forward
         double acc = Wsp(P::X, k);
 #pragma unroll
         for (int c = 1; c < W; ++c)
-          if (k - c >= 0) acc = fma(-Wsp(P::U0 + c, k - c), Wsp(P::X, k - c), acc);
-        Wsp(P::X, k) = acc / Wsp(P::U0, k);
+          if (k - c >= 0) acc = fma(-Wsp(P::U0 + c, k - c), q[c], acc);
+        const double xk = acc / Wsp(P::U0, k);
+        Wsp(P::X, k) = xk;
+#pragma unroll
+        for (int c = W - 1; c >= 2; --c) q[c] = q[c - 1];
+        q[1] = xk;
       }
+      double v[K + 1];  // v[j] = current X[k + j], j = 1 .. K
+#pragma unroll
+      for (int j = 0; j <= K; ++j) v[j] = 0.0;
       for (int64_t k = n - 1; k >= 0; --k) {  // L^T backward, swaps undone in reverse
-        double xk = Wsp(P::X, k);
+        double xk = Wsp(P::X, k);  // untouched by the later steps' swaps (indices > k)
 #pragma unroll
         for (int j = 1; j <= K; ++j)
-          if (k + j < n) xk = fma(-Wsp(P::L0 + j - 1, k), Wsp(P::X, k + j), xk);
+          if (k + j < n) xk = fma(-Wsp(P::L0 + j - 1, k), v[j], xk);
         const int p = (int)Wsp(P::PIV, k);
-        if (p) { Wsp(P::X, k) = Wsp(P::X, k + p); Wsp(P::X, k + p) = xk; }
-        else Wsp(P::X, k) = xk;
+        double xnew = xk;
+#pragma unroll
+        for (int j = 1; j <= K; ++j)
+          if (p == j) { xnew = v[j]; v[j] = xk; }
+        if (k + K < n) Wsp(P::X, k + K) = v[K];  // leaves the window: final
+#pragma unroll
+        for (int j = K; j >= 2; --j) v[j] = v[j - 1];
+        v[1] = xnew;
       }
+#pragma unroll
+      for (int j = 1; j <= K; ++j)
+        if (j - 1 < n) Wsp(P::X, j - 1) = v[j];
     }
   };
   auto asum = [&]() {
