@@ -32,10 +32,19 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
                              int64_t n, Lay lay) {
   using P = Planes<K>;
   constexpr int W = P::W;
+  constexpr int DS = 8, NV = W + 1;  // staging ring: DS rows x NV values x 32 threads
+  extern __shared__ double ring[];
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= batch) return;
   const int64_t pl = batch * n;
   auto Wsp = [&](int p, int64_t k) -> double & { return ws[(int64_t)p * pl + k * batch + s]; };
+  // the solves walk the factor planes row by row; their loads cannot be hoisted
+  // past the X stores (same workspace), so row k +- PF is prefetched into L1
+  constexpr int PF = 8;
+  auto pf = [&](int p, int64_t k) {
+    if (k >= 0 && k < n)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(ws + (int64_t)p * pl + k * batch + s));
+  };
   // coefficient of A at (i, i+o), o in -K..K (0 outside the matrix)
   auto A = [&](int64_t i, int o) -> double {
     if (i < 0 || i >= n || i + o < 0 || i + o >= n) return 0.0;
@@ -46,9 +55,19 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
     const double *d = o == -1 ? dp : o == 0 ? ep : fp;
     return ldg(d + lay(i, s));
   };
+  auto pf_row = [&](int64_t i) {  // the 2K+1 coefficients of row i into L1
+    if (i < 0 || i >= n) return;
+    const double *dg[5] = {cp, dp, ep, fp, gp};
+#pragma unroll
+    for (int o = -K; o <= K; ++o) {
+      const double *d = dg[o + 2];
+      if (d) asm volatile("prefetch.global.L1 [%0];" ::"l"(d + lay(i, s)));
+    }
+  };
   // ||A||_1: max column sum
   double anorm = 0.0;
   for (int64_t c = 0; c < n; ++c) {
+    pf_row(c + K + PF);
     double cs = 0.0;
 #pragma unroll
     for (int o = -K; o <= K; ++o) cs += fabs(A(c + o, -o));
@@ -100,6 +119,7 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
       for (int c = 0; c < W - 1; ++c) w[j][c] = w[j + 1][c + 1];
       w[j][W - 1] = 0.0;
     }
+    pf_row(k + 1 + K + PF);
     load_row(k + 1 + K, w[K], k + 1);
   }
   if (singular || anorm == 0.0) {  // LAPACK: rcond = 0 for an exactly singular U
@@ -111,73 +131,131 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
   // ---- x := A^-1 x (trans = 0) or A^-T x (trans = 1), in place on plane X --
   // Every row step depends on the rows just solved: those are carried in
   // register windows (a global write read back one step later costs an L2
-  // round trip per row); same operations in the same order as the plain loops.
+  // round trip per row), and each step's plane values are fetched DS rows
+  // ahead with cp.async into a per-thread shared-memory ring (the plain loads
+  // cannot be hoisted past the X stores: same workspace).  Same operations in
+  // the same order as the plain loops.  Every value staged was written by an
+  // earlier pass, or is read before this pass overwrites it.
+  auto put = [&](int64_t k, int v, int p, int64_t row) {
+    double *d = ring + ((int)(k % DS) * NV + v) * 32 + threadIdx.x;
+    if (row >= 0 && row < n)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(d)),
+                   "l"(&Wsp(p, row))
+                   : "memory");
+    else
+      *d = 0.0;
+  };
+  auto get = [&](int64_t k, int v) -> double { return ring[((int)(k % DS) * NV + v) * 32 + threadIdx.x]; };
+  auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
+  auto wait = [] { asm volatile("cp.async.wait_group %0;" ::"n"(DS - 1) : "memory"); };
+  // one pass: rows k = first, first + dir, ...; stage(k) puts row k's values
+  auto pass = [&](int64_t first, int dir, auto stage, auto body) {
+    for (int d = 0; d < DS - 1; ++d) {
+      const int64_t k = first + (int64_t)d * dir;
+      if (k >= 0 && k < n) stage(k);
+      commit();
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t k = first + i * dir, kn = k + (int64_t)(DS - 1) * dir;
+      if (kn >= 0 && kn < n) stage(kn);
+      commit();
+      wait();
+      body(k);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  };
   auto solve = [&](int trans) {
     if (!trans) {
       double win[K + 1];  // X[k .. k+K] as modified so far
 #pragma unroll
       for (int j = 0; j <= K; ++j) win[j] = j < n ? Wsp(P::X, j) : 0.0;
-      for (int64_t k = 0; k < n; ++k) {  // L: row swaps + eliminations
-        const int p = (int)Wsp(P::PIV, k);
-        double xk = win[0];
+      pass(0, 1,
+           [&](int64_t k) {
+             put(k, 0, P::PIV, k);
 #pragma unroll
-        for (int j = 1; j <= K; ++j)
-          if (p == j) { const double t = win[j]; win[j] = xk; xk = t; }
-        Wsp(P::X, k) = xk;
+             for (int j = 1; j <= K; ++j) put(k, j, P::L0 + j - 1, k);
+             put(k, K + 1, P::X, k + K + 1);
+           },
+           [&](int64_t k) {  // L: row swaps + eliminations
+             const int p = (int)get(k, 0);
+             double xk = win[0];
 #pragma unroll
-        for (int j = 1; j <= K; ++j)
-          if (k + j < n) win[j] = fma(-Wsp(P::L0 + j - 1, k), xk, win[j]);
+             for (int j = 1; j <= K; ++j)
+               if (p == j) { const double t = win[j]; win[j] = xk; xk = t; }
+             Wsp(P::X, k) = xk;
 #pragma unroll
-        for (int j = 0; j < K; ++j) win[j] = win[j + 1];
-        win[K] = k + K + 1 < n ? Wsp(P::X, k + K + 1) : 0.0;
-      }
+             for (int j = 1; j <= K; ++j)
+               if (k + j < n) win[j] = fma(-get(k, j), xk, win[j]);
+#pragma unroll
+             for (int j = 0; j < K; ++j) win[j] = win[j + 1];
+             win[K] = get(k, K + 1);
+           });
       double r[W];  // r[c] = solved X[k + c], c = 1 .. 2K
 #pragma unroll
       for (int c = 0; c < W; ++c) r[c] = 0.0;
-      for (int64_t k = n - 1; k >= 0; --k) {  // U back substitution
-        double acc = Wsp(P::X, k);
+      pass(n - 1, -1,
+           [&](int64_t k) {
+             put(k, 0, P::X, k);
 #pragma unroll
-        for (int c = 1; c < W; ++c)
-          if (k + c < n) acc = fma(-Wsp(P::U0 + c, k), r[c], acc);
-        const double xk = acc / Wsp(P::U0, k);
-        Wsp(P::X, k) = xk;
+             for (int c = 0; c < W; ++c) put(k, 1 + c, P::U0 + c, k);
+           },
+           [&](int64_t k) {  // U back substitution
+             double acc = get(k, 0);
 #pragma unroll
-        for (int c = W - 1; c >= 2; --c) r[c] = r[c - 1];
-        r[1] = xk;
-      }
+             for (int c = 1; c < W; ++c)
+               if (k + c < n) acc = fma(-get(k, 1 + c), r[c], acc);
+             const double xk = acc / get(k, 1);
+             Wsp(P::X, k) = xk;
+#pragma unroll
+             for (int c = W - 1; c >= 2; --c) r[c] = r[c - 1];
+             r[1] = xk;
+           });
     } else {
       double q[W];  // q[c] = solved X[k - c]
 #pragma unroll
       for (int c = 0; c < W; ++c) q[c] = 0.0;
-      for (int64_t k = 0; k < n; ++k) {  // U^T forward
-        double acc = Wsp(P::X, k);
+      pass(0, 1,
+           [&](int64_t k) {
+             put(k, 0, P::X, k);
 #pragma unroll
-        for (int c = 1; c < W; ++c)
-          if (k - c >= 0) acc = fma(-Wsp(P::U0 + c, k - c), q[c], acc);
-        const double xk = acc / Wsp(P::U0, k);
-        Wsp(P::X, k) = xk;
+             for (int c = 0; c < W; ++c) put(k, 1 + c, P::U0 + c, k - c);
+           },
+           [&](int64_t k) {  // U^T forward
+             double acc = get(k, 0);
 #pragma unroll
-        for (int c = W - 1; c >= 2; --c) q[c] = q[c - 1];
-        q[1] = xk;
-      }
+             for (int c = 1; c < W; ++c)
+               if (k - c >= 0) acc = fma(-get(k, 1 + c), q[c], acc);
+             const double xk = acc / get(k, 1);
+             Wsp(P::X, k) = xk;
+#pragma unroll
+             for (int c = W - 1; c >= 2; --c) q[c] = q[c - 1];
+             q[1] = xk;
+           });
       double v[K + 1];  // v[j] = current X[k + j], j = 1 .. K
 #pragma unroll
       for (int j = 0; j <= K; ++j) v[j] = 0.0;
-      for (int64_t k = n - 1; k >= 0; --k) {  // L^T backward, swaps undone in reverse
-        double xk = Wsp(P::X, k);  // untouched by the later steps' swaps (indices > k)
+      pass(n - 1, -1,
+           [&](int64_t k) {
+             put(k, 0, P::X, k);
+             put(k, 1, P::PIV, k);
 #pragma unroll
-        for (int j = 1; j <= K; ++j)
-          if (k + j < n) xk = fma(-Wsp(P::L0 + j - 1, k), v[j], xk);
-        const int p = (int)Wsp(P::PIV, k);
-        double xnew = xk;
+             for (int j = 1; j <= K; ++j) put(k, 1 + j, P::L0 + j - 1, k);
+           },
+           [&](int64_t k) {  // L^T backward, swaps undone in reverse
+             double xk = get(k, 0);  // untouched by the later steps' swaps (indices > k)
 #pragma unroll
-        for (int j = 1; j <= K; ++j)
-          if (p == j) { xnew = v[j]; v[j] = xk; }
-        if (k + K < n) Wsp(P::X, k + K) = v[K];  // leaves the window: final
+             for (int j = 1; j <= K; ++j)
+               if (k + j < n) xk = fma(-get(k, 1 + j), v[j], xk);
+             const int p = (int)get(k, 1);
+             double xnew = xk;
 #pragma unroll
-        for (int j = K; j >= 2; --j) v[j] = v[j - 1];
-        v[1] = xnew;
-      }
+             for (int j = 1; j <= K; ++j)
+               if (p == j) { xnew = v[j]; v[j] = xk; }
+             if (k + K < n) Wsp(P::X, k + K) = v[K];  // leaves the window: final
+#pragma unroll
+             for (int j = K; j >= 2; --j) v[j] = v[j - 1];
+             v[1] = xnew;
+           });
 #pragma unroll
       for (int j = 1; j <= K; ++j)
         if (j - 1 < n) Wsp(P::X, j - 1) = v[j];
@@ -209,6 +287,7 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
   } else {
     est = asum();
     for (int64_t k = 0; k < n; ++k) {
+      pf(P::X, k + PF);
       const double sg = Wsp(P::X, k) >= 0.0 ? 1.0 : -1.0;
       Wsp(P::X, k) = sg;
       Wsp(P::SG, k) = sg;
@@ -226,6 +305,7 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
         same = (Wsp(P::X, k) >= 0.0 ? 1.0 : -1.0) == Wsp(P::SG, k);
       if (same || est <= estold) break;  // repeated sign vector / no increase (dlacn2 70-90)
       for (int64_t k = 0; k < n; ++k) {
+        pf(P::X, k + PF);
         const double sg = Wsp(P::X, k) >= 0.0 ? 1.0 : -1.0;
         Wsp(P::X, k) = sg;
         Wsp(P::SG, k) = sg;
@@ -267,17 +347,17 @@ int rcond_band(int kind, const double *c, const double *d, const double *e, cons
   const dim3 grid((unsigned)((batch + threads - 1) / threads));
   if (kind == 1) {
     if (layout == BX_LAYOUT_INTERLEAVED)
-      rc::rcond_kernel<1><<<grid, threads, 0, stream>>>(c, d, e, f, g, rcond, st, ix, ws, batch, n,
+      rc::rcond_kernel<1><<<grid, threads, sizeof(double) * 8 * 4 * 32, stream>>>(c, d, e, f, g, rcond, st, ix, ws, batch, n,
                                                        Interleaved{ld});
     else
-      rc::rcond_kernel<1><<<grid, threads, 0, stream>>>(c, d, e, f, g, rcond, st, ix, ws, batch, n,
+      rc::rcond_kernel<1><<<grid, threads, sizeof(double) * 8 * 4 * 32, stream>>>(c, d, e, f, g, rcond, st, ix, ws, batch, n,
                                                        SystemMajor{ld});
   } else {
     if (layout == BX_LAYOUT_INTERLEAVED)
-      rc::rcond_kernel<2><<<grid, threads, 0, stream>>>(c, d, e, f, g, rcond, st, ix, ws, batch, n,
+      rc::rcond_kernel<2><<<grid, threads, sizeof(double) * 8 * 6 * 32, stream>>>(c, d, e, f, g, rcond, st, ix, ws, batch, n,
                                                        Interleaved{ld});
     else
-      rc::rcond_kernel<2><<<grid, threads, 0, stream>>>(c, d, e, f, g, rcond, st, ix, ws, batch, n,
+      rc::rcond_kernel<2><<<grid, threads, sizeof(double) * 8 * 6 * 32, stream>>>(c, d, e, f, g, rcond, st, ix, ws, batch, n,
                                                        SystemMajor{ld});
   }
   return BX_OK;
