@@ -38,13 +38,7 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
   if (s >= batch) return;
   const int64_t pl = batch * n;
   auto Wsp = [&](int p, int64_t k) -> double & { return ws[(int64_t)p * pl + k * batch + s]; };
-  // the solves walk the factor planes row by row; their loads cannot be hoisted
-  // past the X stores (same workspace), so row k +- PF is prefetched into L1
-  constexpr int PF = 8;
-  auto pf = [&](int p, int64_t k) {
-    if (k >= 0 && k < n)
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(ws + (int64_t)p * pl + k * batch + s));
-  };
+  constexpr int PF = 8;  // anorm: rows prefetched ahead into L1
   // coefficient of A at (i, i+o), o in -K..K (0 outside the matrix)
   auto A = [&](int64_t i, int o) -> double {
     if (i < 0 || i >= n || i + o < 0 || i + o >= n) return 0.0;
@@ -63,6 +57,43 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
       const double *d = dg[o + 2];
       if (d) asm volatile("prefetch.global.L1 [%0];" ::"l"(d + lay(i, s)));
     }
+  };
+  auto put = [&](int64_t k, int v, int p, int64_t row) {
+    double *d = ring + ((int)(k % DS) * NV + v) * 32 + threadIdx.x;
+    if (row >= 0 && row < n)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(d)),
+                   "l"(&Wsp(p, row))
+                   : "memory");
+    else
+      *d = 0.0;
+  };
+  auto putp = [&](int64_t k, int v, const double *g) {  // g == nullptr: the value is 0
+    double *d = ring + ((int)(k % DS) * NV + v) * 32 + threadIdx.x;
+    if (g)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(d)),
+                   "l"(g)
+                   : "memory");
+    else
+      *d = 0.0;
+  };
+  auto get = [&](int64_t k, int v) -> double { return ring[((int)(k % DS) * NV + v) * 32 + threadIdx.x]; };
+  auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
+  auto wait = [] { asm volatile("cp.async.wait_group %0;" ::"n"(DS - 1) : "memory"); };
+  // one pass: rows k = first, first + dir, ...; stage(k) puts row k's values
+  auto pass = [&](int64_t first, int dir, auto stage, auto body) {
+    for (int d = 0; d < DS - 1; ++d) {
+      const int64_t k = first + (int64_t)d * dir;
+      if (k >= 0 && k < n) stage(k);
+      commit();
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t k = first + i * dir, kn = k + (int64_t)(DS - 1) * dir;
+      if (kn >= 0 && kn < n) stage(kn);
+      commit();
+      wait();
+      body(k);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   };
   // ||A||_1: max column sum
   double anorm = 0.0;
@@ -89,7 +120,17 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
   for (int j = 0; j <= K; ++j) load_row(j, w[j], 0);
   bool singular = false;
   int64_t zrow = -1;
-  for (int64_t k = 0; k < n; ++k) {
+  const double *dg[5] = {cp, dp, ep, fp, gp};
+  pass(0, 1,
+       [&](int64_t k) {  // row k+1+K, columns k+1 .. k+1+2K
+         const int64_t i = k + 1 + K;
+#pragma unroll
+         for (int o = -K; o <= K; ++o) {
+           const double *d = dg[o + 2];
+           putp(k, K + o, (d && i < n && i + o >= 0 && i + o < n) ? d + lay(i, s) : nullptr);
+         }
+       },
+       [&](int64_t k) {
     int p = 0;
     double best = fabs(w[0][0]);
 #pragma unroll
@@ -119,9 +160,9 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
       for (int c = 0; c < W - 1; ++c) w[j][c] = w[j + 1][c + 1];
       w[j][W - 1] = 0.0;
     }
-    pf_row(k + 1 + K + PF);
-    load_row(k + 1 + K, w[K], k + 1);
-  }
+#pragma unroll
+    for (int c = 0; c < W; ++c) w[K][c] = get(k, c);
+  });
   if (singular || anorm == 0.0) {  // LAPACK: rcond = 0 for an exactly singular U
     rcond[s] = 0.0;
     set_status(status, index, s, singular ? BX_STATUS_SINGULAR : BX_STATUS_OK,
@@ -136,34 +177,6 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
   // cannot be hoisted past the X stores: same workspace).  Same operations in
   // the same order as the plain loops.  Every value staged was written by an
   // earlier pass, or is read before this pass overwrites it.
-  auto put = [&](int64_t k, int v, int p, int64_t row) {
-    double *d = ring + ((int)(k % DS) * NV + v) * 32 + threadIdx.x;
-    if (row >= 0 && row < n)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(d)),
-                   "l"(&Wsp(p, row))
-                   : "memory");
-    else
-      *d = 0.0;
-  };
-  auto get = [&](int64_t k, int v) -> double { return ring[((int)(k % DS) * NV + v) * 32 + threadIdx.x]; };
-  auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
-  auto wait = [] { asm volatile("cp.async.wait_group %0;" ::"n"(DS - 1) : "memory"); };
-  // one pass: rows k = first, first + dir, ...; stage(k) puts row k's values
-  auto pass = [&](int64_t first, int dir, auto stage, auto body) {
-    for (int d = 0; d < DS - 1; ++d) {
-      const int64_t k = first + (int64_t)d * dir;
-      if (k >= 0 && k < n) stage(k);
-      commit();
-    }
-    for (int64_t i = 0; i < n; ++i) {
-      const int64_t k = first + i * dir, kn = k + (int64_t)(DS - 1) * dir;
-      if (kn >= 0 && kn < n) stage(kn);
-      commit();
-      wait();
-      body(k);
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-  };
   auto solve = [&](int trans) {
     if (!trans) {
       double win[K + 1];  // X[k .. k+K] as modified so far
@@ -263,16 +276,25 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
   };
   auto asum = [&]() {
     double a = 0.0;
-    for (int64_t k = 0; k < n; ++k) a += fabs(Wsp(P::X, k));
+    pass(0, 1, [&](int64_t k) { put(k, 0, P::X, k); }, [&](int64_t k) { a += fabs(get(k, 0)); });
     return a;
+  };
+  auto signs = [&]() {  // x := sign(x), remembered in SG
+    pass(0, 1, [&](int64_t k) { put(k, 0, P::X, k); },
+         [&](int64_t k) {
+           const double sg = get(k, 0) >= 0.0 ? 1.0 : -1.0;
+           Wsp(P::X, k) = sg;
+           Wsp(P::SG, k) = sg;
+         });
   };
   auto iamax = [&]() {  // first index of max |x|
     int64_t j = 0;
     double b = -1.0;
-    for (int64_t k = 0; k < n; ++k) {
-      const double v = fabs(Wsp(P::X, k));
-      if (v > b) { b = v; j = k; }
-    }
+    pass(0, 1, [&](int64_t k) { put(k, 0, P::X, k); },
+         [&](int64_t k) {
+           const double v = fabs(get(k, 0));
+           if (v > b) { b = v; j = k; }
+         });
     return j;
   };
   auto unit = [&](int64_t j) {
@@ -286,12 +308,7 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
     est = fabs(Wsp(P::X, 0));
   } else {
     est = asum();
-    for (int64_t k = 0; k < n; ++k) {
-      pf(P::X, k + PF);
-      const double sg = Wsp(P::X, k) >= 0.0 ? 1.0 : -1.0;
-      Wsp(P::X, k) = sg;
-      Wsp(P::SG, k) = sg;
-    }
+    signs();
     solve(1);
     int64_t j = iamax();
     int iter = 2;
@@ -301,15 +318,10 @@ __global__ void rcond_kernel(const double *__restrict__ cp, const double *__rest
       const double estold = est;
       est = asum();
       bool same = true;
-      for (int64_t k = 0; k < n && same; ++k)
-        same = (Wsp(P::X, k) >= 0.0 ? 1.0 : -1.0) == Wsp(P::SG, k);
+      pass(0, 1, [&](int64_t k) { put(k, 0, P::X, k); put(k, 1, P::SG, k); },
+           [&](int64_t k) { same = same && (get(k, 0) >= 0.0 ? 1.0 : -1.0) == get(k, 1); });
       if (same || est <= estold) break;  // repeated sign vector / no increase (dlacn2 70-90)
-      for (int64_t k = 0; k < n; ++k) {
-        pf(P::X, k + PF);
-        const double sg = Wsp(P::X, k) >= 0.0 ? 1.0 : -1.0;
-        Wsp(P::X, k) = sg;
-        Wsp(P::SG, k) = sg;
-      }
+      signs();
       solve(1);
       const int64_t jlast = j;
       j = iamax();
