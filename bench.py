@@ -194,7 +194,6 @@ def cpu_direct_rate(solver, arrs, sample):
 # ---------------------------------------------------------------------------
 class Direct:
     metric, unit, scaling = "systems_solved_per_s", "systems/s", "weak"
-    launches_per_step = 1
 
     def __init__(self, args, rank, dev, name):
         import torch
@@ -238,6 +237,8 @@ class Direct:
             self.bytes_per_row = 40
             self.outer_bytes = batch * self.outer_k * (4 + 8 + 8)
         self.units = batch
+        # partitioned: the solver kernel + the status / re-solve pass (direct_fixup)
+        self.launches_per_step = 2 if args.algo == "partitioned" and not self.sparse else 1
         gb = self.bytes_per_row * batch * n / 1e9
         # inputs that fit the 126 MB L2 (config 1: 42 MB) are flushed out of it
         # before every timed step (a 512 MB write, outside the step's events)
@@ -642,7 +643,7 @@ class Hb:
 class Adi:
     """Config 5: one ADI step on an 8192^2 grid (x-sweep, transpose / all-to-all, y-sweep)."""
     metric, unit, scaling = "systems_solved_per_s", "systems/s", "strong"
-    launches_per_step = 3
+    launches_per_step = 5  # 2 x (partitioned NTDM + status pass) + transpose
 
     def __init__(self, args, rank, dev, world, n=8192):
         import torch

@@ -27,14 +27,21 @@ class CudaBackend:
 
     def __init__(self, device):
         self.device = device
+        self._ws = {}
 
     def tri_solve(self, sub1, main, sup1, rhs, out):
         from .core import ptr, stream_handle
         B, n = main.shape
         status = torch.empty(B, dtype=torch.int32, device=self.device)
+        ws = self._ws.get((B, n))
+        if ws is None:  # flags + re-solve scratch of the partitioned path, allocated once
+            nbytes = _lib.lib().bx_workspace_bytes(_lib.SOLVER["ntdm"], B, n, _lib.LAYOUT_SYSTEM_MAJOR,
+                                                   _lib.ALGO_PARTITIONED)
+            ws = self._ws[(B, n)] = torch.empty(max(int(nbytes), 256), dtype=torch.uint8,
+                                                device=self.device)
         _lib.call("bx_ntdm_f64", ptr(sub1), ptr(main), ptr(sup1), ptr(rhs), ptr(out), ptr(status),
                   None, B, n, main.stride(0), _lib.LAYOUT_SYSTEM_MAJOR, _lib.ALGO_PARTITIONED,
-                  None, 0, stream_handle())
+                  ptr(ws), ws.numel(), stream_handle())
         return status
 
     def transpose(self, src, dst):

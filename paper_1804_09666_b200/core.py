@@ -66,9 +66,22 @@ def _to_device(a, device):
     return torch.from_numpy(np.ascontiguousarray(a)).to(device=device)
 
 
-def pack_rows(arr, n, first_row, layout, device, batch):
+def padded_ld(n):
+    """System-major leading dimension of the band containers: n rounded up to
+    4 doubles, so every system starts 32-byte aligned (the streaming
+    partitioned kernel's vector loads, bx_direct_stream.cu)."""
+    return (n + 3) // 4 * 4
+
+
+def _system_major(batch, n, ld, device):
+    ld = n if ld is None else ld
+    return torch.zeros((batch, ld), dtype=torch.float64, device=device)[:, :n]
+
+
+def pack_rows(arr, n, first_row, layout, device, batch, ld=None):
     """Reference-length diagonal (B, L) -> row-aligned device storage whose
-    rows first_row .. first_row+L-1 hold it (other slots zero)."""
+    rows first_row .. first_row+L-1 hold it (other slots zero); system-major
+    storage with leading dimension ld (default n)."""
     t = _to_device(arr, device)
     if t.shape[0] != batch:
         raise DimensionMismatch(f"batch {t.shape[0]} != {batch}")
@@ -77,7 +90,7 @@ def pack_rows(arr, n, first_row, layout, device, batch):
         out = torch.zeros((n, batch), dtype=torch.float64, device=device)
         out[first_row:first_row + L].copy_(t.t())
     else:
-        out = torch.zeros((batch, n), dtype=torch.float64, device=device)
+        out = _system_major(batch, n, ld, device)
         out[:, first_row:first_row + L].copy_(t)
     return out
 
@@ -89,14 +102,19 @@ def unpack_rows(t, first_row, length, layout):
     return t[:, first_row:first_row + length]
 
 
-def vector_to_layout(v, n, layout, device):
-    """(B, n) host/device vector -> device storage of the layout."""
+def vector_to_layout(v, n, layout, device, ld=None):
+    """(B, n) host/device vector -> device storage of the layout (system-major:
+    leading dimension ld, default n)."""
     t = _to_device(v, device)
     if t.shape[1] != n:
         raise DimensionMismatch(f"rhs has length {t.shape[1]}, expected {n}")
     if layout == _lib.LAYOUT_INTERLEAVED:
         return t.t().contiguous()
-    return t.contiguous()
+    if ld is None or ld == n:
+        return t.contiguous()
+    out = _system_major(t.shape[0], n, ld, device)
+    out.copy_(t)
+    return out
 
 
 def vector_from_layout(t, layout):
@@ -146,7 +164,8 @@ class _Band:
                 raise InvalidInput(f"{nm}: batch {m.shape[0]} != {batch}")
             if m.shape[1] != n - abs(off):
                 raise InvalidInput(f"diagonal lengths do not match n={n} ({nm} has {m.shape[1]})")
-        diags = [pack_rows(m, n, -off if off < 0 else 0, lay, device, batch)
+        ld = padded_ld(n) if lay == _lib.LAYOUT_SYSTEM_MAJOR else None
+        diags = [pack_rows(m, n, -off if off < 0 else 0, lay, device, batch, ld)
                  for m, off in zip(mats, cls.offsets)]
         return n, batch, diags, lay, single, device
 
@@ -168,12 +187,13 @@ class _Band:
             raise DimensionMismatch(f"rhs batch {bb.shape[0]} != {self.batch}")
         if bb.shape[1] != self.n:
             raise DimensionMismatch(f"rhs length {bb.shape[1]}, expected {self.n}")
-        return vector_to_layout(bb, self.n, self.layout, self.device)
+        return vector_to_layout(bb, self.n, self.layout, self.device, self.ld)
 
     def new_vector(self):
+        """Solution storage with the container's layout and leading dimension."""
         if self.layout == _lib.LAYOUT_INTERLEAVED:
             return torch.empty((self.n, self.batch), dtype=torch.float64, device=self.device)
-        return torch.empty((self.batch, self.n), dtype=torch.float64, device=self.device)
+        return torch.empty((self.batch, self.ld), dtype=torch.float64, device=self.device)[:, :self.n]
 
     def to_dense(self):
         """Dense (B, n, n) float64 host copy, for oracles and small reports (core.py:148-155)."""

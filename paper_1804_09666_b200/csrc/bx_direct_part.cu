@@ -809,26 +809,84 @@ static int dispatch(const double *c2, const double *c1, const double *e, const d
 
 }  // namespace part
 
-size_t part_workspace_bytes(int, int64_t, int64_t) { return 0; }
-
-int ntdm_part(const double *d, const double *e, const double *f, const double *b, double *x,
-              double *, int32_t *st, int32_t *ix, int64_t batch, int64_t n, int64_t ld, int layout,
-              cudaStream_t stream) {
-  if (layout == BX_LAYOUT_SYSTEM_MAJOR)
-    return part::dispatch<1>(nullptr, d, e, f, nullptr, b, x, st, ix, nullptr, batch, n,
-                             SystemMajor{ld}, stream, ld % 4 == 0);
-  return part::dispatch<1>(nullptr, d, e, f, nullptr, b, x, st, ix, nullptr, batch, n,
-                           Interleaved{ld}, stream, false);
+// Workspace of the partitioned path: per-system flags (zero / non-finite
+// pivots of the partitioned elimination) and the re-solve scratch of
+// direct_fixup (bx_direct_seq.cu).
+// BX_PART_SEG=1 (developer knob, experiment): use the segment-resident kernel
+// (bx_direct_seg.cu; measured slower than part_kernel)
+static bool seg_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *env = getenv("BX_PART_SEG");
+    v = env ? atoi(env) : 0;
+  }
+  return v != 0;
 }
 
-int penta_part(bool, const double *c, const double *d, const double *e, const double *f,
-               const double *g, const double *b, double *x, double *, int32_t *st, int32_t *ix,
+static size_t flag_bytes(int64_t batch) { return ((size_t)batch * 8 * 4 + 255) / 256 * 256; }
+size_t part_workspace_bytes(int bandwidth, int64_t batch, int64_t n) {
+  return 2 * flag_bytes(batch) + 8 * fixup_scratch_doubles(bandwidth == 1 ? 0 : 1, n);
+}
+
+// workspace: flags [batch][8] | nz parts [batch][8] | re-solve scratch
+static void carve(double *ws, int64_t batch, int32_t *&flags, int32_t *&nzpart, double *&scratch) {
+  char *p = reinterpret_cast<char *>(ws);
+  flags = reinterpret_cast<int32_t *>(p);
+  nzpart = reinterpret_cast<int32_t *>(p + flag_bytes(batch));
+  scratch = reinterpret_cast<double *>(p + 2 * flag_bytes(batch));
+}
+
+int ntdm_part(const double *d, const double *e, const double *f, const double *b, double *x,
+              double *ws, int32_t *st, int32_t *ix, int64_t batch, int64_t n, int64_t ld, int layout,
+              cudaStream_t stream) {
+  int32_t *flags, *nzpart;
+  double *scratch;
+  carve(ws, batch, flags, nzpart, scratch);
+  const double *ptrs[] = {d, e, f, b, x};
+  int rc = BX_ERR_UNSUPPORTED, fs = 1;
+  if (seg_enabled() && seg_applicable(ptrs, 5, n, ld, layout))
+    rc = seg_solve(1, nullptr, d, e, f, nullptr, b, x, flags, nullptr, batch, n, ld, stream, &fs);
+  if (rc == BX_ERR_UNSUPPORTED) {
+    fs = 1;
+    if (layout == BX_LAYOUT_SYSTEM_MAJOR)
+      rc = part::dispatch<1>(nullptr, d, e, f, nullptr, b, x, flags, nullptr, nullptr, batch, n,
+                             SystemMajor{ld}, stream, ld % 4 == 0);
+    else
+      rc = part::dispatch<1>(nullptr, d, e, f, nullptr, b, x, flags, nullptr, nullptr, batch, n,
+                             Interleaved{ld}, stream, false);
+  }
+  if (rc != BX_OK) return rc;
+  direct_fixup(0, nullptr, d, e, f, nullptr, b, x, scratch, flags, fs, nullptr, st, ix, nullptr,
+               batch, n, ld, layout, stream);
+  return bxh::check_launch("partitioned solver re-solve");
+}
+
+int penta_part(bool mod, const double *c, const double *d, const double *e, const double *f,
+               const double *g, const double *b, double *x, double *ws, int32_t *st, int32_t *ix,
                int64_t *nz, int64_t batch, int64_t n, int64_t ld, int layout, cudaStream_t stream) {
-  if (layout == BX_LAYOUT_SYSTEM_MAJOR)
-    return part::dispatch<2>(c, d, e, f, g, b, x, st, ix, nz, batch, n, SystemMajor{ld}, stream,
-                             ld % 4 == 0);
-  return part::dispatch<2>(c, d, e, f, g, b, x, st, ix, nz, batch, n, Interleaved{ld}, stream,
-                           false);
+  int32_t *flags, *nzpart;
+  double *scratch;
+  carve(ws, batch, flags, nzpart, scratch);
+  const double *ptrs[] = {c, d, e, f, g, b, x};
+  int rc = BX_ERR_UNSUPPORTED, fs = 1;
+  bool seg = false;
+  if (seg_enabled() && seg_applicable(ptrs, 7, n, ld, layout)) {
+    rc = seg_solve(2, c, d, e, f, g, b, x, flags, nz ? nzpart : nullptr, batch, n, ld, stream, &fs);
+    seg = rc != BX_ERR_UNSUPPORTED;
+  }
+  if (!seg) {
+    fs = 1;
+    if (layout == BX_LAYOUT_SYSTEM_MAJOR)
+      rc = part::dispatch<2>(c, d, e, f, g, b, x, flags, nullptr, nz, batch, n, SystemMajor{ld},
+                             stream, ld % 4 == 0);
+    else
+      rc = part::dispatch<2>(c, d, e, f, g, b, x, flags, nullptr, nz, batch, n, Interleaved{ld},
+                             stream, false);
+  }
+  if (rc != BX_OK) return rc;
+  direct_fixup(mod ? 2 : 1, c, d, e, f, g, b, x, scratch, flags, fs, seg && nz ? nzpart : nullptr,
+               st, ix, nz, batch, n, ld, layout, stream);
+  return bxh::check_launch("partitioned solver re-solve");
 }
 
 int outer_compact(const double *sub2, const double *sup2, int32_t *count, int32_t *rows,

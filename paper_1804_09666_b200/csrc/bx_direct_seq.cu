@@ -31,15 +31,13 @@ __device__ __forceinline__ void fill_nan(double *x, int64_t n, int64_t s, Lay la
 // ----------------------------------------------------------------------------
 // NTDM
 // ----------------------------------------------------------------------------
+// one system (s) with its scratch column w of a Scratch{ws}: the kernel body
 template <class Lay>
-__global__ void __launch_bounds__(kSeqThreads)
-ntdm_seq_kernel(const double *__restrict__ d, const double *__restrict__ e,
-                const double *__restrict__ f, const double *__restrict__ b,
-                double *__restrict__ x, double *__restrict__ recw, int32_t *status,
-                int32_t *index, int64_t batch, int64_t n, Lay lay) {
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= batch) return;
-  const Scratch ws{batch};
+__device__ __forceinline__ void ntdm_one(const double *__restrict__ d, const double *__restrict__ e,
+                                         const double *__restrict__ f, const double *__restrict__ b,
+                                         double *__restrict__ x, double *__restrict__ recw,
+                                         int32_t *status, int32_t *index, int64_t n, Lay lay,
+                                         int64_t s, const Scratch ws, int64_t w) {
 
   // ---- factor + forward substitution (rows 0..n-1) ----
   double cd[U], ce[U], cf[U], cb[U];   // current chunk: d_i, e_i, f_{i-1}, b_i
@@ -80,7 +78,7 @@ ntdm_seq_kernel(const double *__restrict__ d, const double *__restrict__ e,
         }
         rprev = dvd(1.0, mi);                           // _elim.py:108
         yprev = yi;
-        recw[ws(i, s)] = rprev;
+        recw[ws(i, w)] = rprev;
         x[lay(i, s)] = yi;
       }
     }
@@ -98,7 +96,7 @@ ntdm_seq_kernel(const double *__restrict__ d, const double *__restrict__ e,
       const int64_t i = top - u;
       if (i >= 0) {
         Y[u] = x[lay(i, s)];
-        R[u] = recw[ws(i, s)];
+        R[u] = recw[ws(i, w)];
         C[u] = ldg(f + lay(i, s));
       }
     }
@@ -120,22 +118,48 @@ ntdm_seq_kernel(const double *__restrict__ d, const double *__restrict__ e,
   set_status(status, index, s, BX_STATUS_OK, -1);
 }
 
+// flags == nullptr: one thread per system, scratch column = system.
+// flags != nullptr (re-solve of systems a partitioned kernel flagged): `slots`
+// threads walk the batch; flagged systems are solved with the thread's own
+// scratch column (Scratch{slots}); every other system gets status OK / -1.
+__device__ __forceinline__ bool flagged(const int32_t *flags, int64_t s, int fs) {
+  bool f = false;
+  for (int r = 0; r < fs; ++r) f |= flags[s * fs + r] != 0;
+  return f;
+}
+
+template <class Lay>
+__global__ void __launch_bounds__(kSeqThreads)
+ntdm_seq_kernel(const double *__restrict__ d, const double *__restrict__ e,
+                const double *__restrict__ f, const double *__restrict__ b,
+                double *__restrict__ x, double *__restrict__ recw, int32_t *status,
+                int32_t *index, int64_t batch, int64_t n, Lay lay, const int32_t *flags,
+                int64_t slots, int fs) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (!flags) {
+    if (t < batch) ntdm_one(d, e, f, b, x, recw, status, index, n, lay, t, Scratch{batch}, t);
+    return;
+  }
+  if (t >= slots) return;
+  for (int64_t s = t; s < batch; s += slots) {
+    if (flagged(flags, s, fs)) ntdm_one(d, e, f, b, x, recw, status, index, n, lay, s, Scratch{slots}, t);
+    else set_status(status, index, s, BX_STATUS_OK, -1);
+  }
+}
+
 // ----------------------------------------------------------------------------
 // NPDM (and MNPDM: kMod = true)
 // ----------------------------------------------------------------------------
 // Forward sweep state (row-aligned names of _elim.py): piv = mu (NPDM) or
 // rec = 1/mu (MNPDM); phi = U(i,i+1); psi = U(i,i+2) = sup2[i].
 template <bool kMod, class Lay>
-__global__ void __launch_bounds__(kSeqThreads)
-penta_seq_kernel(const double *__restrict__ c, const double *__restrict__ d,
-                 const double *__restrict__ e, const double *__restrict__ f,
-                 const double *__restrict__ g, const double *__restrict__ b,
-                 double *__restrict__ x, double *__restrict__ pivw, double *__restrict__ phiw,
-                 int32_t *status, int32_t *index, int64_t *nz_out, int64_t batch, int64_t n,
-                 Lay lay) {
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= batch) return;
-  const Scratch ws{batch};
+__device__ __forceinline__ void penta_one(const double *__restrict__ c, const double *__restrict__ d,
+                                          const double *__restrict__ e, const double *__restrict__ f,
+                                          const double *__restrict__ g, const double *__restrict__ b,
+                                          double *__restrict__ x, double *__restrict__ pivw,
+                                          double *__restrict__ phiw, int32_t *status,
+                                          int32_t *index, int64_t *nz_out, int64_t n, Lay lay,
+                                          int64_t s, const Scratch ws, int64_t w) {
 
   double cc[U], cd[U], ce[U], cf[U], cg[U], cb[U];
   double nc[U], nd[U], ne[U], nf[U], ng[U], nb[U];
@@ -204,8 +228,8 @@ penta_seq_kernel(const double *__restrict__ c, const double *__restrict__ d,
           return;
         }
         const double piv = kMod ? dvd(1.0, mi) : mi;             // rec (MNPDM) or mu
-        pivw[ws(i, s)] = piv;
-        phiw[ws(i, s)] = phi;
+        pivw[ws(i, w)] = piv;
+        phiw[ws(i, w)] = phi;
         x[lay(i, s)] = yi;
         p2 = p1; p1 = piv;
         ph2 = ph1; ph1 = phi;
@@ -235,8 +259,8 @@ penta_seq_kernel(const double *__restrict__ c, const double *__restrict__ d,
       const int64_t i = top - u;
       if (i >= 0) {
         Y[u] = x[lay(i, s)];
-        P[u] = pivw[ws(i, s)];
-        PH[u] = phiw[ws(i, s)];
+        P[u] = pivw[ws(i, w)];
+        PH[u] = phiw[ws(i, w)];
         PS[u] = ldg(g + lay(i, s));
       }
     }
@@ -257,6 +281,37 @@ penta_seq_kernel(const double *__restrict__ c, const double *__restrict__ d,
     for (int u = 0; u < U; ++u) { cy[u] = ny[u]; cp[u] = np_[u]; cph[u] = nph[u]; cps[u] = nps[u]; }
   }
   set_status(status, index, s, BX_STATUS_OK, -1);
+}
+
+template <bool kMod, class Lay>
+__global__ void __launch_bounds__(kSeqThreads)
+penta_seq_kernel(const double *__restrict__ c, const double *__restrict__ d,
+                 const double *__restrict__ e, const double *__restrict__ f,
+                 const double *__restrict__ g, const double *__restrict__ b,
+                 double *__restrict__ x, double *__restrict__ pivw, double *__restrict__ phiw,
+                 int32_t *status, int32_t *index, int64_t *nz_out, int64_t batch, int64_t n,
+                 Lay lay, const int32_t *flags, int64_t slots, int fs, const int32_t *nzpart) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (!flags) {
+    if (t < batch)
+      penta_one<kMod>(c, d, e, f, g, b, x, pivw, phiw, status, index, nz_out, n, lay, t,
+                      Scratch{batch}, t);
+    return;
+  }
+  if (t >= slots) return;
+  for (int64_t s = t; s < batch; s += slots) {
+    if (flagged(flags, s, fs)) {
+      penta_one<kMod>(c, d, e, f, g, b, x, pivw, phiw, status, index, nz_out, n, lay, s,
+                      Scratch{slots}, t);
+    } else {
+      set_status(status, index, s, BX_STATUS_OK, -1);
+      if (nz_out && nzpart) {
+        int64_t nz = 0;
+        for (int r = 0; r < fs; ++r) nz += nzpart[s * fs + r];
+        nz_out[s] = nz;
+      }
+    }
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -307,7 +362,7 @@ static void launch_ntdm(const double *d, const double *e, const double *f, const
                         double *x, double *ws, int32_t *st, int32_t *ix, int64_t batch,
                         int64_t n, Lay lay, cudaStream_t stream) {
   ntdm_seq_kernel<Lay><<<seq_grid(batch), kSeqThreads, 0, stream>>>(d, e, f, b, x, ws, st, ix,
-                                                                     batch, n, lay);
+                                                                     batch, n, lay, nullptr, 0, 1);
 }
 
 template <bool kMod, class Lay>
@@ -316,7 +371,7 @@ static void launch_penta(const double *c, const double *d, const double *e, cons
                          int32_t *ix, int64_t *nz, int64_t batch, int64_t n, Lay lay,
                          cudaStream_t stream) {
   penta_seq_kernel<kMod, Lay><<<seq_grid(batch), kSeqThreads, 0, stream>>>(
-      c, d, e, f, g, b, x, ws, ws + batch * n, st, ix, nz, batch, n, lay);
+      c, d, e, f, g, b, x, ws, ws + batch * n, st, ix, nz, batch, n, lay, nullptr, 0, 1, nullptr);
 }
 
 void ntdm_seq(const double *d, const double *e, const double *f, const double *b, double *x,
@@ -338,6 +393,41 @@ void penta_seq(bool mod, const double *c, const double *d, const double *e, cons
   } else {
     if (mod) launch_penta<true>(c, d, e, f, g, b, x, ws, st, ix, nz, batch, n, SystemMajor{ld}, stream);
     else launch_penta<false>(c, d, e, f, g, b, x, ws, st, ix, nz, batch, n, SystemMajor{ld}, stream);
+  }
+}
+
+// Re-solve, in the reference's operation order, the systems a partitioned
+// kernel flagged (flags[s] != 0), and write status / index of every system
+// (OK / -1 for the unflagged ones).  Scratch: fixup_scratch_doubles(...).
+constexpr int64_t kFixSlots = 128;
+size_t fixup_scratch_doubles(int kind, int64_t n) { return (size_t)(kind == 0 ? 1 : 2) * kFixSlots * n; }
+
+void direct_fixup(int kind, const double *c, const double *d, const double *e, const double *f,
+                  const double *g, const double *b, double *x, double *scratch,
+                  const int32_t *flags, int fs, const int32_t *nzpart, int32_t *st, int32_t *ix,
+                  int64_t *nz, int64_t batch, int64_t n, int64_t ld, int layout,
+                  cudaStream_t stream) {
+  const dim3 grid((unsigned)(kFixSlots / kSeqThreads));
+  if (kind == 0) {
+    if (layout == BX_LAYOUT_INTERLEAVED)
+      ntdm_seq_kernel<<<grid, kSeqThreads, 0, stream>>>(d, e, f, b, x, scratch, st, ix, batch, n,
+                                                       Interleaved{ld}, flags, kFixSlots, fs);
+    else
+      ntdm_seq_kernel<<<grid, kSeqThreads, 0, stream>>>(d, e, f, b, x, scratch, st, ix, batch, n,
+                                                       SystemMajor{ld}, flags, kFixSlots, fs);
+    return;
+  }
+  double *phiw = scratch + kFixSlots * n;
+  if (layout == BX_LAYOUT_INTERLEAVED) {
+    if (kind == 2)
+      penta_seq_kernel<true><<<grid, kSeqThreads, 0, stream>>>(c, d, e, f, g, b, x, scratch, phiw, st, ix, nz, batch, n, Interleaved{ld}, flags, kFixSlots, fs, nzpart);
+    else
+      penta_seq_kernel<false><<<grid, kSeqThreads, 0, stream>>>(c, d, e, f, g, b, x, scratch, phiw, st, ix, nz, batch, n, Interleaved{ld}, flags, kFixSlots, fs, nzpart);
+  } else {
+    if (kind == 2)
+      penta_seq_kernel<true><<<grid, kSeqThreads, 0, stream>>>(c, d, e, f, g, b, x, scratch, phiw, st, ix, nz, batch, n, SystemMajor{ld}, flags, kFixSlots, fs, nzpart);
+    else
+      penta_seq_kernel<false><<<grid, kSeqThreads, 0, stream>>>(c, d, e, f, g, b, x, scratch, phiw, st, ix, nz, batch, n, SystemMajor{ld}, flags, kFixSlots, fs, nzpart);
   }
 }
 

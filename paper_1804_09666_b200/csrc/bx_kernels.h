@@ -16,9 +16,24 @@ void penta_seq(bool mod, const double *c, const double *d, const double *e, cons
                const double *g, const double *b, double *x, double *ws, int32_t *st,
                int32_t *ix, int64_t *nz, int64_t batch, int64_t n, int64_t ld, int layout,
                cudaStream_t stream);
+size_t fixup_scratch_doubles(int kind, int64_t n);  // kind 0 NTDM, 1 NPDM, 2 MNPDM
+// flags[s*fs + r] != 0 for some r < fs: system s is re-solved in the
+// reference order; otherwise status OK / -1 and (nzpart) nz = sum of parts
+void direct_fixup(int kind, const double *c, const double *d, const double *e, const double *f,
+                  const double *g, const double *b, double *x, double *scratch,
+                  const int32_t *flags, int fs, const int32_t *nzpart, int32_t *st, int32_t *ix,
+                  int64_t *nz, int64_t batch, int64_t n, int64_t ld, int layout,
+                  cudaStream_t stream);
 void residual_inf(int bw, const double *c, const double *d, const double *e, const double *f,
                   const double *g, const double *x, const double *b, double *out, int64_t batch,
                   int64_t n, int64_t ld, int layout, cudaStream_t stream);
+
+// bx_direct_seg.cu (system-major, n <= 32768: the default partitioned path);
+// flags / nzpart: [batch][*csize] per segment
+bool seg_applicable(const double *const *ptrs, int nptr, int64_t n, int64_t ld, int layout);
+int seg_solve(int K, const double *c2, const double *c1, const double *e, const double *f1,
+              const double *f2, const double *b, double *x, int32_t *flags, int32_t *nzpart,
+              int64_t batch, int64_t n, int64_t ld, cudaStream_t stream, int *csize);
 
 // bx_direct_part.cu
 size_t part_workspace_bytes(int bandwidth, int64_t batch, int64_t n);

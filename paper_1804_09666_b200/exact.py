@@ -46,7 +46,7 @@ def _rhs(a, b):
         raise InvalidInput(f"rhs length {bb.shape[1]} does not match n={a.n}")
     if bb.shape[0] != a.batch:
         raise InvalidInput(f"rhs batch {bb.shape[0]} != {a.batch}")
-    return vector_to_layout(bb, a.n, a.layout, a.device)
+    return vector_to_layout(bb, a.n, a.layout, a.device, a.ld)
 
 
 def _solve(kind, a, b):

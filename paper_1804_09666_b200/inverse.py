@@ -72,13 +72,13 @@ def sip_hb_solve(a, b, cfg: SipConfig | None = None, mode: str = "dense", hb_ban
         raise DimensionMismatch(f"rhs length {bb.shape[1]}, expected {n}")
     if n > dense_cap:
         raise DenseCapExceeded(n, dense_cap)
-    b_store = vector_to_layout(bb, n, s.layout, dev)
+    b_store = vector_to_layout(bb, n, s.layout, dev, s.ld)
     tl = _tol(cfg, B, dev)
     x = s.new_vector()
     use_x0 = 0
     if cfg.initial_guess is not None:
         g, _ = _as_batch(cfg.initial_guess, "initial_guess")
-        x.copy_(vector_to_layout(np.broadcast_to(g, (B, n)), n, s.layout, dev))
+        x.copy_(vector_to_layout(np.broadcast_to(g, (B, n)), n, s.layout, dev, s.ld))
         use_x0 = 1
     best_x = s.new_vector()
     iters = torch.zeros(B, dtype=torch.int64, device=dev)
@@ -228,13 +228,13 @@ def _sip_hb_banded(s, b, cfg, hb_bandwidth, record_history, max_inv_iter, w_cap=
         raise InvalidInput("banded inversion needs bandwidth w >= 2")
     w = min(w, n - 1) if w else 0
     cap = int(w_cap) if w_cap else (w if w else min(n - 1, 256))
-    b_store = vector_to_layout(bb, n, s.layout, dev)
+    b_store = vector_to_layout(bb, n, s.layout, dev, s.ld)
     tl = _tol(cfg, B, dev)
     x = s.new_vector()
     use_x0 = 0
     if cfg.initial_guess is not None:
         g, _ = _as_batch(cfg.initial_guess, "initial_guess")
-        x.copy_(vector_to_layout(np.broadcast_to(g, (B, n)), n, s.layout, dev))
+        x.copy_(vector_to_layout(np.broadcast_to(g, (B, n)), n, s.layout, dev, s.ld))
         use_x0 = 1
     best_x = s.new_vector()
     iters = torch.zeros(B, dtype=torch.int64, device=dev)

@@ -179,7 +179,7 @@ def sip_solve(a, b, cfg: SipConfig | None = None, record_history: bool = False, 
         raise DimensionMismatch(f"rhs length {bb.shape[1]}, expected {n}")
     if bb.shape[0] != B:
         raise DimensionMismatch(f"rhs batch {bb.shape[0]} != {B}")
-    b_store = vector_to_layout(bb, n, s.layout, dev)
+    b_store = vector_to_layout(bb, n, s.layout, dev, s.ld)
     tol = torch.as_tensor(np.broadcast_to(np.asarray(cfg.tolerance, dtype=np.float64), (B,)).copy(),
                           device=dev)
     x = s.new_vector()
@@ -189,7 +189,7 @@ def sip_solve(a, b, cfg: SipConfig | None = None, record_history: bool = False, 
         if g.shape[1] != n:
             raise DimensionMismatch("initial guess has wrong length")
         x.copy_(vector_to_layout(np.broadcast_to(g, (B, n)) if not isinstance(g, torch.Tensor)
-                                 else g.expand(B, n), n, s.layout, dev))
+                                 else g.expand(B, n), n, s.layout, dev, s.ld))
         use_x0 = 1
     best_x = s.new_vector()
     iters = torch.zeros(B, dtype=torch.int64, device=dev)

@@ -41,11 +41,13 @@ st = torch.empty(batch, dtype=torch.int32, device=dev)
 ix = torch.empty(batch, dtype=torch.int32, device=dev)
 p = lambda t: t.data_ptr()  # noqa: E731
 s = torch.cuda.current_stream().cuda_stream
+nws = L.bx_workspace_bytes(0 if k == 1 else 1, batch, n, 1, 1)
+ws = torch.empty(nws, dtype=torch.uint8, device=dev)
 for _ in range(3):
     if k == 1:
-        rc = L.bx_ntdm_f64(*(p(a) for a in arrs), p(x), p(st), p(ix), batch, n, n, 1, 1, None, 0, s)
+        rc = L.bx_ntdm_f64(*(p(a) for a in arrs), p(x), p(st), p(ix), batch, n, n, 1, 1, p(ws), nws, s)
     else:
-        rc = L.bx_npdm_f64(*(p(a) for a in arrs), p(x), p(st), p(ix), batch, n, n, 1, 1, None, 0, s)
+        rc = L.bx_npdm_f64(*(p(a) for a in arrs), p(x), p(st), p(ix), batch, n, n, 1, 1, p(ws), nws, s)
     assert rc == 0, L.bx_last_error()
 torch.cuda.synchronize()
 buf = np.zeros((4096, 24), dtype=np.int64)
