@@ -192,6 +192,53 @@ def cpu_direct_rate(solver, arrs, sample):
 # ---------------------------------------------------------------------------
 # workloads
 # ---------------------------------------------------------------------------
+def static_config(args, world):
+    """The `config` object of the JSON line, identical for both arms (it depends
+    on the command line only, never on the data or the device)."""
+    w = args.workload
+    par = (f"grid split over {world} ranks, NCCL all-to-all between sweeps" if w == "adi"
+           else f"dp{world} (system-index sharding)")
+    if w in DIRECT:
+        solver, batch, n, cfg, sparse, desc = DIRECT[w]
+        sparse = solver == "mnpdm" and sparse and args.algo == "partitioned"
+        bpr = 40 if solver == "ntdm" or sparse else 56
+        gb = bpr * batch * n / 1e9
+        l2 = (f"inputs {gb:.2f} GB per step < 126 MB L2: L2 flushed (512 MB write) before every timed "
+              "step; value and ms_per_step from the per-step CUDA events (flushes excluded)"
+              if gb < 0.5 else f"inputs {gb:.2f} GB per step > 126 MB L2, no flush")
+        c = {"workload": desc, "solver": solver, "algo": args.algo, "batch_per_gpu": batch, "n": n,
+             "layout": f"{args.layout} row-aligned", "l2": l2}
+        if sparse:
+            c["outer"] = ("+-2 diagonals as per-system row lists, compacted once per matrix outside "
+                          "the timed region")
+    elif w == "sip":
+        cs = SIP_CFG
+        c = {"workload": (f"config 4 SIP: B={cs['batch']} five-point systems, {cs['n'] // cs['m']}x"
+                          f"{cs['m']} grid (N={cs['n']}, offsets +-1, +-{cs['m']}), Stone alpha="
+                          f"{cs['alpha']}, rel. tol 1e-8, <=500 iterations, seed {cs['cfg']}; a step = "
+                          "one full sip_solve (ILU(0) + all iterations)"),
+             "solver": "sip", "algo": "wavefront", "batch_per_gpu": cs["batch"], "n": cs["n"],
+             "m": cs["m"], "alpha": cs["alpha"],
+             "l2": "every iteration streams the 22 skewed planes (5.9 GB) > 126 MB L2"}
+    elif w in ("stdm", "spdm"):
+        bpr = 40 if w == "stdm" else 56
+        c = {"workload": (f"config 3 {w.upper()}: B=4096 non-dominant systems, N=2048, 8 decoupled "
+                          "zero pivots per system, seed 2"),
+             "solver": w, "batch_per_gpu": 4096, "n": 2048, "layout": "interleaved row-aligned",
+             "l2": f"inputs {bpr * 4096 * 2048 / 1e9:.2f} GB > 126 MB L2"}
+    elif w == "hb":
+        c = {"workload": ("config 4 HB: B=64 five-point systems, 64x32 grid (N=2048), alpha=0.5; step = "
+                          "sip_hb_solve (dense HB inverses of L and U on DMMA + SIP-HB iterations), seed 3"),
+             "solver": "sip_hb", "batch_per_gpu": 64, "n": 2048, "m": 32,
+             "l2": "X, X_next, P per factor: 3 x 2B x 33.5 MB = 12.9 GB"}
+    else:  # adi
+        c = {"workload": ("config 5 ADI: one step on a 8192x8192 grid (x-sweep of 8192 TD systems, "
+                          "transpose/all-to-all, y-sweep of 8192), seed 0"),
+             "solver": "adi (ntdm partitioned x2)", "grid": 8192, "l2": "5.4 GB per step > 126 MB L2"}
+    c["parallelism"] = par
+    return c
+
+
 class Direct:
     metric, unit, scaling = "systems_solved_per_s", "systems/s", "weak"
 
@@ -243,14 +290,6 @@ class Direct:
         # inputs that fit the 126 MB L2 (config 1: 42 MB) are flushed out of it
         # before every timed step (a 512 MB write, outside the step's events)
         self.flush_l2 = gb < 0.5
-        l2 = (f"inputs {gb:.2f} GB per step < 126 MB L2: L2 flushed (512 MB write) before every timed "
-              "step; value and ms_per_step from the per-step CUDA events (flushes excluded)"
-              if self.flush_l2 else f"inputs {gb:.2f} GB per step > 126 MB L2, no flush")
-        self.config = {"workload": desc, "solver": solver, "algo": args.algo, "batch_per_gpu": batch,
-                       "n": n, "layout": f"{args.layout} row-aligned", "l2": l2}
-        if self.sparse:
-            self.config["outer"] = (f"+-2 diagonals as per-system row lists ({self.outer_k} rows per "
-                                    "system), compacted once per matrix outside the timed region")
 
     def solve(self, ins, out):
         import torch
@@ -378,12 +417,6 @@ class Sip:
         self.res = torch.empty(self.batch, **f64)
         self.status = torch.empty(self.batch, dtype=torch.int32, device=dev)
         self.ws = workspace(_lib.lib().bx_sip_workspace_bytes(self.batch, self.n, m), dev)
-        desc = (f"config 4 SIP: B={self.batch} five-point systems, {self.n // m}x{m} grid "
-                f"(N={self.n}, offsets +-1, +-{m}), Stone alpha={self.alpha}, rel. tol 1e-8, "
-                f"<=500 iterations, seed {c['cfg']}; a step = one full sip_solve (ILU(0) + all iterations)")
-        self.config = {"workload": desc, "solver": "sip", "algo": "wavefront",
-                       "batch_per_gpu": self.batch, "n": self.n, "m": m, "alpha": self.alpha,
-                       "l2": "every iteration streams the 22 skewed planes (5.9 GB) > 126 MB L2"}
 
     def solve(self, ins, x):
         import torch
@@ -471,11 +504,6 @@ class Exact:
         self.ws = workspace(_lib.lib().bx_workspace_bytes(_lib.SOLVER[kind], self.batch, self.n, 0, 0), dev)
         self.units = self.batch
         self.bytes_per_row = 40 if kind == "stdm" else 56
-        self.config = {"workload": f"config 3 {kind.upper()}: B=4096 non-dominant systems, N=2048, "
-                                   f"8 decoupled zero pivots per system, seed 2",
-                       "solver": kind, "batch_per_gpu": self.batch, "n": self.n,
-                       "layout": "interleaved row-aligned",
-                       "l2": f"inputs {self.bytes_per_row * self.batch * self.n / 1e9:.2f} GB > 126 MB L2"}
 
     def solve(self, ins, x):
         import torch
@@ -553,11 +581,6 @@ class Hb:
         self.inv_it = torch.empty(2 * batch, dtype=torch.int64, device=dev)
         self.st = torch.empty(batch, dtype=torch.int32, device=dev)
         self.ws = workspace(_lib.lib().bx_hb_workspace_bytes(batch, n), dev)
-        self.config = {"workload": f"config 4 HB: B={batch} five-point systems, {n // m}x{m} grid "
-                                   f"(N={n}), alpha={alpha}; step = sip_hb_solve (dense HB inverses "
-                                   f"of L and U on DMMA + SIP-HB iterations), seed 3",
-                       "solver": "sip_hb", "batch_per_gpu": batch, "n": n, "m": m,
-                       "l2": "X, X_next, P per factor: 3 x 2B x 33.5 MB = 12.9 GB"}
 
     def solve(self, ins, x):
         import torch
@@ -668,10 +691,6 @@ class Adi:
         self.stepper = ADIStep(self.dx[:3], self.dy, group=dist.group.WORLD if world > 1 else None)
         self.units = 2 * n // world          # systems solved per rank per step
         self.x = self.stepper.U
-        self.config = {"workload": f"config 5 ADI: one step on a {n}x{n} grid (x-sweep of {n} TD "
-                                   f"systems, transpose/all-to-all, y-sweep of {n}), seed 0",
-                       "solver": "adi (ntdm partitioned x2)", "grid": n,
-                       "l2": "5.4 GB per step > 126 MB L2"}
 
     def step(self):
         self.stepper(self.dx[3])
@@ -730,10 +749,28 @@ WORKLOADS = sorted(list(DIRECT) + ["sip", "stdm", "spdm", "hb", "adi"])
 
 
 def cpu_reference_arm(args):
-    """--impl reference: the CPU restatement on the host cores, rank 0 only."""
+    """--impl reference: the CPU restatement on the host cores, rank 0 only
+    (under a launcher the ranks form a gloo group; the others only join it)."""
     world, rank, _ = dist_env()
-    if rank != 0:
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        try:
+            if rank == 0:
+                _cpu_reference_run(args, world)
+            dist.barrier()
+        finally:
+            dist.destroy_process_group()
         return
+    _cpu_reference_run(args, world)
+
+
+def _cpu_reference_run(args, world):
+    # all host threads (a launcher exports OMP_NUM_THREADS=1 to every rank;
+    # only rank 0 works here, before the OpenMP runtime is loaded)
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
+    from oracle import cport
+    cport.set_threads(len(os.sched_getaffinity(0)))
     from oracle import cport
     times = []
     if args.workload not in DIRECT and args.workload != "sip":
@@ -776,7 +813,7 @@ def cpu_reference_arm(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "sample": samp},
+            "config": static_config(args, world),
             "cpu_baseline": {"value": value, "unit": unit, "cores": thr, "kind": "port",
                              "sample": f"{samp}, C restatement (oracle/c/bx_oracle.c), OpenMP {thr} threads"},
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -875,10 +912,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = wl.cpu_baseline()
     if rank == 0:
-        cfg = dict(wl.config)
-        cfg["parallelism"] = (f"grid split over {world} ranks, NCCL all-to-all between sweeps"
-                              if args.workload == "adi" else f"dp{world} (system-index sharding)")
-        cfg["parity_gate"] = f"sampled systems vs C restatement, max rel err {gate_err:.2e}"
+        cfg = static_config(args, world)
         line = {
             "metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
@@ -893,6 +927,7 @@ def run_ours(args):
                     "pcie_frac": (wl.h2d * e2e_steps / e2e_elapsed / 1e9 / pcie) if pcie else None},
             "gpu_launches": args.steps * wl.launches_per_step,
             "clocks": clocks,
+            "parity_gate": f"sampled systems vs C restatement, max rel err {gate_err:.2e}",
         }
         print(json.dumps(line))
     if world > 1:
@@ -915,12 +950,32 @@ def main():
                     help="system chunks of the overlapped host pipeline (e2e leg)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return launch_ranks(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+                         "(torchrun --nproc-per-node N bench.py --gpus N, or plain bench.py --gpus N)")
     if args.layout is None:
         args.layout = "system" if args.algo == "partitioned" else "interleaved"
     if args.impl == "reference":
         cpu_reference_arm(args)
     else:
         run_ours(args)
+
+
+def launch_ranks(args):
+    """`python bench.py --gpus N` without a launcher: start N ranks on this node
+    (torch.distributed.run on 127.0.0.1, a free port), forward their output,
+    exit with the first non-zero rank status."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    raise SystemExit(subprocess.call(cmd))
 
 
 if __name__ == "__main__":

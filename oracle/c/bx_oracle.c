@@ -35,6 +35,15 @@ int ox_threads(void) {
 #endif
 }
 
+/* the host threads of the timed sections (a launcher may export OMP_NUM_THREADS=1) */
+void ox_set_threads(int n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 static void nan_fill(double *x, int64_t n) {
   for (int64_t i = 0; i < n; ++i) x[i] = NAN;
 }

@@ -24,6 +24,11 @@ def build():
     return LIB
 
 
+def set_threads(n):
+    """OpenMP threads of the C restatement's timed sections."""
+    lib().ox_set_threads(int(n))
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -32,6 +37,7 @@ def lib():
         p = C.c_void_p
         i64 = C.c_int64
         _lib.ox_threads.restype = C.c_int
+        _lib.ox_set_threads.argtypes = [C.c_int]
         _lib.ox_ntdm.argtypes = [p] * 7 + [i64] * 3
         _lib.ox_penta.argtypes = [C.c_int] + [p] * 10 + [i64] * 3
         _lib.ox_sip.argtypes = [p] * 14 + [i64] * 4 + [C.c_double, i64]

@@ -266,3 +266,125 @@ def test_mnpdm_sparse_outer_edge_cases(cuda):
     rep = solve_mnpdm(PentaMatrix.from_diagonals(*q[:5]).sparse_outer(), q[5], algo="partitioned")
     xm, _, _, _ = D.mnpdm(*q)
     assert rel_err(host(rep.x), xm).max() <= REL_TOL
+
+
+# ---- zero-pivot contract of the partitioned path --------
+# A pivot of the partitioned elimination that is zero or not finite flags the
+# system, and direct_fixup re-solves it in the reference's operation order: x,
+# status and index are then the reference's (bit for bit).  Only a pivot that
+# is exactly zero in the reference's order but not in the partitioned order
+# (cancellation inside a chunk) goes unreported by the partitioned path --
+# that system is nonsingular, and the partitioned path returns its solution;
+# the sequential (default) algorithm raises ZeroPivot(i) exactly as the
+# reference ("zero pivots").
+
+def _zero_diag_at_chunk_starts(k, n, rows, seed):
+    if k == 1:
+        a = [x.copy() for x in W.td_dominant(3, n, seed=seed)]
+        for r in rows:
+            a[1][1, r] = 0.0
+        return a
+    a = [x.copy() for x in W.pd_dominant(3, n, seed=seed)]
+    for r in rows:
+        a[2][1, r] = 0.0
+    return a
+
+
+@pytest.mark.parametrize("k", [1, 2])
+@pytest.mark.parametrize("rows", [(1024,), (16, 1024, 2048, 3008), (3072,)])
+def test_partitioned_zero_diagonal_at_chunk_start_is_resolved(cuda, k, rows):
+    """Zero main-diagonal entries at chunk-start rows: the reference's pivot
+    there is nonzero (no ZeroPivot); the chunk-local pivot is zero, the system
+    is flagged and re-solved in the reference order -> bit-identical x."""
+    n = 4096
+    a = _zero_diag_at_chunk_starts(k, n, rows, seed=41)
+    if k == 1:
+        x_ref, st_ref, _ = D.ntdm(*a)
+        rep = solve_ntdm(TriMatrix.from_diagonals(*a[:3], layout="system"), a[3], algo="partitioned")
+    else:
+        x_ref, st_ref, _ = D.npdm(*a)
+        rep = solve_npdm(PentaMatrix.from_diagonals(*a[:5], layout="system"), a[5], algo="partitioned")
+    assert (st_ref == 0).all()
+    assert (host(rep.status) == 0).all()
+    assert np.array_equal(host(rep.x)[1], x_ref[1])          # the re-solved system: reference bits
+    assert rel_err(host(rep.x)[[0, 2]], x_ref[[0, 2]]).max() <= REL_TOL
+
+
+def _cancel_pivot(a, k, i):
+    """Make the reference's pivot at row i exactly zero by cancellation
+    (nonzero terms), as tri_factor_recip / penta_factor compute it."""
+    if k == 1:
+        d, e, f = a[0][0], a[1][0], a[2][0]
+        rec = 1.0 / e[0]
+        for r in range(1, i):
+            rec = 1.0 / (e[r] - (d[r - 1] * rec) * f[r - 1])
+        li = d[i - 1] * rec
+        e[i] = li * f[i - 1]                    # mi = e - li f = 0 exactly
+        return
+    mu, l1, l2, phi, psi, st, _ = D.penta_factor(*(x[:1] for x in a[:5]))
+    c, d = a[0][0], a[1][0]
+    li2 = c[i - 2] / mu[0, i - 2]
+    li1 = (d[i - 1] - li2 * phi[0, i - 2]) / mu[0, i - 1]
+    A, B = li2 * psi[0, i - 2], li1 * phi[0, i - 1]
+    e = A + B
+    for _ in range(64):                         # fl(e - A) == B  =>  mi = 0 exactly
+        if (e - A) - B == 0.0:
+            break
+        e = np.nextafter(e, np.inf if (e - A) < B else -np.inf)
+    a[2][0, i] = e
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_cancellation_zero_pivot_inside_a_chunk(cuda, k):
+    """Reference ZeroPivot(3001) by cancellation (row 3001 is inside a chunk).
+    Sequential: ZeroPivot(3001) exactly like the reference.  Partitioned: the
+    chunk-local pivot is not zero, so the system is not flagged -- the
+    documented contract difference (the partitioned path reports only the
+    zero / non-finite pivots of its own elimination order; a leading minor
+    that is singular in the reference's rounding is not detected, and no
+    accuracy is promised for such a matrix: use the sequential algorithm)."""
+    n, i = 4096, 3001
+    if k == 1:
+        a = [x.copy() for x in W.td_dominant(2, n, seed=43)]
+        _cancel_pivot(a, 1, i)
+        _, st_ref, ix_ref = D.ntdm(*a)
+        T = TriMatrix.from_diagonals(*a[:3], layout="system")
+        seq = solve_ntdm(T, a[3], residual=False)
+        par = solve_ntdm(T, a[3], algo="partitioned")
+    else:
+        a = [x.copy() for x in W.pd_dominant(2, n, seed=43)]
+        _cancel_pivot(a, 2, i)
+        _, st_ref, ix_ref = D.npdm(*a)
+        P = PentaMatrix.from_diagonals(*a[:5], layout="system")
+        seq = solve_npdm(P, a[5], residual=False)
+        par = solve_npdm(P, a[5], algo="partitioned")
+    assert st_ref[0] == 1 and ix_ref[0] == i and st_ref[1] == 0
+    assert host(seq.status).tolist() == st_ref.tolist() and host(seq.index)[0] == i
+    assert host(par.status).tolist() == [0, 0]
+    x_ok = D.ntdm(*(v[1:] for v in a))[0] if k == 1 else D.npdm(*(v[1:] for v in a))[0]
+    assert rel_err(host(par.x)[1:], x_ok).max() <= REL_TOL  # the untouched system is unaffected
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_partitioned_nonfinite_entry_matches_reference(cuda, k):
+    """An inf on the diagonal: the reference never raises for it (only exact
+    zeros do); the partitioned path flags the system and the re-solve gives
+    the reference's bits (NaN/inf propagation included)."""
+    n = 2048
+    if k == 1:
+        a = [x.copy() for x in W.td_dominant(2, n, seed=44)]
+        a[1][0, 700] = np.inf
+        x_ref, st_ref, _ = D.ntdm(*a)
+        rep = solve_ntdm(TriMatrix.from_diagonals(*a[:3], layout="system"), a[3], algo="partitioned",
+                         residual=False)
+    else:
+        a = [x.copy() for x in W.pd_dominant(2, n, seed=44)]
+        a[2][0, 700] = np.inf
+        x_ref, st_ref, _ = D.npdm(*a)
+        rep = solve_npdm(PentaMatrix.from_diagonals(*a[:5], layout="system"), a[5], algo="partitioned",
+                         residual=False)
+    assert host(rep.status).tolist() == st_ref.tolist()
+    x = host(rep.x)
+    assert np.array_equal(np.isnan(x[0]), np.isnan(x_ref[0]))
+    fin = np.isfinite(x_ref[0])
+    assert np.array_equal(x[0][fin], x_ref[0][fin])
