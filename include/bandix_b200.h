@@ -226,7 +226,7 @@ int bx_rcond_band_f64(int32_t bandwidth, const double *sub2, const double *sub1,
  * row-aligned array in the call's layout and may be NULL: factors mu (U
  * main), l1 (L(i,i-1)), l2 (L(i,i-m)), phi (U(i,i+1)), psi (U(i,i+m)); defect
  * diagonals at offsets -m, -1, 0, +1, +m, -(m-1), +(m-1) (the last two are
- * zero for m = 2).  Synchronises the stream (factor export). */
+ * zero for m = 2).  Stream-ordered; no allocation. */
 int bx_ilu0_f64(const double *subm, const double *sub1, const double *main, const double *sup1,
                 const double *supm, double *mu, double *l1, double *l2, double *phi, double *psi,
                 double *k_subm, double *k_sub1, double *k_main, double *k_sup1, double *k_supm,

@@ -263,15 +263,23 @@ sip_seq_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
   set_status(status, index, s, st, -1);
 }
 
-// copy the factor / defect planes out in the caller's layout (row-aligned)
+// copy the factor / defect planes out in the caller's layout (row-aligned);
+// the 12 output pointers travel by value as a kernel parameter (no device
+// staging buffer, no copies, no stream synchronisation)
+struct ExportArgs {
+  double *outs[12];
+  int which[12];
+};
+
 template <class Lay>
-__global__ void export_planes_kernel(Planes P, double *const *outs, const int *which, int count,
-                                     int64_t batch, int64_t n, Lay lay) {
+__global__ void export_planes_kernel(Planes P, const ExportArgs args, int64_t batch, int64_t n,
+                                     Lay lay) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= batch * n) return;
   const int64_t i = idx / batch, s = idx % batch;
-  for (int c = 0; c < count; ++c)
-    if (outs[c]) outs[c][lay(i, s)] = P(which[c])[i * batch + s];
+#pragma unroll
+  for (int c = 0; c < 12; ++c)
+    if (args.outs[c]) args.outs[c][lay(i, s)] = P(args.which[c])[i * batch + s];
 }
 
 }  // namespace sip
@@ -313,30 +321,21 @@ int sip_seq(const double *a2, const double *a1, const double *e, const double *c
 // K_{+1}, K_{+m}, K_{-(m-1)}, K_{+(m-1)}) -> caller arrays (NULL skips)
 int sip_export(double *ws, int64_t batch, int64_t n, double *const *outs12, int64_t ld,
                int layout, cudaStream_t stream) {
-  double **d_outs = nullptr;
-  int *d_which = nullptr;
   static const int which[12] = {sip::MU, sip::L1, sip::L2, sip::PHI, sip::PSI, sip::KM,
                                 sip::K1N, sip::K0, sip::K1P, sip::KP, sip::KQN, sip::KQP};
-  // tiny argument block through the stream (no allocation on the host path
-  // besides this 144-byte staging buffer)
-  if (cudaMallocAsync((void **)&d_outs, sizeof(double *) * 12 + sizeof(int) * 12, stream) !=
-      cudaSuccess)
-    return BX_ERR_CUDA;
-  d_which = reinterpret_cast<int *>(d_outs + 12);
-  cudaMemcpyAsync(d_outs, outs12, sizeof(double *) * 12, cudaMemcpyHostToDevice, stream);
-  cudaMemcpyAsync(d_which, which, sizeof(int) * 12, cudaMemcpyHostToDevice, stream);
+  sip::ExportArgs args;
+  for (int c = 0; c < 12; ++c) {
+    args.outs[c] = outs12[c];
+    args.which[c] = which[c];
+  }
   sip::Planes P{ws, batch, n};
   const int64_t tot = batch * n;
   const dim3 grid((unsigned)((tot + 255) / 256));
   if (layout == BX_LAYOUT_INTERLEAVED)
-    sip::export_planes_kernel<<<grid, 256, 0, stream>>>(P, d_outs, d_which, 12, batch, n,
-                                                        Interleaved{ld});
+    sip::export_planes_kernel<<<grid, 256, 0, stream>>>(P, args, batch, n, Interleaved{ld});
   else
-    sip::export_planes_kernel<<<grid, 256, 0, stream>>>(P, d_outs, d_which, 12, batch, n,
-                                                        SystemMajor{ld});
-  cudaStreamSynchronize(stream);  // outs12 is a host array owned by the caller
-  cudaFreeAsync(d_outs, stream);
-  return BX_OK;
+    sip::export_planes_kernel<<<grid, 256, 0, stream>>>(P, args, batch, n, SystemMajor{ld});
+  return bxh::check_launch("bx_ilu0_f64 export");
 }
 
 }  // namespace bx

@@ -20,12 +20,40 @@ import numpy as np
 import torch
 
 from . import _lib
-from .core import BandFactors, SolveReport, _as_batch, _Timer, ptr, stream_handle, \
+from .core import BandFactors, OpCounter, SolveReport, _as_batch, _Timer, ptr, stream_handle, \
     vector_from_layout, vector_to_layout, workspace
 from .errors import (DenseCapExceeded, DimensionMismatch, InvalidInput, MaxIterationsExceeded,
                      STATUS_MAX_ITER, STATUS_OK, STATUS_STAGNATED, Stagnated, exception_for)
-from .iterative import SipConfig, _as_stencil, _sip_ops
+from .iterative import SipConfig, _as_stencil
 
+
+
+def _sweep_ops(n):
+    """_sweep_apply: 5N-6 muls, 5N-6 adds (iterative.py:203-214)."""
+    return 5 * n - 6
+
+
+def _banded_apply_muls(n, w):
+    """BandedApproxInverse.matvec: sum_{j<=w} (N - j) muls, that minus N adds
+    (inverse.py:48-61); w may be a per-system tensor."""
+    return (w + 1) * n - w * (w + 1) // 2
+
+
+def _sip_hb_ops(n, k, mode="dense", w_lower=None, w_upper=None):
+    """SolveReport.ops of sip_hb_solve: the CounterBox tally of its loop body
+    (inverse.py:284-290) per iteration -- defect sweep, vec add, the two
+    inverse applies, A sweep, vec sub.  Dense applies count N^2 muls and
+    N(N-1) adds each (inverse.py:198-202): 4N^2 + 20N - 24 per iteration;
+    banded applies count their band (inverse.py:48-61).  Pinned to the
+    reference's own counts (tests/golden: hb_ops, sip_*_32_ops)."""
+    sw = _sweep_ops(n)
+    if mode == "dense":
+        ml = mu = n * n
+    else:
+        ml, mu = _banded_apply_muls(n, w_lower), _banded_apply_muls(n, w_upper)
+    muls = (2 * sw + ml + mu) * k
+    adds = (2 * sw + n + (ml - n) + (mu - n)) * k
+    return OpCounter(adds=adds, subs=n * k, muls=muls, divs=0)
 
 def _tol(cfg, B, dev):
     return torch.as_tensor(np.broadcast_to(np.asarray(cfg.tolerance, dtype=np.float64), (B,)).copy(),
@@ -110,9 +138,9 @@ def sip_hb_solve(a, b, cfg: SipConfig | None = None, mode: str = "dense", hb_ban
             if record_history else ()
         x1 = xv[0].cpu().numpy()
         x1.setflags(write=False)
-        return SolveReport(x=x1, iterations=k, residual_inf=float(res[0]), ops=_sip_ops(n, k),
+        return SolveReport(x=x1, iterations=k, residual_inf=float(res[0]), ops=_sip_hb_ops(n, k),
                            wall_seconds=timer.seconds(), history=history)
-    rep = SolveReport(x=xv, iterations=iters, residual_inf=res, ops=_sip_ops(n, iters),
+    rep = SolveReport(x=xv, iterations=iters, residual_inf=res, ops=_sip_hb_ops(n, iters),
                       wall_seconds=timer.seconds(), history=hist if record_history else (),
                       status=st, index=ix, x_storage=x)
     rep.best_x = vector_from_layout(best_x, s.layout)
@@ -269,9 +297,11 @@ def _sip_hb_banded(s, b, cfg, hb_bandwidth, record_history, max_inv_iter, w_cap=
             if record_history else ()
         x1 = xv[0].cpu().numpy()
         x1.setflags(write=False)
-        return SolveReport(x=x1, iterations=k, residual_inf=float(res[0]), ops=_sip_ops(n, k),
+        return SolveReport(x=x1, iterations=k, residual_inf=float(res[0]),
+                           ops=_sip_hb_ops(n, k, "banded", int(wu[0]), int(wu[B])),
                            wall_seconds=timer.seconds(), history=history)
-    rep = SolveReport(x=xv, iterations=iters, residual_inf=res, ops=_sip_ops(n, iters),
+    rep = SolveReport(x=xv, iterations=iters, residual_inf=res,
+                      ops=_sip_hb_ops(n, iters, "banded", wu[:B], wu[B:]),
                       wall_seconds=timer.seconds(), history=hist if record_history else (),
                       status=st, index=ix, x_storage=x)
     rep.best_x = vector_from_layout(best_x, s.layout)

@@ -178,15 +178,17 @@ def golden_inverse():
     bsz, n = p[5].shape
     xs = np.zeros((bsz, n)); its = np.zeros(bsz, np.int64); res = np.zeros(bsz)
     li = np.zeros(bsz, np.int64); ui = np.zeros(bsz, np.int64)
+    ops = np.zeros((bsz, 4), np.int64)   # SolveReport.ops (adds, subs, muls, divs)
     for s in range(bsz):
         a = core.PentaMatrix.from_diagonals(*[d[s] for d in p[:5]])
         rep = inverse.sip_hb_solve(a, p[5][s], iterative.SipConfig(tolerance=float(tol[s]),
                                                                    max_iterations=500))
         xs[s] = rep.x; its[s] = rep.iterations; res[s] = rep.residual_inf
+        ops[s] = (rep.ops.adds, rep.ops.subs, rep.ops.muls, rep.ops.divs)
         f = iterative.ilu0_penta(a)
         li[s] = inverse.hb_invert_dense(inverse.dense_lower_factor(f), float(tol[s])).iterations
         ui[s] = inverse.hb_invert_dense(inverse.dense_upper_factor(f), float(tol[s])).iterations
-    out.update(hb_tol=tol, hb_x=xs, hb_k=its, hb_res=res, hb_linv_iters=li, hb_uinv_iters=ui)
+    out.update(hb_tol=tol, hb_x=xs, hb_k=its, hb_res=res, hb_linv_iters=li, hb_uinv_iters=ui, hb_ops=ops)
     # [[1,0],[3,1]] inverts in one iteration
     r = inverse.hb_invert_dense(np.array([[1.0, 0.0], [3.0, 1.0]]))
     out.update(hb_spec_iters=np.int64(r.iterations), hb_spec_inv=np.asarray(r.inverse))
@@ -231,13 +233,15 @@ def golden_hbband():
                         dd[j, :len(v)] = v
                     out.update({key + "_x": dd, key + "_it": np.int64(it), key + "_res": np.float64(r),
                                 key + "_hist": np.asarray(h, dtype=np.float64), key + "_st": np.int32(st)})
-        for w in (3, 6, 12, None):
+        for w in (3, 6, 12, 32, None):
             key = f"sip_{s}_{w if w else 'auto'}"
             cfg = iterative.SipConfig(tolerance=float(tol[s]), max_iterations=60)
             try:
                 rep = inverse.sip_hb_solve(a, p[5][s], cfg, mode="banded", hb_bandwidth=w)
                 out.update({key + "_x": np.asarray(rep.x), key + "_k": np.int64(rep.iterations),
-                            key + "_res": np.float64(rep.residual_inf), key + "_st": np.int32(0)})
+                            key + "_res": np.float64(rep.residual_inf), key + "_st": np.int32(0),
+                            key + "_ops": np.array([rep.ops.adds, rep.ops.subs, rep.ops.muls,
+                                                    rep.ops.divs], np.int64)})
             except MaxIterationsExceeded as e:
                 out.update({key + "_x": np.asarray(e.best), key + "_k": np.int64(e.iterations),
                             key + "_res": np.float64(e.residual_inf), key + "_st": np.int32(3)})

@@ -95,3 +95,21 @@ def test_sip_hb_banded_auto_width(cuda, n, bsz):
     assert np.array_equal(host(rep.hb_bandwidth), o["inv_w"])
     assert np.array_equal(host(rep.x), o["x"])
     assert (host(rep.residual_inf) < tol).all()
+
+
+def test_sip_hb_banded_width32_converges_golden(cuda, golden):
+    """hb_bandwidth=32: the reference converges (k = 6); same iterate bits,
+    count, residual and op tally (band applies, inverse.py:48-61)."""
+    g = golden("hbband")
+    p = [g[f"hbb_{k}"] for k in HBB]
+    A = PentaMatrix.from_diagonals(*p[:5])
+    rep = sip_hb_solve(A, p[5], SipConfig(tolerance=g["hbb_tol"], max_iterations=60), mode="banded",
+                       hb_bandwidth=32)
+    for s in range(2):
+        key = f"sip_{s}_32"
+        assert int(rep.status[s]) == 0 == int(g[key + "_st"])
+        assert np.array_equal(host(rep.x[s]), g[key + "_x"])
+        assert int(rep.iterations[s]) == g[key + "_k"]
+        assert float(rep.residual_inf[s]) == float(g[key + "_res"])
+        assert [int(rep.ops.adds[s]), int(rep.ops.subs[s]), int(rep.ops.muls[s]),
+                int(rep.ops.divs)] == g[key + "_ops"].tolist()

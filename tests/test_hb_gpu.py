@@ -33,6 +33,9 @@ def test_sip_hb_golden(cuda, golden, layout):
     x = host(rep.x)
     assert np.abs(x - g["hb_x"]).max() <= 1e-11 * np.abs(g["hb_x"]).max()
     assert np.all(host(rep.residual_inf) < g["hb_tol"])
+    # ops: the reference's dense-apply tally, 4N^2 + 20N - 24 per iteration
+    ops = np.stack([host(v) for v in (rep.ops.adds, rep.ops.subs, rep.ops.muls)], axis=1)
+    assert np.array_equal(ops, g["hb_ops"][:, :3]) and (g["hb_ops"][:, 3] == 0).all()
 
 
 @pytest.mark.parametrize("m,rows,alpha", [(2, 128, 0.0), (16, 24, 0.5), (32, 64, 0.5)])
