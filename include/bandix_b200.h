@@ -155,6 +155,41 @@ int bx_pd2td_ntdm_f64(const double *sub2, const double *sub1, const double *main
                       int64_t ld, int32_t layout, void *workspace, size_t workspace_bytes,
                       void *stream);
 
+/* ---- band building blocks (reference operation order, bit-identical) ------ */
+/* y = A x (rhs == NULL) or y = rhs - A x for a band of bandwidth 1 (subm/supm
+ * unused, may be NULL) or a five-point band with outer offset m (m = 2: the
+ * pentadiagonal).  Replaces penta_matvec / tri_matvec / residual
+ * (core.py:243-314; the float branch's array-sweep order main, sub1, sup1,
+ * sub2, sup2).  One thread per element. */
+int bx_band_matvec_f64(int32_t bandwidth, int64_t m, const double *subm, const double *sub1,
+                       const double *main, const double *sup1, const double *supm, const double *x,
+                       const double *rhs, double *y, int64_t batch, int64_t n, int64_t ld,
+                       int32_t layout, void *stream);
+
+/* lu_penta (direct.py:42-63 -> penta_factor, _elim.py:30-62): banded Doolittle
+ * factors, row-aligned in the call's layout: mu (U main), l1 = L(i,i-1),
+ * l2 = L(i,i-2), phi = U(i,i+1), psi = U(i,i+2); structurally absent slots
+ * are 0.  status ZERO_PIVOT with index = the first zero pivot (ZeroPivot(i);
+ * the factors are then not usable).  n >= 3. */
+int bx_lu_penta_f64(const double *sub2, const double *sub1, const double *main, const double *sup1,
+                    const double *sup2, double *mu, double *l1, double *l2, double *phi, double *psi,
+                    int32_t *status, int32_t *index, int64_t batch, int64_t n, int64_t ld,
+                    int32_t layout, void *stream);
+
+/* forward_sub (iterative.py:127-137 -> penta_forward): L y = rhs with unit
+ * diagonal, l1 at offset -1 and lm at offset -m (m = 2: lu_penta / ilu0
+ * factors of the pentadiagonal; m >= 3: grid ILU(0) factors).  y may alias
+ * rhs. */
+int bx_forward_sub_f64(int64_t m, const double *l1, const double *lm, const double *rhs, double *y,
+                       int64_t batch, int64_t n, int64_t ld, int32_t layout, void *stream);
+
+/* backward_sub (iterative.py:140-149 -> penta_backward): U x = y with pivots
+ * mu, phi at +1, psi at +m.  A zero pivot anywhere gives status ZERO_PIVOT
+ * with index = the first one (checked before any division) and x = NaN. */
+int bx_backward_sub_f64(int64_t m, const double *mu, const double *phi, const double *psi,
+                        const double *y, double *x, int32_t *status, int32_t *index, int64_t batch,
+                        int64_t n, int64_t ld, int32_t layout, void *stream);
+
 /* ||b - A x||_inf per system, the report residual of _finish_report
  * (direct.py:66-70 -> core.py:243-321), in the reference's row-fused
  * operation order.  bandwidth 1 (tridiagonal: sub2/sup2 ignored, may be

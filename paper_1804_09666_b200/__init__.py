@@ -9,14 +9,17 @@ by hand-written sm_100a CUDA kernels behind a C ABI
 fallback: without the built library or a GPU every solver raises.
 """
 
-from .core import BandFactors, OpCounter, OuterSparsePenta, PentaMatrix, SolveReport, TriMatrix  # noqa: F401
-from .direct import pd_to_td, solve_mnpdm, solve_npdm, solve_ntdm, solve_pd2td_ntdm  # noqa: F401
+from .core import (BandFactors, CounterBox, OpCounter, OuterSparsePenta, PentaMatrix,  # noqa: F401
+                   SolveReport, TriMatrix, inf_norm, matvec, outer_nonzero_count, penta_matvec,
+                   residual, tri_matvec)
+from .direct import (lu_penta, pd_to_td, solve_mnpdm, solve_npdm, solve_ntdm,  # noqa: F401
+                     solve_pd2td_ntdm)
 from .exact import (BandDeterminant, ExactSolveResult, exact_det_band, exact_solve_spdm,  # noqa: F401
                     exact_solve_stdm, rcond_band)
 from .inverse import (BandedApproxInverse, InversionReport, hb_invert_banded,  # noqa: F401
                       hb_invert_factors, sip_hb_solve)
-from .iterative import (DefectMatrix, SipConfig, StencilMatrix, defect_matrix,  # noqa: F401
-                        ilu0_penta, sip_solve)
+from .iterative import (DefectMatrix, SipConfig, StencilMatrix, backward_sub,  # noqa: F401
+                        backward_sub_batched, defect_matrix, forward_sub, ilu0_penta, sip_solve)
 from .errors import (BandixError, DenseCapExceeded, DimensionMismatch, Diverged,  # noqa: F401
                      InvalidInput, InvalidSpec, MaxIterationsExceeded, NonAffine,
                      ReductionPivotZero, SingularMatrix, SolverError, Stagnated, ZeroDiagonal,

@@ -35,6 +35,10 @@ _SIGS = {
     "bx_npdm_f64": ([_p] * 9 + [_i64, _i64, _i64, _i32, _i32, _p, _sz, _p], C.c_int),
     "bx_mnpdm_f64": ([_p] * 10 + [_i64, _i64, _i64, _i32, _i32, _p, _sz, _p], C.c_int),
     "bx_residual_inf_f64": ([_i32] + [_p] * 8 + [_i64, _i64, _i64, _i32, _p], C.c_int),
+    "bx_band_matvec_f64": ([_i32, _i64] + [_p] * 8 + [_i64, _i64, _i64, _i32, _p], C.c_int),
+    "bx_lu_penta_f64": ([_p] * 12 + [_i64, _i64, _i64, _i32, _p], C.c_int),
+    "bx_forward_sub_f64": ([_i64] + [_p] * 4 + [_i64, _i64, _i64, _i32, _p], C.c_int),
+    "bx_backward_sub_f64": ([_i64] + [_p] * 7 + [_i64, _i64, _i64, _i32, _p], C.c_int),
     "bx_pd2td_f64": ([_p] * 13 + [_i64, _i64, _i64, _i64, _i32, _p], C.c_int),
     "bx_pd2td_ntdm_f64": ([_p] * 10 + [_i64, _i64, _i64, _i32, _p, _sz, _p], C.c_int),
     "bx_stdm_f64": ([_p] * 8 + [_i64, _i64, _i64, _i32, _p, _sz, _p], C.c_int),

@@ -405,7 +405,10 @@ class SolveReport:
 
 @dataclass(frozen=True)
 class BandFactors:
-    """Banded (I)LU factors, row-aligned device storage (core.py:208-223)."""
+    """Banded (I)LU factors, row-aligned device storage (core.py:208-223):
+    row i of l_sub1 / l_sub2 holds L(i, i-1) / L(i, i-m), of u_main /
+    u_sup1 / u_sup2 U(i, i) / U(i, i+1) / U(i, i+m).  Producers attach
+    ``layout``, ``batch``, ``single``, ``status`` and ``index``."""
 
     n: int
     l_sub1: Any
@@ -415,6 +418,114 @@ class BandFactors:
     u_sup2: Any
     m: int = 2
     exact: bool = False
+
+    def ref(self):
+        """(l_sub1, l_sub2, u_main, u_sup1, u_sup2) as (B, len) views in the
+        reference's unpadded lengths n-1, n-m, n, n-1, n-m."""
+        lay, n, m = getattr(self, "layout", _lib.LAYOUT_INTERLEAVED), self.n, self.m
+        return (unpack_rows(self.l_sub1, 1, n - 1, lay), unpack_rows(self.l_sub2, m, n - m, lay),
+                unpack_rows(self.u_main, 0, n, lay), unpack_rows(self.u_sup1, 0, n - 1, lay),
+                unpack_rows(self.u_sup2, 0, n - m, lay))
+
+
+class CounterBox:
+    """Mutable holder threading an OpCounter through a call (core.py:105-114)."""
+
+    __slots__ = ("counter",)
+
+    def __init__(self):
+        self.counter = OpCounter()
+
+    def add(self, adds=0, subs=0, muls=0, divs=0):
+        self.counter = self.counter.plus(adds, subs, muls, divs)
+
+
+# ---- band helpers of the reference's core.py (243-334) ------------------------
+def _vec_in(a, x, what="vector"):
+    """x for band container a -> (storage in a's layout / ld, single flag)."""
+    xb, single = _as_batch(x, what)
+    if xb.shape[1] != a.n:
+        raise DimensionMismatch(f"{what} has length {xb.shape[1]}, expected {a.n}")
+    if xb.shape[0] != a.batch:
+        raise DimensionMismatch(f"{what} batch {xb.shape[0]} != {a.batch}")
+    return vector_to_layout(xb, a.n, a.layout, a.device, a.ld), single
+
+
+def _vec_out(a, store, single):
+    v = vector_from_layout(store, a.layout)
+    if single:
+        out = v[0].detach().cpu().numpy()
+        out.setflags(write=False)
+        return out
+    return v
+
+
+def _band_matvec(a, x, b=None):
+    """bx_band_matvec_f64: A x, or b - A x when b is given (device storage)."""
+    xs, single = _vec_in(a, x)
+    bs = _vec_in(a, b, "rhs")[0] if b is not None else None
+    y = a.new_vector()
+    diags = a.rowaligned()
+    if len(diags) == 3:
+        bw, m, (c, d, e, f, g) = 1, 2, (None,) + tuple(diags) + (None,)
+    else:
+        bw, m, (c, d, e, f, g) = 2, getattr(a, "m", 2), diags
+    _lib.call("bx_band_matvec_f64", bw, m, ptr(c), ptr(d), ptr(e), ptr(f), ptr(g), ptr(xs), ptr(bs),
+              ptr(y), a.batch, a.n, a.ld, a.layout, stream_handle())
+    return _vec_out(a, y, single and a.single)
+
+
+def penta_matvec(a, x, counter=None):
+    """A @ x for pentadiagonal A (core.py:243-268): 5N-6 muls, 4N-6 adds;
+    the reference's float order (main, sub1, sup1, sub2, sup2), bit-identical."""
+    if counter is not None:
+        counter.add(muls=5 * a.n - 6, adds=4 * a.n - 6)
+    return _band_matvec(a, x)
+
+
+def tri_matvec(t, x, counter=None):
+    """T @ x for tridiagonal T (core.py:271-289): 3N-2 muls, 2N-2 adds."""
+    if counter is not None:
+        counter.add(muls=3 * t.n - 2, adds=2 * t.n - 2)
+    return _band_matvec(t, x)
+
+
+def matvec(a, x, counter=None):
+    """core.py:292-295."""
+    return penta_matvec(a, x, counter) if isinstance(a, PentaMatrix) else tri_matvec(a, x, counter)
+
+
+def residual(a, x, b, counter=None):
+    """b - A @ x, entrywise (core.py:307-316): matvec ops + N subs."""
+    if counter is not None:
+        if isinstance(a, PentaMatrix):
+            counter.add(muls=5 * a.n - 6, adds=4 * a.n - 6)
+        else:
+            counter.add(muls=3 * a.n - 2, adds=2 * a.n - 2)
+        counter.add(subs=a.n)
+    return _band_matvec(a, x, b)
+
+
+def inf_norm(v):
+    """Maximum absolute entry; the empty vector has norm 0 (core.py:298-304).
+    A 2-D batch gives one norm per row (NaN propagates, as numpy.max)."""
+    if isinstance(v, torch.Tensor):
+        if v.numel() == 0:
+            return 0 if v.dim() < 2 else torch.zeros(v.shape[0], dtype=torch.float64, device=v.device)
+        return torch.amax(v.abs(), dim=-1) if v.dim() == 2 else float(torch.amax(v.abs()))
+    a = np.asarray(v, dtype=np.float64)
+    if a.size == 0:
+        return 0
+    return np.max(np.abs(a), axis=-1) if a.ndim == 2 else float(np.max(np.abs(a)))
+
+
+def outer_nonzero_count(a):
+    """Rows with a structurally nonzero sub2 entry plus rows with a nonzero
+    sup2 entry (core.py:319-334): exact zero test on the stored data.  An int
+    for a single system, a (B,) tensor for a batch."""
+    sub2, _, _, _, sup2 = a.diagonals()
+    k = torch.count_nonzero(sub2, dim=1) + torch.count_nonzero(sup2, dim=1)
+    return int(k[0]) if a.single else k
 
 
 _WS_CACHE: dict = {}

@@ -191,6 +191,60 @@ int bx_pd2td_ntdm_f64(const double *sub2, const double *sub1, const double *main
   return bxh::check_launch("bx_pd2td_ntdm_f64");
 }
 
+/* ---- band building blocks (bx_band_ops.cu) ------------------------------ */
+int bx_band_matvec_f64(int32_t bandwidth, int64_t m, const double *subm, const double *sub1,
+                       const double *main, const double *sup1, const double *supm, const double *x,
+                       const double *rhs, double *y, int64_t batch, int64_t n, int64_t ld,
+                       int32_t layout, void *stream) {
+  BX_REQUIRE(bandwidth == 1 || bandwidth == 2, "bx_band_matvec_f64: bandwidth must be 1 or 2");
+  BX_REQUIRE(bandwidth == 1 || m >= 2, "bx_band_matvec_f64: outer stride m must be >= 2");
+  int rc = check_common("bx_band_matvec_f64", batch, n, bandwidth == 1 ? 2 : m + 1, ld, layout);
+  if (rc) return rc;
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(sub1 && main && sup1 && x && y, "bx_band_matvec_f64: null pointer");
+  BX_REQUIRE(bandwidth == 1 || (subm && supm), "bx_band_matvec_f64: null outer diagonal");
+  bx::band_matvec(bandwidth, m, subm, sub1, main, sup1, supm, x, rhs, y, batch, n, ld, layout,
+                  (cudaStream_t)stream);
+  return bxh::check_launch("bx_band_matvec_f64");
+}
+
+int bx_lu_penta_f64(const double *sub2, const double *sub1, const double *main, const double *sup1,
+                    const double *sup2, double *mu, double *l1, double *l2, double *phi, double *psi,
+                    int32_t *status, int32_t *index, int64_t batch, int64_t n, int64_t ld,
+                    int32_t layout, void *stream) {
+  int rc = check_common("bx_lu_penta_f64", batch, n, 3, ld, layout);
+  if (rc) return rc;
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(sub2 && sub1 && main && sup1 && sup2 && mu && l1 && l2 && phi && psi,
+             "bx_lu_penta_f64: null pointer");
+  bx::lu_penta(sub2, sub1, main, sup1, sup2, mu, l1, l2, phi, psi, status, index, batch, n, ld,
+               layout, (cudaStream_t)stream);
+  return bxh::check_launch("bx_lu_penta_f64");
+}
+
+int bx_forward_sub_f64(int64_t m, const double *l1, const double *lm, const double *rhs, double *y,
+                       int64_t batch, int64_t n, int64_t ld, int32_t layout, void *stream) {
+  BX_REQUIRE(m >= 2, "bx_forward_sub_f64: outer stride m must be >= 2");
+  int rc = check_common("bx_forward_sub_f64", batch, n, 2, ld, layout);
+  if (rc) return rc;
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(l1 && lm && rhs && y, "bx_forward_sub_f64: null pointer");
+  bx::forward_sub(m, l1, lm, rhs, y, batch, n, ld, layout, (cudaStream_t)stream);
+  return bxh::check_launch("bx_forward_sub_f64");
+}
+
+int bx_backward_sub_f64(int64_t m, const double *mu, const double *phi, const double *psi,
+                        const double *y, double *x, int32_t *status, int32_t *index, int64_t batch,
+                        int64_t n, int64_t ld, int32_t layout, void *stream) {
+  BX_REQUIRE(m >= 2, "bx_backward_sub_f64: outer stride m must be >= 2");
+  int rc = check_common("bx_backward_sub_f64", batch, n, 2, ld, layout);
+  if (rc) return rc;
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(mu && phi && psi && y && x, "bx_backward_sub_f64: null pointer");
+  bx::backward_sub(m, mu, phi, psi, y, x, status, index, batch, n, ld, layout, (cudaStream_t)stream);
+  return bxh::check_launch("bx_backward_sub_f64");
+}
+
 int bx_residual_inf_f64(int32_t bandwidth, const double *sub2, const double *sub1,
                         const double *main, const double *sup1, const double *sup2,
                         const double *x, const double *rhs, double *res_inf, int64_t batch,

@@ -35,6 +35,19 @@ int seg_solve(int K, const double *c2, const double *c1, const double *e, const 
               const double *f2, const double *b, double *x, int32_t *flags, int32_t *nzpart,
               int64_t batch, int64_t n, int64_t ld, cudaStream_t stream, int *csize);
 
+// bx_band_ops.cu (reference order, bit-exact building blocks)
+void band_matvec(int bw, int64_t m, const double *c, const double *d, const double *e,
+                 const double *f, const double *g, const double *x, const double *b, double *y,
+                 int64_t batch, int64_t n, int64_t ld, int layout, cudaStream_t stream);
+void lu_penta(const double *c, const double *d, const double *e, const double *f, const double *g,
+              double *mu, double *l1, double *l2, double *phi, double *psi, int32_t *st,
+              int32_t *ix, int64_t batch, int64_t n, int64_t ld, int layout, cudaStream_t stream);
+void forward_sub(int64_t m, const double *l1, const double *lm, const double *b, double *y,
+                 int64_t batch, int64_t n, int64_t ld, int layout, cudaStream_t stream);
+void backward_sub(int64_t m, const double *mu, const double *phi, const double *psi, const double *y,
+                  double *x, int32_t *st, int32_t *ix, int64_t batch, int64_t n, int64_t ld,
+                  int layout, cudaStream_t stream);
+
 // bx_direct_part.cu
 size_t part_workspace_bytes(int bandwidth, int64_t batch, int64_t n);
 int outer_compact(const double *sub2, const double *sup2, int32_t *count, int32_t *rows,

@@ -20,8 +20,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .core import (OpCounter, OuterSparsePenta, PentaMatrix, SolveReport, TriMatrix, _Timer, ptr,
-                   stream_handle, vector_from_layout, workspace)
+from .core import (BandFactors, OpCounter, OuterSparsePenta, PentaMatrix, SolveReport, TriMatrix,
+                   _Timer, ptr, stream_handle, vector_from_layout, workspace)
 from .errors import DimensionMismatch, STATUS_OK, exception_for
 from collections import namedtuple
 
@@ -42,6 +42,30 @@ def _coerce(a, kind):
     if kind == "penta" and not isinstance(a, PentaMatrix):
         raise TypeError("expected a bandix_b200 PentaMatrix")
     return a
+
+
+def lu_penta(a: PentaMatrix, counter=None) -> BandFactors:
+    """Doolittle factorisation restricted to the band (direct.py:42-63): 10N-17
+    ops, the reference's operation order (penta_factor, _elim.py:30-62) -- the
+    factors are bit-identical.  Factor once, then ``forward_sub`` /
+    ``backward_sub`` (iterative.py) for every right-hand side.  One system
+    raises ZeroPivot(i); a batch carries ``status`` / ``index``."""
+    a = _coerce(a, "penta")
+    outs = [a.new_vector() for _ in range(5)]   # mu, l1, l2, phi, psi
+    status = torch.empty(a.batch, dtype=torch.int32, device=a.device)
+    index = torch.empty(a.batch, dtype=torch.int32, device=a.device)
+    _lib.call("bx_lu_penta_f64", *(ptr(v) for v in a.rowaligned()), *(ptr(v) for v in outs),
+              ptr(status), ptr(index), a.batch, a.n, a.ld, a.layout, stream_handle())
+    if counter is not None:
+        counter.add(muls=4 * a.n - 7, subs=4 * a.n - 7, divs=2 * a.n - 3)
+    if a.single and int(status[0]) != STATUS_OK:
+        raise exception_for(int(status[0]), int(index[0]))
+    mu, l1, l2, phi, psi = outs
+    f = BandFactors(a.n, l1, l2, mu, phi, psi, m=2)
+    for k, v in (("status", status), ("index", index), ("layout", a.layout), ("single", a.single),
+                 ("batch", a.batch), ("ld", a.ld), ("device", a.device)):
+        object.__setattr__(f, k, v)
+    return f
 
 
 def ops_ntdm(n):

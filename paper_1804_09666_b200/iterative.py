@@ -142,6 +142,68 @@ def ilu0_penta(a, counter=None, *, alpha=0.0):
     return f
 
 
+def _factor_vec(f: BandFactors, v, what):
+    vb, single = _as_batch(v, what)
+    if vb.shape[1] != f.n:
+        raise DimensionMismatch(f"{what} length {vb.shape[1]}, expected {f.n}")
+    ld = getattr(f, "ld", None) or f.u_main.stride(0)
+    return vector_to_layout(vb, f.n, f.layout, f.u_main.device, ld), single, ld
+
+
+def _factor_out(f: BandFactors, store, single):
+    v = vector_from_layout(store, f.layout)
+    if single and getattr(f, "single", single):
+        out = v[0].detach().cpu().numpy()
+        out.setflags(write=False)
+        return out
+    return v
+
+
+def forward_sub(factors: BandFactors, rhs, counter=None):
+    """One sweep of L y = rhs, unit lower with two subdiagonals (iterative.py:
+    127-137 -> penta_forward): 4N-6 ops, the reference's operation order
+    (bit-identical).  Factors from lu_penta or ilu0_penta (outer offset m)."""
+    f = factors
+    b, single, ld = _factor_vec(f, rhs, "rhs")
+    y = torch.empty_like(b)
+    B = b.shape[1] if f.layout == _lib.LAYOUT_INTERLEAVED else b.shape[0]
+    _lib.call("bx_forward_sub_f64", f.m, ptr(f.l_sub1), ptr(f.l_sub2), ptr(b), ptr(y), B, f.n, ld,
+              f.layout, stream_handle())
+    if counter is not None:
+        counter.add(muls=2 * f.n - 3, subs=2 * f.n - 3)
+    return _factor_out(f, y, single)
+
+
+def backward_sub(factors: BandFactors, y, counter=None):
+    """One sweep of U x = y with the pivots plus two superdiagonals
+    (iterative.py:140-149 -> penta_backward): 5N-6 ops, bit-identical; a zero
+    pivot raises ZeroPivot(first) for one system (batches: ``.status`` /
+    ``.index`` on the returned tensor's owner -- see backward_sub_batched)."""
+    x, status, index, single = _backward(factors, y, counter)
+    if single and int(status[0]) != STATUS_OK:
+        raise exception_for(int(status[0]), int(index[0]))
+    return _factor_out(factors, x, single)
+
+
+def backward_sub_batched(factors: BandFactors, y, counter=None):
+    """backward_sub for a batch: (x, status, index) device tensors."""
+    x, status, index, _ = _backward(factors, y, counter)
+    return vector_from_layout(x, factors.layout), status, index
+
+
+def _backward(f, y, counter):
+    ys, single, ld = _factor_vec(f, y, "rhs")
+    x = torch.empty_like(ys)
+    B = ys.shape[1] if f.layout == _lib.LAYOUT_INTERLEAVED else ys.shape[0]
+    status = torch.empty(B, dtype=torch.int32, device=ys.device)
+    index = torch.empty(B, dtype=torch.int32, device=ys.device)
+    _lib.call("bx_backward_sub_f64", f.m, ptr(f.u_main), ptr(f.u_sup1), ptr(f.u_sup2), ptr(ys), ptr(x),
+              ptr(status), ptr(index), B, f.n, ld, f.layout, stream_handle())
+    if counter is not None:
+        counter.add(muls=2 * f.n - 3, subs=2 * f.n - 3, divs=f.n)
+    return x, status, index, single
+
+
 def defect_matrix(factors: BandFactors, a, counter=None) -> DefectMatrix:
     """K = L U - A (iterative.py:186-200): offsets -m, -1, 0, +1, +m and, for
     m >= 3, the dropped fill at +-(m-1)."""
