@@ -308,6 +308,24 @@ int bx_hb_invert_f64(const double *subm, const double *sub1, const double *main,
                      double alpha, int64_t max_iter, int64_t ld, int32_t layout, void *workspace,
                      size_t workspace_bytes, void *stream);
 
+/* hb_invert_dense(m, tol, max_iter) (inverse.py:94-119) on the caller's dense
+ * square matrices: m[s] at m + s*m_stride, row i at +i*ldm (row-major).
+ * X0 = diag(1/m_ii); P = M X, r = ||I - P||_inf, stop when r < tol[s], else
+ * X <- X (2I - P); both products are DMMA GEMMs (agreement with the
+ * reference's BLAS products to rounding; counts and statuses are the
+ * reference's).  x (may be NULL): the returned inverse (the converged iterate;
+ * after max_iter the once-more-updated one, as MaxIterationsExceeded.best).
+ * status: OK, ZERO_DIAG(index = first zero m_ii), MAX_ITER.  iterations,
+ * residual (the last r), history ([batch][max_iter+1], NaN padded) may be
+ * NULL.  Host-driven loop: synchronises the stream.  Workspace:
+ * bx_hb_invert_dense_workspace_bytes(batch, n). */
+size_t bx_hb_invert_dense_workspace_bytes(int64_t batch, int64_t n);
+int bx_hb_invert_dense_f64(const double *m, int64_t n, int64_t ldm, int64_t m_stride, int64_t batch,
+                           const double *tol, int64_t max_iter, double *x, int64_t ldx,
+                           int64_t x_stride, int64_t *iterations, double *residual,
+                           double *history, int32_t *status, int32_t *index, void *workspace,
+                           size_t workspace_bytes, void *stream);
+
 /* SIP with the substitutions replaced by the HB inverses (sip_hb_solve,
  * mode="dense", inverse.py:205-302): same contract as bx_sip_f64 plus the
  * inversion counters.  The inversion tolerance is tol[s], as in the reference

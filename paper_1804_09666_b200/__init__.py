@@ -16,8 +16,9 @@ from .direct import (lu_penta, pd_to_td, solve_mnpdm, solve_npdm, solve_ntdm,  #
                      solve_pd2td_ntdm)
 from .exact import (BandDeterminant, ExactSolveResult, exact_det_band, exact_solve_spdm,  # noqa: F401
                     exact_solve_stdm, rcond_band)
-from .inverse import (BandedApproxInverse, InversionReport, hb_invert_banded,  # noqa: F401
-                      hb_invert_factors, sip_hb_solve)
+from .inverse import (BandedApproxInverse, InversionReport, dense_lower_factor,  # noqa: F401
+                      dense_upper_factor, hb_invert_banded, hb_invert_dense, hb_invert_factors,
+                      sip_hb_solve)
 from .iterative import (DefectMatrix, SipConfig, StencilMatrix, backward_sub,  # noqa: F401
                         backward_sub_batched, defect_matrix, forward_sub, ilu0_penta, sip_solve)
 from .errors import (BandixError, DenseCapExceeded, DimensionMismatch, Diverged,  # noqa: F401

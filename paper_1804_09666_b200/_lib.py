@@ -55,6 +55,9 @@ _SIGS = {
     "bx_mnpdm_sparse_f64": ([_p] * 3 + [_i64] + [_p] * 8 + [_i64, _i64, _i64, _i32, _p], C.c_int),
     "bx_transpose_f64": ([_p, _p] + [_i64] * 7 + [_p], C.c_int),
     "bx_hb_workspace_bytes": ([_i64, _i64], _sz),
+    "bx_hb_invert_dense_workspace_bytes": ([_i64, _i64], _sz),
+    "bx_hb_invert_dense_f64": ([_p, _i64, _i64, _i64, _i64, _p, _i64, _p, _i64, _i64] + [_p] * 6
+                               + [_sz, _p], C.c_int),
     "bx_hb_invert_f64": ([_p] * 12 + [_i64, _i64, _i64, C.c_double, _i64, _i64, _i32, _p, _sz, _p],
                          C.c_int),
     "bx_sip_hb_f64": ([_p] * 17 + [_i64, _i64, _i64, C.c_double, _i64, _i64, _i32, _i64, _i32, _p,

@@ -245,6 +245,29 @@ int bx_backward_sub_f64(int64_t m, const double *mu, const double *phi, const do
   return bxh::check_launch("bx_backward_sub_f64");
 }
 
+size_t bx_hb_invert_dense_workspace_bytes(int64_t batch, int64_t n) {
+  return bx::hb_dense_invert_workspace_bytes(batch, n);
+}
+
+int bx_hb_invert_dense_f64(const double *m, int64_t n, int64_t ldm, int64_t m_stride, int64_t batch,
+                           const double *tol, int64_t max_iter, double *x, int64_t ldx,
+                           int64_t x_stride, int64_t *iterations, double *residual,
+                           double *history, int32_t *status, int32_t *index, void *workspace,
+                           size_t workspace_bytes, void *stream) {
+  BX_REQUIRE(n >= 1 && batch >= 0 && max_iter >= 0, "bx_hb_invert_dense_f64: bad sizes");
+  BX_REQUIRE(ldm >= n && ldx >= n && m_stride >= n * ldm && (x == nullptr || x_stride >= n * ldx),
+             "bx_hb_invert_dense_f64: bad leading dimensions");
+  if (batch == 0) return BX_OK;
+  BX_REQUIRE(m && tol, "bx_hb_invert_dense_f64: null pointer");
+  const size_t need = bx::hb_dense_invert_workspace_bytes(batch, n);
+  if (workspace_bytes < need || !workspace) {
+    set_error("bx_hb_invert_dense_f64: workspace %zu bytes < required %zu", workspace_bytes, need);
+    return BX_ERR_WORKSPACE;
+  }
+  return bx::hb_dense_invert(m, n, ldm, m_stride, batch, tol, max_iter, x, ldx, x_stride, iterations,
+                             residual, history, status, index, workspace, (cudaStream_t)stream);
+}
+
 int bx_residual_inf_f64(int32_t bandwidth, const double *sub2, const double *sub1,
                         const double *main, const double *sup1, const double *sup2,
                         const double *x, const double *rhs, double *res_inf, int64_t batch,

@@ -136,6 +136,13 @@ int sip_hb(const double *a2, const double *a1, const double *e, const double *c1
            int64_t max_inv_iter, int use_x0, int64_t ld, int layout, void *workspace,
            cudaStream_t st, bool invert_only, double *xl, double *xu);
 
+// bx_hb_dense.cu (hb_invert_dense on a caller's dense matrices)
+size_t hb_dense_invert_workspace_bytes(int64_t batch, int64_t n);
+int hb_dense_invert(const double *M, int64_t n, int64_t ldm, int64_t mstride, int64_t batch,
+                    const double *tol, int64_t max_iter, double *X, int64_t ldx, int64_t xstride,
+                    int64_t *iterations, double *residual, double *history, int32_t *status,
+                    int32_t *index, void *ws, cudaStream_t st);
+
 // bx_hb_band.cu (banded HB, inverse.py:122-195)
 size_t hb_band_bytes(int64_t batch, int64_t n, int64_t cap);
 int hb_band_invert_round(const double *fac, double *X, double *Xn, double *P, double *Best,

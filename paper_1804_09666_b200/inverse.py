@@ -20,10 +20,12 @@ import numpy as np
 import torch
 
 from . import _lib
-from .core import BandFactors, OpCounter, SolveReport, _as_batch, _Timer, ptr, stream_handle, \
+from .core import BandFactors, OpCounter, SolveReport, _as_batch, _Timer, default_device, ptr, \
+    stream_handle, \
     vector_from_layout, vector_to_layout, workspace
 from .errors import (DenseCapExceeded, DimensionMismatch, InvalidInput, MaxIterationsExceeded,
-                     STATUS_MAX_ITER, STATUS_OK, STATUS_STAGNATED, Stagnated, exception_for)
+                     STATUS_MAX_ITER, STATUS_OK, STATUS_STAGNATED, STATUS_ZERO_DIAG, Stagnated,
+                     ZeroDiagonal, exception_for)
 from .iterative import SipConfig, _as_stencil
 
 
@@ -191,6 +193,77 @@ class InversionReport:
     residual_history: Any = ()
     status: Any = None
     index: Any = None
+
+
+def hb_invert_dense(m, tol=1e-12, max_iter: int = 200, *, record_history: bool = True):
+    """Quadratically convergent inversion X <- X (2I - M X) of dense square
+    matrices (inverse.py:94-119): X0 = diag(1/m_ii), stop when ||I - M X||_inf
+    < tol.  One (n, n) matrix: an InversionReport with a numpy inverse, and
+    ZeroDiagonal / MaxIterationsExceeded(best, residual, max_iter) exactly as
+    the reference.  A batch (B, n, n): device tensors and per-system status.
+    Both products per iteration are DMMA GEMMs (bx_hb_invert_dense_f64)."""
+    single = False
+    if isinstance(m, torch.Tensor):
+        t = m.detach().to(torch.float64)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(m, dtype=np.float64)))
+    if t.dim() == 2:
+        t, single = t.unsqueeze(0), True
+    if t.dim() != 3 or t.shape[1] != t.shape[2]:
+        raise InvalidInput("dense inversion needs a square matrix")
+    dev = t.device if t.is_cuda else default_device()
+    t = t.to(dev).contiguous()
+    B, n = t.shape[0], t.shape[1]
+    tl = torch.as_tensor(np.broadcast_to(np.asarray(tol, dtype=np.float64), (B,)).copy(), device=dev)
+    x = torch.empty((B, n, n), dtype=torch.float64, device=dev)
+    it = torch.zeros(B, dtype=torch.int64, device=dev)
+    rs = torch.empty(B, dtype=torch.float64, device=dev)
+    hist = torch.empty((B, max_iter + 1), dtype=torch.float64, device=dev) if record_history else None
+    st = torch.empty(B, dtype=torch.int32, device=dev)
+    ix = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = workspace(_lib.lib().bx_hb_invert_dense_workspace_bytes(B, n), dev)
+    _lib.call("bx_hb_invert_dense_f64", ptr(t), n, n, n * n, B, ptr(tl), int(max_iter), ptr(x), n,
+              n * n, ptr(it), ptr(rs), ptr(hist), ptr(st), ptr(ix), ptr(ws), ws.numel(),
+              stream_handle())
+    if single:
+        code, k, r = int(st[0]), int(it[0]), float(rs[0])
+        x1 = x[0].cpu().numpy()
+        if code == STATUS_ZERO_DIAG:
+            raise ZeroDiagonal(int(ix[0]))
+        if code == STATUS_MAX_ITER:
+            raise MaxIterationsExceeded(x1, r, int(max_iter))
+        h = tuple(float(v) for v in hist[0, :k + 1].cpu().numpy()) if record_history else ()
+        return InversionReport(x1, k, r, h)
+    return InversionReport(x, it, rs, hist if record_history else (), status=st, index=ix)
+
+
+def dense_lower_factor(factors: BandFactors):
+    """Unit-lower L as dense (B, n, n) device tensors -- or one (n, n) numpy
+    array for a single system (inverse.py:72-78); outer offset factors.m."""
+    return _dense_factor(factors, lower=True)
+
+
+def dense_upper_factor(factors: BandFactors):
+    """U as dense (B, n, n) / (n, n) (inverse.py:81-87)."""
+    return _dense_factor(factors, lower=False)
+
+
+def _dense_factor(f: BandFactors, lower: bool):
+    l1, lm, mu, p1, pm = f.ref()
+    B, n, m = l1.shape[0], f.n, f.m
+    out = torch.zeros((B, n, n), dtype=torch.float64, device=mu.device)
+    i = torch.arange(n, device=mu.device)
+    if lower:
+        out[:, i, i] = 1.0
+        out[:, i[1:], i[:-1]] = l1
+        out[:, i[m:], i[:n - m]] = lm
+    else:
+        out[:, i, i] = mu
+        out[:, i[:-1], i[1:]] = p1
+        out[:, i[:n - m], i[m:]] = pm
+    if getattr(f, "single", False):
+        return out[0].cpu().numpy()
+    return out
 
 
 def hb_invert_banded(factors: BandFactors, side: str, w: int = 2, tol=1e-12,

@@ -5,6 +5,7 @@ tolerance, not bits."""
 
 import numpy as np
 import pytest
+import torch
 
 from oracle import inverse as H
 from oracle import iterative as I
@@ -93,3 +94,62 @@ def test_hb_inverses_ignore_stale_workspace(cuda):
     xl, xu = host(xl), host(xu)
     assert np.all(np.isfinite(xl)) and np.all(np.isfinite(xu))
     assert np.all(np.triu(xl, 1) == 0.0) and np.all(np.tril(xu, -1) == 0.0)
+
+
+# ---- hb_invert_dense on a caller's dense matrices (inverse.py:94-119) -------
+def test_hb_invert_dense_spec_case(cuda, golden):
+    """[[1, 0], [3, 1]] inverts in one iteration (reference run)."""
+    from paper_1804_09666_b200 import hb_invert_dense
+    g = golden("inverse")
+    r = hb_invert_dense(np.array([[1.0, 0.0], [3.0, 1.0]]))
+    assert r.iterations == int(g["hb_spec_iters"])
+    assert np.array_equal(r.inverse, g["hb_spec_inv"])
+    assert r.residual_inf < 1e-12 and len(r.residual_history) == r.iterations + 1
+
+
+def test_hb_invert_dense_ilu_factors_match_reference_counts(cuda, golden):
+    """dense_lower_factor / dense_upper_factor of the ILU(0) factors, then
+    hb_invert_dense: the reference's iteration counts (golden), inverses within
+    rounding of the numpy restatement."""
+    from oracle import inverse as OI
+    from paper_1804_09666_b200 import (dense_lower_factor, dense_upper_factor, hb_invert_dense,
+                                       ilu0_penta)
+    g = golden("inverse")
+    a = [g[f"hb_{k}"] for k in PD]
+    for s in range(a[0].shape[0]):
+        A = PentaMatrix.from_diagonals(*(v[s] for v in a[:5]))
+        f = ilu0_penta(A)
+        for dense, key in ((dense_lower_factor, "hb_linv_iters"), (dense_upper_factor, "hb_uinv_iters")):
+            M = dense(f)
+            r = hb_invert_dense(M, float(g["hb_tol"][s]))
+            assert r.iterations == int(g[key][s])
+            rx, rit, _, _, _ = OI.hb_invert_dense(M, float(g["hb_tol"][s]))
+            assert r.iterations == rit
+            assert np.abs(r.inverse - rx).max() <= 1e-12 * np.abs(rx).max()
+
+
+def test_hb_invert_dense_batched_general_and_errors(cuda):
+    from oracle import inverse as OI
+    from paper_1804_09666_b200 import MaxIterationsExceeded, ZeroDiagonal, hb_invert_dense
+    rng = np.random.default_rng(4)
+    B, n = 5, 150            # not a multiple of the 64-wide tiles; non-triangular
+    M = np.eye(n)[None] + 0.3 / n * rng.uniform(-1, 1, (B, n, n))
+    M[:, np.arange(n), np.arange(n)] += rng.uniform(0.5, 2.0, (B, n))
+    r = hb_invert_dense(torch.from_numpy(M).cuda(), 1e-13)
+    assert (host(r.status) == 0).all()
+    for s in range(B):
+        rx, rit, _, _, _ = OI.hb_invert_dense(M[s], 1e-13)
+        assert int(r.iterations[s]) == rit
+        x = host(r.inverse[s])
+        assert np.abs(x - rx).max() <= 1e-12 * np.abs(rx).max()
+        assert np.abs(np.eye(n) - M[s] @ x).sum(axis=1).max() < 1e-13
+    Z = M.copy()
+    Z[2, 7, 7] = 0.0
+    rz = hb_invert_dense(Z)
+    assert host(rz.status).tolist() == [0, 0, 5, 0, 0] and int(rz.index[2]) == 7
+    with pytest.raises(ZeroDiagonal) as e:
+        hb_invert_dense(Z[2])
+    assert e.value.index == 7
+    with pytest.raises(MaxIterationsExceeded) as e:
+        hb_invert_dense(M[0], 1e-13, max_iter=1)
+    assert e.value.iterations == 1
