@@ -120,8 +120,9 @@ __device__ __forceinline__ void ntdm_one(const double *__restrict__ d, const dou
 
 // flags == nullptr: one thread per system, scratch column = system.
 // flags != nullptr (re-solve of systems a partitioned kernel flagged): `slots`
-// threads walk the batch; flagged systems are solved with the thread's own
-// scratch column (Scratch{slots}); every other system gets status OK / -1.
+// one-warp CTAs walk the batch 32 systems at a time; a flagged system is
+// solved by its lane with the CTA's scratch column (Scratch{slots}); every
+// other system gets status OK / -1.
 __device__ __forceinline__ bool flagged(const int32_t *flags, int64_t s, int fs) {
   bool f = false;
   for (int r = 0; r < fs; ++r) f |= flags[s * fs + r] != 0;
@@ -140,10 +141,20 @@ ntdm_seq_kernel(const double *__restrict__ d, const double *__restrict__ e,
     if (t < batch) ntdm_one(d, e, f, b, x, recw, status, index, n, lay, t, Scratch{batch}, t);
     return;
   }
-  if (t >= slots) return;
-  for (int64_t s = t; s < batch; s += slots) {
-    if (flagged(flags, s, fs)) ntdm_one(d, e, f, b, x, recw, status, index, n, lay, s, Scratch{slots}, t);
-    else set_status(status, index, s, BX_STATUS_OK, -1);
+  // re-solve mode: one warp per scratch slot (CTA), lanes check 32 systems'
+  // flags at a time; flagged ones are solved one after another by their lane
+  const int slot = blockIdx.x, lane = threadIdx.x;
+  for (int64_t s0 = (int64_t)slot * 32; s0 < batch; s0 += slots * 32) {
+    const int64_t s = s0 + lane;
+    const bool fl = s < batch && flagged(flags, s, fs);
+    if (s < batch && !fl) set_status(status, index, s, BX_STATUS_OK, -1);
+    unsigned todo = __ballot_sync(0xffffffffu, fl);
+    while (todo) {
+      const int l = __ffs(todo) - 1;
+      todo &= todo - 1;
+      if (lane == l) ntdm_one(d, e, f, b, x, recw, status, index, n, lay, s, Scratch{slots}, slot);
+      __syncwarp();
+    }
   }
 }
 
@@ -298,18 +309,26 @@ penta_seq_kernel(const double *__restrict__ c, const double *__restrict__ d,
                       Scratch{batch}, t);
     return;
   }
-  if (t >= slots) return;
-  for (int64_t s = t; s < batch; s += slots) {
-    if (flagged(flags, s, fs)) {
-      penta_one<kMod>(c, d, e, f, g, b, x, pivw, phiw, status, index, nz_out, n, lay, s,
-                      Scratch{slots}, t);
-    } else {
+  const int slot = blockIdx.x, lane = threadIdx.x;
+  for (int64_t s0 = (int64_t)slot * 32; s0 < batch; s0 += slots * 32) {
+    const int64_t s = s0 + lane;
+    const bool fl = s < batch && flagged(flags, s, fs);
+    if (s < batch && !fl) {
       set_status(status, index, s, BX_STATUS_OK, -1);
       if (nz_out && nzpart) {
         int64_t nz = 0;
         for (int r = 0; r < fs; ++r) nz += nzpart[s * fs + r];
         nz_out[s] = nz;
       }
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, fl);
+    while (todo) {
+      const int l = __ffs(todo) - 1;
+      todo &= todo - 1;
+      if (lane == l)
+        penta_one<kMod>(c, d, e, f, g, b, x, pivw, phiw, status, index, nz_out, n, lay, s,
+                        Scratch{slots}, slot);
+      __syncwarp();
     }
   }
 }
@@ -407,7 +426,7 @@ void direct_fixup(int kind, const double *c, const double *d, const double *e, c
                   const int32_t *flags, int fs, const int32_t *nzpart, int32_t *st, int32_t *ix,
                   int64_t *nz, int64_t batch, int64_t n, int64_t ld, int layout,
                   cudaStream_t stream) {
-  const dim3 grid((unsigned)(kFixSlots / kSeqThreads));
+  const dim3 grid((unsigned)kFixSlots);  // one warp per scratch slot
   if (kind == 0) {
     if (layout == BX_LAYOUT_INTERLEAVED)
       ntdm_seq_kernel<<<grid, kSeqThreads, 0, stream>>>(d, e, f, b, x, scratch, st, ix, batch, n,

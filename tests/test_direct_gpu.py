@@ -388,3 +388,21 @@ def test_partitioned_nonfinite_entry_matches_reference(cuda, k):
     assert np.array_equal(np.isnan(x[0]), np.isnan(x_ref[0]))
     fin = np.isfinite(x_ref[0])
     assert np.array_equal(x[0][fin], x_ref[0][fin])
+
+
+@pytest.mark.parametrize("k,n", [(1, 4096), (2, 4096), (2, 6000)])
+def test_partitioned_is_deterministic(cuda, k, n):
+    """compute-sanitizer is closed on this pool; a race in the cluster /
+    DSMEM / mbarrier exchange of the partitioned kernel would show up as
+    run-to-run differences: 12 repeated solves must agree bit for bit."""
+    if k == 1:
+        a = W.td_dominant(64, n, seed=9)
+        A = TriMatrix.from_diagonals(*a[:3], layout="system")
+        run = lambda: host(solve_ntdm(A, a[3], algo="partitioned", residual=False).x)  # noqa: E731
+    else:
+        a = W.pd_dominant(64, n, seed=9)
+        A = PentaMatrix.from_diagonals(*a[:5], layout="system")
+        run = lambda: host(solve_npdm(A, a[5], algo="partitioned", residual=False).x)  # noqa: E731
+    x0 = run()
+    for _ in range(11):
+        assert np.array_equal(run(), x0)

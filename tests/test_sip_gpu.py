@@ -164,3 +164,15 @@ def test_alpha_requires_stride3(cuda):
     p = W.five_point(1, 64, 2)
     with pytest.raises(CudaError):
         sip_solve(PentaMatrix.from_diagonals(*p[:5]), p[5], SipConfig(tolerance=1e-8, alpha=0.5))
+
+
+def test_sip_wavefront_is_deterministic(cuda):
+    """The wavefront kernel's TMA ring / mbarrier / named-barrier protocol:
+    repeated solves give the same bits (race detector substitute)."""
+    g = W.five_point(8, 64 * 48, 48, seed=21)
+    tol = W.sip_tolerance(g[5])
+    S = StencilMatrix.from_diagonals(*g[:5], m=48)
+    cfg = SipConfig(tolerance=tol, max_iterations=100, alpha=0.5)
+    x0 = sip_solve(S, g[5], cfg, algo="wavefront").x.cpu().numpy()
+    for _ in range(8):
+        assert np.array_equal(sip_solve(S, g[5], cfg, algo="wavefront").x.cpu().numpy(), x0)
