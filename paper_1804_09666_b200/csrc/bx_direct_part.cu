@@ -54,9 +54,7 @@ extern "C" int bx_trace_read(void *host, size_t bytes) {
   } while (0)
 #endif
 
-#ifndef BX_PART_LA
-#define BX_PART_LA 1  // input groups in flight ahead of the elimination (measured: 1 > 2 > 3)
-#endif
+#include "bx_part_phases.cuh"
 
 namespace bx {
 namespace part {
@@ -95,21 +93,17 @@ struct Smem {
       sizeof(double) * (size_t)(kState + kInfo + kWPort + kWLR + kRoots + kMisc);
 };
 
-// +-2 diagonals held sparse (MNPDM's case): per system a row-sorted list of
-// the rows where sub2 or sup2 is nonzero, k slots per system (row -1 pads)
-struct Outer {
-  const int32_t *rows;
-  const double *sub2, *sup2;
-  int64_t k;
-};
-
 template <int K, int M, int T, bool VEC, bool SP, class Lay>
 __global__ void __launch_bounds__(T)
 part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
             const double *__restrict__ ep, const double *__restrict__ f1p,
             const double *__restrict__ f2p, const double *__restrict__ bp,
             double *__restrict__ xp, int32_t *status, int32_t *index, int64_t *nz_out,
-            int64_t batch, int64_t n, Lay lay, int csize, Outer outer) {
+            int64_t batch, int64_t n, Lay lay, int csize, Outer outer,
+            const int32_t *__restrict__ only) {
+  // only != nullptr: retry pass after the interface-iteration kernel
+  // (bx_direct_halo.cu) -- solve just the systems it marked, OR flags into status
+  if (only && only[blockIdx.x / csize] == 0) return;
   using SM = Smem<K, M, T>;
   constexpr int NW = SM::NW;
   static_assert(T % 32 == 0 && (NW & (NW - 1)) == 0, "T must be 32 * power of two");
@@ -126,7 +120,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   const int64_t s = blockIdx.x / csize;
   const int64_t seg0 = (int64_t)crank * (T * M);
   const int64_t base = seg0 + (int64_t)t * M;
-  auto st = [&](int q, int j) -> double & { return state[(q * M + j) * T + t]; };
+  using CH = Chunk<K, M, T, VEC, SP, Lay>;
   // misc: [0] nz counter (int), [1] cluster mbarrier (8-byte slot)
   uint64_t *cbar = reinterpret_cast<uint64_t *>(misc + 2);
   if (t == 0) {
@@ -140,246 +134,17 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   if (csize > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
   BX_TR(0);
-  // ---------------- phase 1: downward elimination --------------------------
-  // Gaussian elimination of the chunk against its own normalised rows:
-  // x_{j-2} is eliminated with row j-2, then x_{j-1} with row j-1, and the
-  // row is scaled by 1/mu (MUFU seed + Newton, rcp).  Stored (normalised):
-  //   x_j + p x_{j+1} + q x_{j+2} + W.L = y
-  // (measured: 20 FP64 ops/row beat the division-free variant's 37, whose
-  // shorter dependent chain does not pay for its extra issue slots)
-  int32_t bad = -1;
-  int nzc = 0;
-  // carried rows j-1 (f1, g1, y1, W1) and j-2: p, q, y, W of the stored rows
-  double f1 = 0, g1 = 0, y1 = 0, f2 = 0, g2 = 0, y2 = 0;
-  double W1[K], W2[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) W1[k] = W2[k] = 0.0;
-  if (K == 2) { W2[0] = -1.0; W1[K - 1] = -1.0; }
-  else W1[0] = -1.0;
-  constexpr int G = 4;
-  static_assert(M % G == 0, "M must be a multiple of 4");
-  // register ring of input groups, LA groups in flight ahead of the one being
-  // eliminated; the g loop is fully unrolled so the ring slots are fixed
-  // registers (a copy between loop iterations would wait for the load)
-  constexpr int LA = BX_PART_LA < M / G ? BX_PART_LA : M / G - 1 > 0 ? M / G - 1 : 1;
-  constexpr int RG = LA + 1;
-  struct Grp {
-    double a2[G], a1[G], e[G], c1[G], c2[G], b[G];
-  } ring[RG];
-  auto load_group = [&](int g, Grp &gr) {
-    double(&A2)[G] = gr.a2;
-    double(&A1)[G] = gr.a1;
-    double(&E)[G] = gr.e;
-    double(&C1)[G] = gr.c1;
-    double(&C2)[G] = gr.c2;
-    double(&Bv)[G] = gr.b;
-    const int64_t i0 = base + g * G;
-    if (VEC && i0 + G <= n) {
-      if (K == 2 && !SP) ld4(c2p + lay(i0, s), A2);
-      ld4(c1p + lay(i0, s), A1);
-      ld4(ep + lay(i0, s), E);
-      ld4(f1p + lay(i0, s), C1);
-      if (K == 2 && !SP) ld4(f2p + lay(i0, s), C2);
-      ld4(bp + lay(i0, s), Bv);
-      // (slots outside the matrix are masked where the group is consumed:
-      // touching the registers here would wait for the load)
-    } else {
-#pragma unroll
-      for (int u = 0; u < G; ++u) {
-        const int64_t i = i0 + u;
-        const bool in = i < n;
-        A2[u] = (K == 2 && !SP && in && i >= 2) ? ldg(c2p + lay(i, s)) : 0.0;
-        A1[u] = (in && i >= 1) ? ldg(c1p + lay(i, s)) : 0.0;
-        E[u] = in ? ldg(ep + lay(i, s)) : 1.0;  // padding rows: identity
-        C1[u] = (in && i <= n - 2) ? ldg(f1p + lay(i, s)) : 0.0;
-        C2[u] = (K == 2 && !SP && in && i <= n - 3) ? ldg(f2p + lay(i, s)) : 0.0;
-        Bv[u] = in ? ldg(bp + lay(i, s)) : 0.0;
-      }
-    }
-  };
-  // sparse outer diagonals: the slice [ob, oe) of this system's sorted list
-  // that falls in this thread's rows (empty for almost every thread); the
-  // first 8 list rows are fetched with independent loads (one round trip)
-  int ob = 0, oe = 0;
-  auto outer_slice = [&]() {
-    const int32_t *orow = outer.rows + s * outer.k;
-    const int k = (int)outer.k;
-    int32_t r8[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) r8[q] = q < k ? __ldg(orow + q) : -1;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      ob += (r8[q] >= 0 && r8[q] < base) ? 1 : 0;
-      oe += (r8[q] >= 0 && r8[q] < base + M) ? 1 : 0;
-    }
-    if (k > 8 && oe == 8) {  // long lists: continue the walk
-      ob = min(ob, 8);
-      while (ob < k && orow[ob] >= 0 && orow[ob] < base) ++ob;
-      oe = ob;
-      while (oe < k && orow[oe] >= 0 && orow[oe] < base + M) ++oe;
-    }
-  };
-  // this thread's first 4 entries in registers (rows compared per row, no
-  // memory access on the elimination chain); more than 4 fall back to loads
-  int32_t er[4] = {-1, -1, -1, -1};
-  double es2[4] = {0, 0, 0, 0}, ep2[4] = {0, 0, 0, 0};
-  auto outer_regs = [&]() {
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (ob + q < oe) {
-        const int64_t o = s * outer.k + ob + q;
-        er[q] = __ldg(outer.rows + o);
-        es2[q] = __ldg(outer.sub2 + o);
-        ep2[q] = __ldg(outer.sup2 + o);
-      }
-  };
-
-
-  const bool first = base == 0;                             // rows 0, 1 of the system
-  const int rend = (int)min(n - base, (int64_t)(M + 4));     // n - base, clamped
-#pragma unroll
-  for (int g = 0; g < LA && g < M / G; ++g) load_group(g, ring[g]);
-  if (SP) {  // after the first input loads are in flight
-    outer_slice();
-    outer_regs();
-  }
-#pragma unroll
-  for (int g = 0; g < M / G; ++g) {
-    if (g + LA < M / G) load_group(g + LA, ring[(g + LA) % RG]);
-    const Grp &cur = ring[g % RG];
-#pragma unroll
-    for (int u = 0; u < G; ++u) {
-    const int j = g * G + u;
-    const int64_t i = base + j;  // slots outside the matrix are never trusted:
-    // chunk bases are multiples of M, so only rows j < 2 of the first chunk
-    // can fall left of the matrix; the right edge is a 32-bit test on rend
-    double a2 = (K != 2 || SP) ? 0.0 : cur.a2[u];
-    double a1 = cur.a1[u];
-    if (j < 2 && first) {
-      a2 = 0.0;
-      if (j < 1) a1 = 0.0;
-    }
-    const double e = cur.e[u];
-    const double c1 = j > rend - 2 ? 0.0 : cur.c1[u];
-    double c2 = (K != 2 || SP || j > rend - 3) ? 0.0 : cur.c2[u];
-    if (SP) {  // branch-free for the register entries (the row loop stays one block)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const bool h = er[q] == (int32_t)i;
-        a2 = h ? (i < 2 ? 0.0 : es2[q]) : a2;
-        c2 = h ? (i > n - 3 ? 0.0 : ep2[q]) : c2;
-      }
-    }
-    if (SP && oe - ob > 4) {
-      for (int q = ob + 4; q < oe; ++q)
-        if (outer.rows[s * outer.k + q] == (int32_t)i) {
-          a2 = i < 2 ? 0.0 : outer.sub2[s * outer.k + q];
-          c2 = i > n - 3 ? 0.0 : outer.sup2[s * outer.k + q];
-        }
-    }
-    const double b = cur.b[u];
-    // reciprocal form on normalised carried rows (p, q, y, w); rows -2, -1
-    // are the virtual rows x_{-2} - L_0 = 0, x_{-1} - L_{K-1} = 0
-    double mu, c1p, yy, ww[K];
-    if (K == 2) {
-      nzc += (a2 != 0.0);
-      const double t1 = fma(-a2, f2, a1);
-      const double e2 = fma(-a2, g2, e);
-      const double y2p = fma(-a2, y2, b);
-      mu = fma(-t1, f1, e2);
-      c1p = fma(-t1, g1, c1);
-      yy = fma(-t1, y1, y2p);
-#pragma unroll
-      for (int k = 0; k < K; ++k) ww[k] = fma(-t1, W1[k], -a2 * W2[k]);
-    } else {
-      mu = fma(-a1, f1, e);
-      c1p = c1;
-      yy = fma(-a1, y1, b);
-      ww[0] = -a1 * W1[0];
-    }
-    if (mu == 0.0 || !isfinite(mu)) {
-      if (bad < 0) bad = (int32_t)(base + j);
-      mu = 1.0;
-    }
-    const double r = rcp(mu);
-    const double pn = c1p * r, qn = c2 * r, yn = yy * r;
-    st(0, j) = pn;
-    if (K == 2) st(1, j) = qn;
-    st(K, j) = yn;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const double w = ww[k] * r;
-      st(K + 1 + k, j) = w;
-      W2[k] = W1[k];
-      W1[k] = w;
-    }
-    f2 = f1; g2 = g1; y2 = y1;
-    f1 = pn; g1 = qn; y1 = yn;
-    }
-  }
+  // ---------------- phase 1: downward elimination (bx_part_phases.cuh) ------
+  int32_t bad;
+  int nzc;
+  CH::down(state, t, s, base, n, lay, c2p, c1p, ep, f1p, f2p, bp, outer, bad, nzc);
 
   BX_TR(1);
-  // ---------------- phase 1b: upward elimination ---------------------------
-  // x_j = d_j - W_j.L - V_j.R ; state slots after: 0:d, 1..K: W, K+1..2K: V
-  {
-    double d1 = 0, d2 = 0, Wu1[K], Wu2[K], V1[K], V2[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) Wu1[k] = Wu2[k] = V1[k] = V2[k] = 0.0;
-#pragma unroll
-    for (int j = M - 1; j >= 0; --j) {
-      const double p = st(0, j);
-      const double q = K == 2 ? st(1, j) : 0.0;
-      const double y = st(K, j);
-      double W[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) W[k] = st(K + 1 + k, j);
-      double d, Wu[K], V[K];
-      if (j == M - 1) {
-        d = y;
-#pragma unroll
-        for (int k = 0; k < K; ++k) Wu[k] = W[k];
-        V[0] = p;
-        if (K == 2) V[1] = q;
-      } else if (K == 2 && j == M - 2) {
-        d = fma(-p, d1, y);
-#pragma unroll
-        for (int k = 0; k < K; ++k) Wu[k] = fma(-p, Wu1[k], W[k]);
-        V[0] = fma(-p, V1[0], q);
-        V[1] = -p * V1[1];
-      } else {
-        // row j+2 terms first: the row j+1 results (newest) enter last
-        d = K == 2 ? fma(-p, d1, fma(-q, d2, y)) : fma(-p, d1, y);
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          Wu[k] = K == 2 ? fma(-p, Wu1[k], fma(-q, Wu2[k], W[k])) : fma(-p, Wu1[k], W[k]);
-          V[k] = K == 2 ? fma(-p, V1[k], -q * V2[k]) : -p * V1[k];
-        }
-      }
-      st(0, j) = d;
-#pragma unroll
-      for (int k = 0; k < K; ++k) { st(1 + k, j) = Wu[k]; st(1 + K + k, j) = V[k]; }
-      d2 = d1; d1 = d;
-#pragma unroll
-      for (int k = 0; k < K; ++k) { Wu2[k] = Wu1[k]; Wu1[k] = Wu[k]; V2[k] = V1[k]; V1[k] = V[k]; }
-    }
-  }
+  CH::up(state, t);
 
   BX_TR(2);
   // chunk two-port from the thread's own rows 0..K-1 (F) and M-K..M-1 (E)
-  TwoPort<K> port;
-#pragma unroll
-  for (int a = 0; a < K; ++a) {
-    const int jf = a, je = M - K + a;
-    port.F.g.v[a] = st(0, jf);
-    port.E.g.v[a] = st(0, je);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      port.F.A.m[a][k] = -st(1 + k, jf);
-      port.F.B.m[a][k] = -st(1 + K + k, jf);
-      port.E.A.m[a][k] = -st(1 + k, je);
-      port.E.B.m[a][k] = -st(1 + K + k, je);
-    }
-  }
+  TwoPort<K> port = CH::port(state, t);
 
   // ---------------- tree ascent ---------------------------------------------
   // Levels 0..NLW-1 inside every warp (shuffles), then warp 0 alone reduces
@@ -586,26 +351,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
 
   BX_TR(6);
   // ---------------- phase 3: x_j = d - W.L - V.R -----------------------------
-#pragma unroll 1
-  for (int g = 0; g < M / G; ++g) {
-    double xv[G];
-#pragma unroll
-    for (int u = 0; u < G; ++u) {
-      const int j = g * G + u;
-      double v = st(0, j);
-#pragma unroll
-      for (int k = 0; k < K; ++k) v = fma(-st(1 + k, j), L.v[k], fma(-st(1 + K + k, j), R.v[k], v));
-      xv[u] = v;
-    }
-    const int64_t i0 = base + g * G;
-    if (VEC && i0 + G <= n) {
-      st4(xp + lay(i0, s), xv);
-    } else {
-#pragma unroll
-      for (int u = 0; u < G; ++u)
-        if (i0 + u < n) xp[lay(i0 + u, s)] = xv[u];
-    }
-  }
+  CH::write_x(state, t, s, base, n, lay, xp, L, R);
 
   BX_TR(7);
   // ---------------- status / counters ---------------------------------------
@@ -621,7 +367,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
       if (bad >= 0) atomicMin(&misc[1], bad);
       __syncthreads();
     }
-    if (t == 0) {
+    if (t == 0 && (any_bad || !only)) {
       if (status) status[s] = any_bad ? BX_STATUS_ZERO_PIVOT : BX_STATUS_OK;
       if (index) index[s] = any_bad ? misc[1] : -1;
     }
@@ -651,11 +397,13 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
 // ----------------------------------------------------------------------------
 // launch configuration
 // ----------------------------------------------------------------------------
+static const Outer kNoOuter{nullptr, nullptr, nullptr, 0};
+
 template <int K, int M, int T, bool VEC, class Lay, bool SP = false>
 static int launch(const double *c2, const double *c1, const double *e, const double *f1,
                   const double *f2, const double *b, double *x, int32_t *st, int32_t *ix,
                   int64_t *nz, int64_t batch, int64_t n, Lay lay, cudaStream_t stream,
-                  Outer outer = Outer{nullptr, nullptr, nullptr, 0}) {
+                  Outer outer = kNoOuter, const int32_t *only = nullptr) {
   constexpr int rows = M * T;
   const int csize = (int)((n + rows - 1) / rows);
   if (csize > 8) {
@@ -669,7 +417,7 @@ static int launch(const double *c2, const double *c1, const double *e, const dou
 #endif
   auto kern = part_kernel<K, M, T, VEC, SP, Lay>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (csize > 1) {  // single-CTA systems write status/index/nz in the kernel
+  if (csize > 1 && !only) {  // single-CTA systems write status/index/nz in the kernel
     if (nz) cudaMemsetAsync(nz, 0, sizeof(int64_t) * (size_t)batch, stream);
     if (st) cudaMemsetAsync(st, 0, sizeof(int32_t) * (size_t)batch, stream);     // BX_STATUS_OK
     if (ix) cudaMemsetAsync(ix, 0xff, sizeof(int32_t) * (size_t)batch, stream);  // -1
@@ -687,7 +435,7 @@ static int launch(const double *c2, const double *c1, const double *e, const dou
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t err = cudaLaunchKernelEx(&cfg, kern, c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n,
-                                       lay, csize, outer);
+                                       lay, csize, outer, only);
   if (err != cudaSuccess) {
     bxh::set_error("partitioned solver launch: %s", cudaGetErrorString(err));
     return BX_ERR_CUDA;
@@ -710,7 +458,8 @@ static bool use_1k_ctas(int64_t n) {
 template <int K, bool VEC, class Lay>
 static int dispatch2(const double *c2, const double *c1, const double *e, const double *f1,
                      const double *f2, const double *b, double *x, int32_t *st, int32_t *ix,
-                     int64_t *nz, int64_t batch, int64_t n, Lay lay, cudaStream_t stream) {
+                     int64_t *nz, int64_t batch, int64_t n, Lay lay, cudaStream_t stream,
+                     const int32_t *only) {
   // rows per CTA = M*T; small systems use small CTAs (many CTAs per SM).
   // BX_PART_CFG (developer knob, benchmarking only) forces one configuration.
   static int forced = -2;
@@ -719,19 +468,19 @@ static int dispatch2(const double *c2, const double *c1, const double *e, const 
     forced = env ? atoi(env) : -1;
   }
   switch (forced) {
-    case 0: return launch<K, 8, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
-    case 1: return launch<K, 8, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
-    case 2: return launch<K, 8, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
-    case 3: return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
-    case 4: return launch<K, 16, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
-    case 5: return launch<K, 32, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
-    case 6: return launch<K, 16, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+    case 0: return launch<K, 8, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
+    case 1: return launch<K, 8, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
+    case 2: return launch<K, 8, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
+    case 3: return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
+    case 4: return launch<K, 16, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
+    case 5: return launch<K, 32, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
+    case 6: return launch<K, 16, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
     default: break;
   }
-  if (n <= 256) return launch<K, 8, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
-  if (n <= 512) return launch<K, 8, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
-  if (use_1k_ctas(n)) return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
-  return launch<K, 16, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+  if (n <= 256) return launch<K, 8, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
+  if (n <= 512) return launch<K, 8, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
+  if (use_1k_ctas(n)) return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
+  return launch<K, 16, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
 }
 
 // sparse +-2 diagonals (MNPDM): default shapes only, K = 2
@@ -800,11 +549,11 @@ template <int K, class Lay>
 static int dispatch(const double *c2, const double *c1, const double *e, const double *f1,
                     const double *f2, const double *b, double *x, int32_t *st, int32_t *ix,
                     int64_t *nz, int64_t batch, int64_t n, Lay lay, cudaStream_t stream,
-                    bool vec_ok) {
+                    bool vec_ok, const int32_t *only = nullptr) {
   vec_ok = vec_ok && aligned32(c2) && aligned32(c1) && aligned32(e) && aligned32(f1) &&
            aligned32(f2) && aligned32(b) && aligned32(x);
-  if (vec_ok) return dispatch2<K, true>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
-  return dispatch2<K, false>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream);
+  if (vec_ok) return dispatch2<K, true>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, only);
+  return dispatch2<K, false>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, only);
 }
 
 }  // namespace part
@@ -848,12 +597,20 @@ int ntdm_part(const double *d, const double *e, const double *f, const double *b
     rc = seg_solve(1, nullptr, d, e, f, nullptr, b, x, flags, nullptr, batch, n, ld, stream, &fs);
   if (rc == BX_ERR_UNSUPPORTED) {
     fs = 1;
+    // first pass: interface iteration; the tree then solves only what it marked
+    const int32_t *only = nullptr;
+    if (halo_enabled()) {
+      rc = halo_solve(1, nullptr, d, e, f, nullptr, b, x, flags, nullptr, batch, n, ld, layout,
+                      stream, nullptr, nullptr, nullptr, 0);
+      if (rc == BX_OK) only = flags + batch;
+      else if (rc != BX_ERR_UNSUPPORTED) return rc;
+    }
     if (layout == BX_LAYOUT_SYSTEM_MAJOR)
       rc = part::dispatch<1>(nullptr, d, e, f, nullptr, b, x, flags, nullptr, nullptr, batch, n,
-                             SystemMajor{ld}, stream, ld % 4 == 0);
+                             SystemMajor{ld}, stream, ld % 4 == 0, only);
     else
       rc = part::dispatch<1>(nullptr, d, e, f, nullptr, b, x, flags, nullptr, nullptr, batch, n,
-                             Interleaved{ld}, stream, false);
+                             Interleaved{ld}, stream, false, only);
   }
   if (rc != BX_OK) return rc;
   direct_fixup(0, nullptr, d, e, f, nullptr, b, x, scratch, flags, fs, nullptr, st, ix, nullptr,
@@ -876,12 +633,22 @@ int penta_part(bool mod, const double *c, const double *d, const double *e, cons
   }
   if (!seg) {
     fs = 1;
+    // first pass: interface iteration (it also counts nz); the tree then
+    // solves only the systems it marked
+    const int32_t *only = nullptr;
+    if (halo_enabled()) {
+      rc = halo_solve(2, c, d, e, f, g, b, x, flags, nz, batch, n, ld, layout, stream, nullptr,
+                      nullptr, nullptr, 0);
+      if (rc == BX_OK) only = flags + batch;
+      else if (rc != BX_ERR_UNSUPPORTED) return rc;
+    }
+    int64_t *tnz = only ? nullptr : nz;
     if (layout == BX_LAYOUT_SYSTEM_MAJOR)
-      rc = part::dispatch<2>(c, d, e, f, g, b, x, flags, nullptr, nz, batch, n, SystemMajor{ld},
-                             stream, ld % 4 == 0);
+      rc = part::dispatch<2>(c, d, e, f, g, b, x, flags, nullptr, tnz, batch, n, SystemMajor{ld},
+                             stream, ld % 4 == 0, only);
     else
-      rc = part::dispatch<2>(c, d, e, f, g, b, x, flags, nullptr, nz, batch, n, Interleaved{ld},
-                             stream, false);
+      rc = part::dispatch<2>(c, d, e, f, g, b, x, flags, nullptr, tnz, batch, n, Interleaved{ld},
+                             stream, false, only);
   }
   if (rc != BX_OK) return rc;
   direct_fixup(mod ? 2 : 1, c, d, e, f, g, b, x, scratch, flags, fs, seg && nz ? nzpart : nullptr,

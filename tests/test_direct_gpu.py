@@ -406,3 +406,97 @@ def test_partitioned_is_deterministic(cuda, k, n):
     x0 = run()
     for _ in range(11):
         assert np.array_equal(run(), x0)
+
+
+# --------------------------------------------------------------------------
+# interface-iteration first pass (bx_direct_halo.cu) and its retry contract
+# --------------------------------------------------------------------------
+def _weakly_dominant(k, bsz, n, margin, seed):
+    """Band rows whose dominance margin is tiny: the chunk Green functions
+    barely decay, so the interface coupling is far above the sweep guard and
+    the two-port tree has to take the systems over."""
+    rng = np.random.default_rng(seed)
+    if k == 1:
+        sub = -np.ones((bsz, n)); sub[:, 0] = 0.0
+        sup = -np.ones((bsz, n)); sup[:, n - 1] = 0.0
+        main = np.abs(sub) + np.abs(sup) + margin * (1.0 + rng.uniform(0, 1, (bsz, n)))
+        rhs = rng.uniform(-1, 1, (bsz, n))
+        return (np.ascontiguousarray(sub[:, 1:]), main, np.ascontiguousarray(sup[:, :-1]), rhs)
+    s2 = -0.25 * np.ones((bsz, n)); s2[:, :2] = 0.0
+    s1 = -np.ones((bsz, n)); s1[:, 0] = 0.0
+    p1 = -np.ones((bsz, n)); p1[:, n - 1] = 0.0
+    p2 = -0.25 * np.ones((bsz, n)); p2[:, n - 2:] = 0.0
+    main = np.abs(s2) + np.abs(s1) + np.abs(p1) + np.abs(p2) + margin * (1.0 + rng.uniform(0, 1, (bsz, n)))
+    rhs = rng.uniform(-1, 1, (bsz, n))
+    return (np.ascontiguousarray(s2[:, 2:]), np.ascontiguousarray(s1[:, 1:]), main,
+            np.ascontiguousarray(p1[:, :-1]), np.ascontiguousarray(p2[:, :-2]), rhs)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("n", [200, 1024, 4096, 6000])
+@pytest.mark.parametrize("k", [1, 2])
+def test_partitioned_weakly_dominant_retries_on_the_tree(cuda, layout, k, n):
+    d = _weakly_dominant(k, 12, n, 1e-3, seed=n + k)
+    if k == 1:
+        x_ref, _, _ = D.ntdm(*d)
+        rep = solve_ntdm(TriMatrix.from_diagonals(*d[:3], layout=layout), d[3], algo="partitioned")
+    else:
+        x_ref, _, _ = D.npdm(*d)
+        rep = solve_npdm(PentaMatrix.from_diagonals(*d[:5], layout=layout), d[5], algo="partitioned")
+    assert (host(rep.status) == 0).all()
+    # cond ~ 4 / margin: the bound is the tolerance scaled by it
+    assert rel_err(host(rep.x), x_ref).max() <= 1e-9
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_partitioned_mixed_batch_only_marked_systems_retry(cuda, k):
+    # dominant and weakly dominant systems interleaved in one batch: both
+    # passes run, each system ends with its own pass's solution
+    n, bsz = 4096, 16
+    strong = W.td_dominant(bsz, n, seed=5) if k == 1 else W.pd_dominant(bsz, n, seed=5)
+    weak = _weakly_dominant(k, bsz, n, 1e-3, seed=6)
+    mix = [np.where((np.arange(bsz) % 2 == 0)[:, None], a, b) for a, b in zip(strong, weak)]
+    if k == 1:
+        x_ref, _, _ = D.ntdm(*mix)
+        rep = solve_ntdm(TriMatrix.from_diagonals(*mix[:3], layout="system"), mix[3], algo="partitioned")
+    else:
+        x_ref, _, _ = D.npdm(*mix)
+        rep = solve_mnpdm(PentaMatrix.from_diagonals(*mix[:5], layout="system"), mix[5], algo="partitioned")
+        _, _, _, nz = D.mnpdm(*mix)
+        assert np.array_equal(host(rep.ops.total),
+                              np.array([sum(D.ops_mnpdm(n, int(z)).values()) for z in nz]))
+    assert (host(rep.status) == 0).all()
+    err = rel_err(host(rep.x), x_ref)
+    assert err[0::2].max() <= REL_TOL and err[1::2].max() <= 1e-9
+
+
+_KNOB_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {repo!r})
+from paper_1804_09666_b200 import PentaMatrix, TriMatrix, solve_npdm, solve_ntdm, workloads as W
+from oracle import direct as D
+p = W.pd_dominant(8, 4096, seed=21)
+x_ref, _, _ = D.npdm(*p)
+rep = solve_npdm(PentaMatrix.from_diagonals(*p[:5], layout="system"), p[5], algo="partitioned")
+x = rep.x.cpu().numpy()
+e2 = np.abs(x - x_ref).max() / np.abs(x_ref).max()
+d = W.td_dominant(8, 3000, seed=22)
+x_ref, _, _ = D.ntdm(*d)
+rep1 = solve_ntdm(TriMatrix.from_diagonals(*d[:3], layout="system"), d[3], algo="partitioned")
+e1 = np.abs(rep1.x.cpu().numpy() - x_ref).max() / np.abs(x_ref).max()
+ok = bool((rep.status.cpu().numpy() == 0).all() and (rep1.status.cpu().numpy() == 0).all())
+print("KNOB", ok, e1, e2)
+"""
+
+
+@pytest.mark.parametrize("env", [{"BX_HALO_RHO": "0"}, {"BX_PART_HALO": "0"}])
+def test_partitioned_tree_pass_alone_still_solves_dominant_systems(cuda, env):
+    # developer knobs (read once per process): every system marked for the
+    # retry pass / the first pass switched off -- the tree path's parity
+    import os, subprocess, sys
+    from conftest import REPO
+    out = subprocess.run([sys.executable, "-c", _KNOB_SCRIPT.format(repo=REPO)], env={**os.environ, **env},
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = [l for l in out.stdout.splitlines() if l.startswith("KNOB")][-1].split()
+    assert line[1] == "True" and float(line[2]) <= REL_TOL and float(line[3]) <= REL_TOL
