@@ -32,6 +32,7 @@
 // chunk pivots flag the system for the reference-order re-solve exactly as
 // in bx_direct_part.cu.  HBM traffic is the compulsory I/O.
 #include <cooperative_groups.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "bx_common.cuh"
@@ -61,6 +62,10 @@ extern "C" int bx_halo_trace_read(void *host, size_t bytes) {
 
 namespace bx {
 namespace part {
+
+#ifndef BX_HALO_PF
+#define BX_HALO_PF 1  // L2 bulk prefetch: 0 none, 1 own segment (measured 0.473 -> 0.462 ms cfg 2), 2 own + a later CTA's (slower)
+#endif
 
 constexpr int kNit = 3;       // interface sweeps
 constexpr int kH = kNit + 1;  // halo chunks per side
@@ -114,17 +119,19 @@ __device__ __forceinline__ Port<K> zero_port() {
 
 // shared memory (doubles): state[Q][M][T] | halo[2][kH] two-ports (side 0:
 // chunks -kH..-1 of the left neighbour, side 1: chunks T..T+kH-1 of the right
-// one) | itU, itV [T + 2 kH + 1][K] interface iterates (slot i + kH + 1 for
-// interface i in [-kH-1, T+kH-1]; the two end slots stay zero) | misc
+// one) | per warp: itU, itV [kChain + 4][K] interface iterates (slot p + 1
+// for position p of the warp's chain; slots 0 and kChain + 1 stay zero, slot
+// kChain + 2 is the dump of lanes without a second interface) | misc
+constexpr int kChain = 32 + 2 * kH - 1;  // left halo kH | 32 primaries | right halo kH - 1
 template <int K, int M, int T>
 struct HaloSmem {
   static constexpr int Q = 1 + 2 * K;
   static constexpr int NP = (int)(sizeof(TwoPort<K>) / 8);
-  static constexpr int NS = T + 2 * kH + 1;
+  static constexpr int NW = T / 32;
   static constexpr int kState = Q * M * T;
   static constexpr int kHalo = 2 * kH * NP;
-  static constexpr int kIt = NS * K;
-  static constexpr size_t bytes = sizeof(double) * (size_t)(kState + kHalo + 2 * kIt + 8);
+  static constexpr int kIt = (kChain + 4) * K;  // one array of one warp (+1: the dump slot's right neighbour)
+  static constexpr size_t bytes = sizeof(double) * (size_t)(kState + kHalo + 2 * NW * kIt + 8);
 };
 
 template <int K, int M, int T, bool VEC, bool SP, class Lay>
@@ -132,22 +139,23 @@ __global__ void __launch_bounds__(T)
 halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
             const double *__restrict__ ep, const double *__restrict__ f1p,
             const double *__restrict__ f2p, const double *__restrict__ bp,
-            double *__restrict__ xp, int32_t *flags, int32_t *retry, int64_t *nz_out,
-            int64_t batch, int64_t n, Lay lay, int csize, Outer outer, double rho_max) {
+            double *__restrict__ xp, int32_t *flags, int32_t *retry, int32_t *nzpart,
+            int64_t batch, int64_t n, Lay lay, int csize, Outer outer, double rho_max,
+            int pf_ahead) {
   using SM = HaloSmem<K, M, T>;
   using CH = Chunk<K, M, T, VEC, SP, Lay>;
-  constexpr int H = kH, NP = SM::NP, NS = SM::NS;
+  constexpr int H = kH, NP = SM::NP, NW = SM::NW;
   static_assert(T % 32 == 0 && T >= 2 * H, "T must be a multiple of 32");
   extern __shared__ __align__(16) double smem[];
   double *state = smem;
   double *halo = smem + SM::kState;
-  double *itU = halo + SM::kHalo;
+  double *itU = halo + SM::kHalo + (threadIdx.x >> 5) * 2 * SM::kIt;  // this warp's arrays
   double *itV = itU + SM::kIt;
-  int *misc = reinterpret_cast<int *>(itV + SM::kIt);
+  int *misc = reinterpret_cast<int *>(halo + SM::kHalo + 2 * NW * SM::kIt);
   // misc: [0] nz counter (int), [2..3] halo mbarrier (8-byte slot)
   uint64_t *cbar = reinterpret_cast<uint64_t *>(misc + 2);
 
-  const int t = threadIdx.x, lane = t & 31;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int crank = csize > 1 ? (int)cg::this_cluster().block_rank() : 0;
   const bool hasL = crank > 0, hasR = crank < csize - 1;
   const int64_t s = blockIdx.x / csize;
@@ -162,7 +170,28 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     }
   }
   if (csize > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-  for (int k = t; k < 2 * SM::kIt; k += T) itU[k] = 0.0;  // itU | itV are contiguous
+#if BX_HALO_PF
+  if (VEC && t < (K == 2 && !SP ? 6 : 4)) {
+    // warm L2 with this CTA's segment of one array per thread (TMA bulk
+    // prefetch, no registers): the per-group loads of the down sweep then see
+    // L2 latency after the first group.  Bytes still leave HBM exactly once.
+    const double *arr[6] = {bp, ep, c1p, f1p, c2p, f2p};
+    const int64_t rows = min((int64_t)(T * M), n - seg0) & ~(int64_t)3;
+    if (rows > 0) {
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(arr[t] + lay(seg0, s)),
+                   "r"((unsigned)(rows * sizeof(double)))
+                   : "memory");
+#if BX_HALO_PF > 1
+      // ... and with the segment of the CTA BX_HALO_PF_AHEAD launches later
+      const int64_t bn = (int64_t)blockIdx.x + pf_ahead;
+      if (bn < (int64_t)gridDim.x)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(arr[t] + lay((bn % csize) * (T * M), bn / csize)),
+                     "r"((unsigned)(rows * sizeof(double)))
+                     : "memory");
+#endif
+    }
+  }
+#endif
 
   BX_TR(0);
   int32_t bad;
@@ -203,21 +232,37 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   __syncthreads();  // every chunk's state rows are visible
 
   // ---------------- interfaces --------------------------------------------------
-  // thread t: interface t (chunk t | t+1).  Left halo interfaces -kH..-1 are
-  // held as second interfaces by threads 0..kH-1, right halo interfaces
-  // T..T+kH-2 by threads T-kH..T-2.
-  auto halo_port = [&](int side, int h) -> TwoPort<K> {
-    TwoPort<K> p;
+  // Every warp iterates its own chain of interfaces without CTA barriers:
+  //   positions 0..kH-1      the kH interfaces left of the warp's first chunk
+  //                          (second interfaces of lanes 0..kH-1),
+  //   positions kH..kH+31    interface (c | c+1) of the lane's own chunk c,
+  //   positions kH+32..      the kH-1 interfaces right of the warp's last chunk
+  //                          (second interfaces of lanes 32-kH..30).
+  // Chunks outside the CTA come from the halo slots (cluster neighbours) or
+  // are absent (system ends: zero ports, inert interfaces).
+  auto halo_side = [&](int side, int h, bool isE) -> Port<K> {
+    Port<K> p;
     double *v = reinterpret_cast<double *>(&p);
+    const double *src = halo + (side * H + h) * NP + (isE ? NP / 2 : 0);  // TwoPort = {F, E}
 #pragma unroll
-    for (int c = 0; c < NP; ++c) v[c] = halo[(side * H + h) * NP + c];
+    for (int c = 0; c < NP / 2; ++c) v[c] = src[c];
     return p;
+  };
+  auto chunk_side = [&](int c, bool isE) -> Port<K> {  // chunk c of this CTA's numbering
+    if (c >= 0 && c < T) return CH::port_side(state, c, isE ? M - K : 0);
+    if (c < 0 && hasL) return halo_side(0, c + H, isE);
+    if (c >= T && hasR) return halo_side(1, c - T, isE);
+    return zero_port<K>();
   };
   bool ok = true;
   MergeInfo<K> mi, mi2;
-  const Port<K> aE = CH::port_side(state, t, M - K);
-  if (t < T - 1) ok &= iface<K>(aE, CH::port_side(state, t + 1, 0), mi);
-  else if (!hasR) ok &= iface<K>(aE, zero_port<K>(), mi);
+  {  // lanes without a second interface carry an inert one (all zero)
+    double *z = reinterpret_cast<double *>(&mi2);
+#pragma unroll
+    for (int c = 0; c < NP; ++c) z[c] = 0.0;
+  }
+  const bool prim_early = t < T - 1 || !hasR;  // needs nothing from the halo
+  if (prim_early) ok &= iface<K>(chunk_side(t, true), chunk_side(t + 1, false), mi);
   BX_TR(3);
   if (hasL || hasR) {
     asm volatile(
@@ -228,27 +273,25 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
         : "memory");
   }
   BX_TR(4);
-  if (t == T - 1 && hasR) ok &= iface<K>(aE, halo_port(1, 0).F, mi);
-  int i2 = 0;
-  bool sec = false;
-  if (hasL && t < H) {
-    const Port<K> bF = t < H - 1 ? halo_port(0, t + 1).F : CH::port_side(state, 0, 0);
-    ok &= iface<K>(halo_port(0, t).E, bF, mi2);
-    i2 = t - H;
-    sec = true;
-  } else if (hasR && t >= T - H && t < T - 1) {
-    const int h = t - (T - H);
-    ok &= iface<K>(halo_port(1, h).E, halo_port(1, h + 1).F, mi2);
-    i2 = T + h;
-    sec = true;
+  if (!prim_early) ok &= iface<K>(chunk_side(t, true), chunk_side(t + 1, false), mi);
+  const int w0 = t - lane;  // the warp's first chunk
+  int pos2 = kChain + 1;    // dump slot
+  if (lane < H) {
+    const int c = w0 - H + lane;
+    ok &= iface<K>(chunk_side(c, true), chunk_side(c + 1, false), mi2);
+    pos2 = lane;
+  } else if (lane >= 32 - H && lane < 31) {
+    const int c = w0 + lane + H;
+    ok &= iface<K>(chunk_side(c, true), chunk_side(c + 1, false), mi2);
+    pos2 = lane + 2 * H;
   }
   double rho = coupling<K>(mi);
-  if (sec) {
+  {
     const double r2 = coupling<K>(mi2);
     rho = (r2 > rho || r2 != r2) ? r2 : rho;
   }
 
-  // ---------------- block-Jacobi sweeps over the interfaces ---------------------
+  // ---------------- block-Jacobi sweeps over the warp's chain -------------------
   auto ldv = [&](const double *a, int slot) -> Vec<K> {
     Vec<K> r;
 #pragma unroll
@@ -259,33 +302,29 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
 #pragma unroll
     for (int k = 0; k < K; ++k) a[slot * K + k] = x.v[k];
   };
-  const int sl = t + H + 1, sl2 = i2 + H + 1;
+  const int sl = H + lane + 1, sl2 = pos2 + 1;
   Vec<K> u = mi.u.g, v = mi.v.g;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) itU[k] = itV[(kChain + 1) * K + k] = 0.0;
+  }
   stv(itU, sl, u);
   stv(itV, sl, v);
-  if (sec) {
-    stv(itU, sl2, mi2.u.g);
-    stv(itV, sl2, mi2.v.g);
-  }
-  __syncthreads();
+  stv(itU, sl2, mi2.u.g);
+  stv(itV, sl2, mi2.v.g);
+  __syncwarp();
 #pragma unroll 1
   for (int it = 0; it < kNit; ++it) {
     const Vec<K> um = ldv(itU, sl - 1), vp = ldv(itV, sl + 1);
-    Vec<K> um2, vp2;
-    if (sec) {
-      um2 = ldv(itU, sl2 - 1);
-      vp2 = ldv(itV, sl2 + 1);
-    }
-    __syncthreads();
+    const Vec<K> um2 = ldv(itU, sl2 - 1), vp2 = ldv(itV, sl2 + 1);
+    __syncwarp();
     u = apply<K>(mi.u, um, vp);
     v = apply<K>(mi.v, um, vp);
     stv(itU, sl, u);
     stv(itV, sl, v);
-    if (sec) {
-      stv(itU, sl2, apply<K>(mi2.u, um2, vp2));
-      stv(itV, sl2, apply<K>(mi2.v, um2, vp2));
-    }
-    __syncthreads();
+    stv(itU, sl2, apply<K>(mi2.u, um2, vp2));
+    stv(itV, sl2, apply<K>(mi2.v, um2, vp2));
+    __syncwarp();
   }
   const Vec<K> L = ldv(itU, sl - 1), R = v;  // E of chunk t-1, F of chunk t+1
   BX_TR(5);
@@ -295,28 +334,29 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   BX_TR(6);
 
   // ---------------- flags / counters ----------------------------------------------
-  // csize == 1: this CTA owns the system and writes its words itself (no
-  // memsets in the launch); csize > 1: the launcher preset them to 0.
+  // every CTA owns word [s * csize + crank] of flags / retry / nzpart (no
+  // presets, no atomics on global memory)
   if (!ok && bad < 0) bad = (int32_t)seg0;
-  const bool any_bad = __syncthreads_or(bad >= 0);
-  const bool any_slow = __syncthreads_or(!(rho <= rho_max));
+  const bool slow = !(rho <= rho_max);
+  const int64_t w = s * csize + crank;
+  const bool rare = __syncthreads_or(bad >= 0 || slow);
   if (t == 0) {
-    if (csize == 1) {
-      flags[s] = any_bad ? BX_STATUS_ZERO_PIVOT : BX_STATUS_OK;
-      retry[s] = any_slow ? 1 : 0;
-    } else {
-      if (any_bad) flags[s] = BX_STATUS_ZERO_PIVOT;
-      if (any_slow) retry[s] = 1;
-    }
+    flags[w] = BX_STATUS_OK;
+    retry[w] = 0;
   }
-  if (K == 2 && nz_out) {
-    nzc = __reduce_add_sync(0xffffffffu, nzc);
-    if (lane == 0) atomicAdd(&misc[0], nzc);
+  if (rare) {  // say which
     __syncthreads();
-    if (t == 0) {
-      if (csize == 1) nz_out[s] = misc[0];
-      else atomicAdd(reinterpret_cast<unsigned long long *>(nz_out + s), (unsigned long long)misc[0]);
+    if (bad >= 0) flags[w] = BX_STATUS_ZERO_PIVOT;
+    if (slow) retry[w] = 1;
+  }
+  if (K == 2 && nzpart) {
+    nzc = __reduce_add_sync(0xffffffffu, nzc);
+    if (NW > 1) {
+      if (lane == 0) atomicAdd(&misc[0], nzc);
+      __syncthreads();
+      nzc = misc[0];
     }
+    if (t == 0) nzpart[w] = nzc;
   }
 #ifdef BX_HALO_TRACE
   if (threadIdx.x == 0 && blockIdx.x - BX_HALO_TRACE_BASE < 4096u) {
@@ -343,17 +383,21 @@ static double rho_max_default() {
 template <int K, int M, int T, bool VEC, bool SP, class Lay>
 static int halo_launch(const double *c2, const double *c1, const double *e, const double *f1,
                        const double *f2, const double *b, double *x, int32_t *flags,
-                       int32_t *retry, int64_t *nz, int64_t batch, int64_t n, Lay lay,
-                       cudaStream_t stream, Outer outer) {
+                       int32_t *retry, int32_t *nzpart, int64_t batch, int64_t n, Lay lay,
+                       cudaStream_t stream, Outer outer, int *csize_out) {
   constexpr int rows = M * T;
   const int csize = (int)((n + rows - 1) / rows);
   if (csize > 8) return BX_ERR_UNSUPPORTED;  // (the tree kernel reports the limit)
+  *csize_out = csize;
   const size_t smem = HaloSmem<K, M, T>::bytes;
   auto kern = halo_kernel<K, M, T, VEC, SP, Lay>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (csize > 1) {  // flags | retry are contiguous (halo_solve's contract)
-    cudaMemsetAsync(flags, 0, sizeof(int32_t) * 2 * (size_t)batch, stream);
-    if (nz) cudaMemsetAsync(nz, 0, sizeof(int64_t) * (size_t)batch, stream);
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  static const int pf_ahead = getenv("BX_HALO_PF_AHEAD") ? atoi(getenv("BX_HALO_PF_AHEAD")) : 740;
+  if (getenv("BX_HALO_DEBUG")) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T, smem);
+    fprintf(stderr, "halo_kernel<K=%d,M=%d,T=%d>: smem %zu B, %d CTAs/SM, csize %d\n", K, M, T, smem, nb, csize);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(batch * csize));
@@ -367,8 +411,8 @@ static int halo_launch(const double *c2, const double *c1, const double *e, cons
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t err = cudaLaunchKernelEx(&cfg, kern, c2, c1, e, f1, f2, b, x, flags, retry, nz, batch,
-                                       n, lay, csize, outer, rho_max_default());
+  cudaError_t err = cudaLaunchKernelEx(&cfg, kern, c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch,
+                                       n, lay, csize, outer, rho_max_default(), pf_ahead);
   if (err != cudaSuccess) {
     bxh::set_error("partitioned solver (interface iteration) launch: %s", cudaGetErrorString(err));
     return BX_ERR_CUDA;
@@ -379,26 +423,26 @@ static int halo_launch(const double *c2, const double *c1, const double *e, cons
 template <int K, bool VEC, bool SP, class Lay>
 static int halo_shapes(const double *c2, const double *c1, const double *e, const double *f1,
                        const double *f2, const double *b, double *x, int32_t *flags,
-                       int32_t *retry, int64_t *nz, int64_t batch, int64_t n, Lay lay,
-                       cudaStream_t stream, Outer o) {
-  if (n <= 256) return halo_launch<K, 8, 32, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nz, batch, n, lay, stream, o);
-  if (n <= 512) return halo_launch<K, 8, 64, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nz, batch, n, lay, stream, o);
-  if (n <= 8192) return halo_launch<K, 16, 64, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nz, batch, n, lay, stream, o);
-  return halo_launch<K, 16, 128, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nz, batch, n, lay, stream, o);
+                       int32_t *retry, int32_t *nzpart, int64_t batch, int64_t n, Lay lay,
+                       cudaStream_t stream, Outer o, int *cs) {
+  if (n <= 256) return halo_launch<K, 8, 32, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, lay, stream, o, cs);
+  if (n <= 512) return halo_launch<K, 8, 64, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, lay, stream, o, cs);
+  if (n <= 8192) return halo_launch<K, 16, 64, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, lay, stream, o, cs);
+  return halo_launch<K, 16, 128, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, lay, stream, o, cs);
 }
 
 template <int K, bool SP>
 static int halo_layouts(const double *c2, const double *c1, const double *e, const double *f1,
                         const double *f2, const double *b, double *x, int32_t *flags,
-                        int32_t *retry, int64_t *nz, int64_t batch, int64_t n, int64_t ld,
-                        int layout, cudaStream_t stream, Outer o) {
+                        int32_t *retry, int32_t *nzpart, int64_t batch, int64_t n, int64_t ld,
+                        int layout, cudaStream_t stream, Outer o, int *cs) {
   auto a32 = [](const void *p) { return p == nullptr || ((uintptr_t)p & 31u) == 0; };
   if (layout == BX_LAYOUT_SYSTEM_MAJOR) {
     const bool vec = ld % 4 == 0 && a32(c2) && a32(c1) && a32(e) && a32(f1) && a32(f2) && a32(b) && a32(x);
-    if (vec) return halo_shapes<K, true, SP>(c2, c1, e, f1, f2, b, x, flags, retry, nz, batch, n, SystemMajor{ld}, stream, o);
-    return halo_shapes<K, false, SP>(c2, c1, e, f1, f2, b, x, flags, retry, nz, batch, n, SystemMajor{ld}, stream, o);
+    if (vec) return halo_shapes<K, true, SP>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, SystemMajor{ld}, stream, o, cs);
+    return halo_shapes<K, false, SP>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, SystemMajor{ld}, stream, o, cs);
   }
-  return halo_shapes<K, false, SP>(c2, c1, e, f1, f2, b, x, flags, retry, nz, batch, n, Interleaved{ld}, stream, o);
+  return halo_shapes<K, false, SP>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, Interleaved{ld}, stream, o, cs);
 }
 
 }  // namespace part
@@ -412,23 +456,23 @@ bool halo_enabled() {
   return v != 0;
 }
 
-// flags[batch] | retry[batch] contiguous int32 words (retry = flags + batch).
+// flags / retry / nzpart: [batch][*csize] int32 words, one per CTA of a
+// system's cluster (direct_fixup's fs = *csize convention).
 // outer_rows != nullptr: the +-2 diagonals come from the sparse lists (K = 2).
 int halo_solve(int K, const double *c2, const double *c1, const double *e, const double *f1,
-               const double *f2, const double *b, double *x, int32_t *flags, int64_t *nz,
-               int64_t batch, int64_t n, int64_t ld, int layout, cudaStream_t stream,
-               const int32_t *outer_rows, const double *outer_sub2, const double *outer_sup2,
-               int64_t outer_k) {
-  int32_t *retry = flags + batch;
+               const double *f2, const double *b, double *x, int32_t *flags, int32_t *retry,
+               int32_t *nzpart, int64_t batch, int64_t n, int64_t ld, int layout,
+               cudaStream_t stream, const int32_t *outer_rows, const double *outer_sub2,
+               const double *outer_sup2, int64_t outer_k, int *csize) {
   const part::Outer o{outer_rows, outer_sub2, outer_sup2, outer_k};
   if (K == 1)
     return part::halo_layouts<1, false>(nullptr, c1, e, f1, nullptr, b, x, flags, retry, nullptr,
-                                        batch, n, ld, layout, stream, o);
+                                        batch, n, ld, layout, stream, o, csize);
   if (outer_rows)
-    return part::halo_layouts<2, true>(nullptr, c1, e, f1, nullptr, b, x, flags, retry, nz, batch,
-                                       n, ld, layout, stream, o);
-  return part::halo_layouts<2, false>(c2, c1, e, f1, f2, b, x, flags, retry, nz, batch, n, ld,
-                                      layout, stream, o);
+    return part::halo_layouts<2, true>(nullptr, c1, e, f1, nullptr, b, x, flags, retry, nzpart,
+                                       batch, n, ld, layout, stream, o, csize);
+  return part::halo_layouts<2, false>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, ld,
+                                      layout, stream, o, csize);
 }
 
 }  // namespace bx

@@ -100,10 +100,11 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
             const double *__restrict__ f2p, const double *__restrict__ bp,
             double *__restrict__ xp, int32_t *status, int32_t *index, int64_t *nz_out,
             int64_t batch, int64_t n, Lay lay, int csize, Outer outer,
-            const int32_t *__restrict__ only) {
+            const int32_t *__restrict__ only, int fs) {
   // only != nullptr: retry pass after the interface-iteration kernel
-  // (bx_direct_halo.cu) -- solve just the systems it marked, OR flags into status
-  if (only && only[blockIdx.x / csize] == 0) return;
+  // (bx_direct_halo.cu) -- a small persistent grid whose clusters walk the
+  // batch and solve just the systems it marked (only[s * fs + r] != 0 for some
+  // r < fs), OR-ing flags into status[s * fs]; fs = 1 otherwise
   using SM = Smem<K, M, T>;
   constexpr int NW = SM::NW;
   static_assert(T % 32 == 0 && (NW & (NW - 1)) == 0, "T must be 32 * power of two");
@@ -117,7 +118,6 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
 
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int crank = csize > 1 ? (int)cg::this_cluster().block_rank() : 0;
-  const int64_t s = blockIdx.x / csize;
   const int64_t seg0 = (int64_t)crank * (T * M);
   const int64_t base = seg0 + (int64_t)t * M;
   using CH = Chunk<K, M, T, VEC, SP, Lay>;
@@ -133,6 +133,22 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   }
   if (csize > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
+  unsigned ph = 0;  // parity of the root mbarrier's current phase
+  const int64_t nclus = gridDim.x / csize;
+  for (int64_t s0 = blockIdx.x / csize; s0 < batch; s0 += only ? 32 * nclus : batch) {
+  // retry pass: 32 of this cluster's systems are tested per round trip (every
+  // warp of the cluster reads the same words: the walk is cluster-uniform)
+  unsigned todo = 1u;
+  if (only) {
+    const int64_t sl = s0 + (int64_t)lane * nclus;
+    bool marked = false;
+    if (sl < batch)
+      for (int r = 0; r < fs; ++r) marked |= only[sl * fs + r] != 0;
+    todo = __ballot_sync(0xffffffffu, marked);
+  }
+  while (todo) {
+  const int64_t s = s0 + (int64_t)(__ffs(todo) - 1) * nclus;
+  todo &= todo - 1;
   BX_TR(0);
   // ---------------- phase 1: downward elimination (bx_part_phases.cuh) ------
   int32_t bad;
@@ -253,8 +269,8 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "W_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
-        "@!p bra W_%=;\n}" ::"r"(smem_addr(cbar))
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n}" ::"r"(smem_addr(cbar)), "r"(ph)
         : "memory");
     __syncwarp();
     if (lane == 0) {
@@ -368,11 +384,11 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
       __syncthreads();
     }
     if (t == 0 && (any_bad || !only)) {
-      if (status) status[s] = any_bad ? BX_STATUS_ZERO_PIVOT : BX_STATUS_OK;
+      if (status) status[s * fs] = any_bad ? BX_STATUS_ZERO_PIVOT : BX_STATUS_OK;
       if (index) index[s] = any_bad ? misc[1] : -1;
     }
   } else if (__syncthreads_or(bad >= 0)) {
-    if (status) status[s] = BX_STATUS_ZERO_PIVOT;
+    if (status) status[s * fs] = BX_STATUS_ZERO_PIVOT;
     if (index && bad >= 0) atomicMin(reinterpret_cast<unsigned int *>(index + s), (unsigned int)bad);
   }
 #ifdef BX_TRACE
@@ -392,6 +408,20 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
       else atomicAdd(reinterpret_cast<unsigned long long *>(nz_out + s), (unsigned long long)misc[0]);
     }
   }
+  if (only) {
+    // next marked system: this one's shared memory (and, in a cluster, the
+    // root slots the peers push into) must be done with everywhere first
+    __syncthreads();
+    if (csize > 1) {
+      if (warp != 0) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // pairs the arrive above
+      asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // "started" for the next one
+      ph ^= 1u;
+    }
+  }
+  }  // marked systems of this round
+  }  // systems of this cluster
 }
 
 // ----------------------------------------------------------------------------
@@ -403,7 +433,7 @@ template <int K, int M, int T, bool VEC, class Lay, bool SP = false>
 static int launch(const double *c2, const double *c1, const double *e, const double *f1,
                   const double *f2, const double *b, double *x, int32_t *st, int32_t *ix,
                   int64_t *nz, int64_t batch, int64_t n, Lay lay, cudaStream_t stream,
-                  Outer outer = kNoOuter, const int32_t *only = nullptr) {
+                  Outer outer = kNoOuter, const int32_t *only = nullptr, int fs = 1) {
   constexpr int rows = M * T;
   const int csize = (int)((n + rows - 1) / rows);
   if (csize > 8) {
@@ -423,7 +453,10 @@ static int launch(const double *c2, const double *c1, const double *e, const dou
     if (ix) cudaMemsetAsync(ix, 0xff, sizeof(int32_t) * (size_t)batch, stream);  // -1
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(batch * csize));
+  // retry pass: a few clusters per SM walk the batch (launching batch * csize
+  // CTAs that mostly exit at once cost 42 us on config 2)
+  const int64_t nclus = only ? (batch < 2 * 148 ? batch : 2 * 148) : batch;
+  cfg.gridDim = dim3((unsigned)(nclus * csize));
   cfg.blockDim = dim3(T);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -435,7 +468,7 @@ static int launch(const double *c2, const double *c1, const double *e, const dou
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t err = cudaLaunchKernelEx(&cfg, kern, c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n,
-                                       lay, csize, outer, only);
+                                       lay, csize, outer, only, fs);
   if (err != cudaSuccess) {
     bxh::set_error("partitioned solver launch: %s", cudaGetErrorString(err));
     return BX_ERR_CUDA;
@@ -459,7 +492,7 @@ template <int K, bool VEC, class Lay>
 static int dispatch2(const double *c2, const double *c1, const double *e, const double *f1,
                      const double *f2, const double *b, double *x, int32_t *st, int32_t *ix,
                      int64_t *nz, int64_t batch, int64_t n, Lay lay, cudaStream_t stream,
-                     const int32_t *only) {
+                     const int32_t *only, int fs) {
   // rows per CTA = M*T; small systems use small CTAs (many CTAs per SM).
   // BX_PART_CFG (developer knob, benchmarking only) forces one configuration.
   static int forced = -2;
@@ -468,19 +501,19 @@ static int dispatch2(const double *c2, const double *c1, const double *e, const 
     forced = env ? atoi(env) : -1;
   }
   switch (forced) {
-    case 0: return launch<K, 8, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
-    case 1: return launch<K, 8, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
-    case 2: return launch<K, 8, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
-    case 3: return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
-    case 4: return launch<K, 16, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
-    case 5: return launch<K, 32, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
-    case 6: return launch<K, 16, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
+    case 0: return launch<K, 8, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only, fs);
+    case 1: return launch<K, 8, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only, fs);
+    case 2: return launch<K, 8, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only, fs);
+    case 3: return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only, fs);
+    case 4: return launch<K, 16, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only, fs);
+    case 5: return launch<K, 32, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only, fs);
+    case 6: return launch<K, 16, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only, fs);
     default: break;
   }
-  if (n <= 256) return launch<K, 8, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
-  if (n <= 512) return launch<K, 8, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
-  if (use_1k_ctas(n)) return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
-  return launch<K, 16, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only);
+  if (n <= 256) return launch<K, 8, 32, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only, fs);
+  if (n <= 512) return launch<K, 8, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only, fs);
+  if (use_1k_ctas(n)) return launch<K, 16, 64, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only, fs);
+  return launch<K, 16, 128, VEC, Lay>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, kNoOuter, only, fs);
 }
 
 // sparse +-2 diagonals (MNPDM): default shapes only, K = 2
@@ -549,11 +582,11 @@ template <int K, class Lay>
 static int dispatch(const double *c2, const double *c1, const double *e, const double *f1,
                     const double *f2, const double *b, double *x, int32_t *st, int32_t *ix,
                     int64_t *nz, int64_t batch, int64_t n, Lay lay, cudaStream_t stream,
-                    bool vec_ok, const int32_t *only = nullptr) {
+                    bool vec_ok, const int32_t *only = nullptr, int fs = 1) {
   vec_ok = vec_ok && aligned32(c2) && aligned32(c1) && aligned32(e) && aligned32(f1) &&
            aligned32(f2) && aligned32(b) && aligned32(x);
-  if (vec_ok) return dispatch2<K, true>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, only);
-  return dispatch2<K, false>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, only);
+  if (vec_ok) return dispatch2<K, true>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, only, fs);
+  return dispatch2<K, false>(c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n, lay, stream, only, fs);
 }
 
 }  // namespace part
@@ -574,23 +607,26 @@ static bool seg_enabled() {
 
 static size_t flag_bytes(int64_t batch) { return ((size_t)batch * 8 * 4 + 255) / 256 * 256; }
 size_t part_workspace_bytes(int bandwidth, int64_t batch, int64_t n) {
-  return 2 * flag_bytes(batch) + 8 * fixup_scratch_doubles(bandwidth == 1 ? 0 : 1, n);
+  return 3 * flag_bytes(batch) + 8 * fixup_scratch_doubles(bandwidth == 1 ? 0 : 1, n);
 }
 
-// workspace: flags [batch][8] | nz parts [batch][8] | re-solve scratch
-static void carve(double *ws, int64_t batch, int32_t *&flags, int32_t *&nzpart, double *&scratch) {
+// workspace: flags [batch][8] | nz parts [batch][8] | retry marks [batch][8] |
+// re-solve scratch
+static void carve(double *ws, int64_t batch, int32_t *&flags, int32_t *&nzpart, int32_t *&retry,
+                  double *&scratch) {
   char *p = reinterpret_cast<char *>(ws);
   flags = reinterpret_cast<int32_t *>(p);
   nzpart = reinterpret_cast<int32_t *>(p + flag_bytes(batch));
-  scratch = reinterpret_cast<double *>(p + 2 * flag_bytes(batch));
+  retry = reinterpret_cast<int32_t *>(p + 2 * flag_bytes(batch));
+  scratch = reinterpret_cast<double *>(p + 3 * flag_bytes(batch));
 }
 
 int ntdm_part(const double *d, const double *e, const double *f, const double *b, double *x,
               double *ws, int32_t *st, int32_t *ix, int64_t batch, int64_t n, int64_t ld, int layout,
               cudaStream_t stream) {
-  int32_t *flags, *nzpart;
+  int32_t *flags, *nzpart, *retry;
   double *scratch;
-  carve(ws, batch, flags, nzpart, scratch);
+  carve(ws, batch, flags, nzpart, retry, scratch);
   const double *ptrs[] = {d, e, f, b, x};
   int rc = BX_ERR_UNSUPPORTED, fs = 1;
   if (seg_enabled() && seg_applicable(ptrs, 5, n, ld, layout))
@@ -600,17 +636,18 @@ int ntdm_part(const double *d, const double *e, const double *f, const double *b
     // first pass: interface iteration; the tree then solves only what it marked
     const int32_t *only = nullptr;
     if (halo_enabled()) {
-      rc = halo_solve(1, nullptr, d, e, f, nullptr, b, x, flags, nullptr, batch, n, ld, layout,
-                      stream, nullptr, nullptr, nullptr, 0);
-      if (rc == BX_OK) only = flags + batch;
+      rc = halo_solve(1, nullptr, d, e, f, nullptr, b, x, flags, retry, nullptr, batch, n, ld,
+                      layout, stream, nullptr, nullptr, nullptr, 0, &fs);
+      if (rc == BX_OK) only = retry;
       else if (rc != BX_ERR_UNSUPPORTED) return rc;
+      else fs = 1;
     }
     if (layout == BX_LAYOUT_SYSTEM_MAJOR)
       rc = part::dispatch<1>(nullptr, d, e, f, nullptr, b, x, flags, nullptr, nullptr, batch, n,
-                             SystemMajor{ld}, stream, ld % 4 == 0, only);
+                             SystemMajor{ld}, stream, ld % 4 == 0, only, fs);
     else
       rc = part::dispatch<1>(nullptr, d, e, f, nullptr, b, x, flags, nullptr, nullptr, batch, n,
-                             Interleaved{ld}, stream, false, only);
+                             Interleaved{ld}, stream, false, only, fs);
   }
   if (rc != BX_OK) return rc;
   direct_fixup(0, nullptr, d, e, f, nullptr, b, x, scratch, flags, fs, nullptr, st, ix, nullptr,
@@ -621,37 +658,39 @@ int ntdm_part(const double *d, const double *e, const double *f, const double *b
 int penta_part(bool mod, const double *c, const double *d, const double *e, const double *f,
                const double *g, const double *b, double *x, double *ws, int32_t *st, int32_t *ix,
                int64_t *nz, int64_t batch, int64_t n, int64_t ld, int layout, cudaStream_t stream) {
-  int32_t *flags, *nzpart;
+  int32_t *flags, *nzpart, *retry;
   double *scratch;
-  carve(ws, batch, flags, nzpart, scratch);
+  carve(ws, batch, flags, nzpart, retry, scratch);
   const double *ptrs[] = {c, d, e, f, g, b, x};
   int rc = BX_ERR_UNSUPPORTED, fs = 1;
-  bool seg = false;
+  bool seg = false, halo = false;
   if (seg_enabled() && seg_applicable(ptrs, 7, n, ld, layout)) {
     rc = seg_solve(2, c, d, e, f, g, b, x, flags, nz ? nzpart : nullptr, batch, n, ld, stream, &fs);
     seg = rc != BX_ERR_UNSUPPORTED;
   }
   if (!seg) {
     fs = 1;
-    // first pass: interface iteration (it also counts nz); the tree then
-    // solves only the systems it marked
+    // first pass: interface iteration (it also counts nz, per CTA); the tree
+    // then solves only the systems it marked
     const int32_t *only = nullptr;
     if (halo_enabled()) {
-      rc = halo_solve(2, c, d, e, f, g, b, x, flags, nz, batch, n, ld, layout, stream, nullptr,
-                      nullptr, nullptr, 0);
-      if (rc == BX_OK) only = flags + batch;
+      rc = halo_solve(2, c, d, e, f, g, b, x, flags, retry, nz ? nzpart : nullptr, batch, n, ld,
+                      layout, stream, nullptr, nullptr, nullptr, 0, &fs);
+      if (rc == BX_OK) only = retry;
       else if (rc != BX_ERR_UNSUPPORTED) return rc;
+      else fs = 1;
     }
+    halo = only != nullptr;
     int64_t *tnz = only ? nullptr : nz;
     if (layout == BX_LAYOUT_SYSTEM_MAJOR)
       rc = part::dispatch<2>(c, d, e, f, g, b, x, flags, nullptr, tnz, batch, n, SystemMajor{ld},
-                             stream, ld % 4 == 0, only);
+                             stream, ld % 4 == 0, only, fs);
     else
       rc = part::dispatch<2>(c, d, e, f, g, b, x, flags, nullptr, tnz, batch, n, Interleaved{ld},
-                             stream, false, only);
+                             stream, false, only, fs);
   }
   if (rc != BX_OK) return rc;
-  direct_fixup(mod ? 2 : 1, c, d, e, f, g, b, x, scratch, flags, fs, seg && nz ? nzpart : nullptr,
+  direct_fixup(mod ? 2 : 1, c, d, e, f, g, b, x, scratch, flags, fs, (seg || halo) && nz ? nzpart : nullptr,
                st, ix, nz, batch, n, ld, layout, stream);
   return bxh::check_launch("partitioned solver re-solve");
 }

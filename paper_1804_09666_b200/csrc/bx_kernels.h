@@ -36,15 +36,16 @@ int seg_solve(int K, const double *c2, const double *c1, const double *e, const 
               int64_t batch, int64_t n, int64_t ld, cudaStream_t stream, int *csize);
 
 // bx_direct_halo.cu: interface-iteration first pass of the partitioned path.
-// flags[batch] | retry[batch] contiguous int32 words; systems whose interface
-// coupling is too strong for the fixed sweep count get retry[s] = 1 and are
-// solved again by the two-port tree kernel (bx_direct_part.cu)
+// flags / retry / nzpart: [batch][*csize] int32 words (one per CTA of a
+// system's cluster).  Systems whose interface coupling is too strong for the
+// fixed sweep count get a nonzero retry word and are solved again by the
+// two-port tree kernel (bx_direct_part.cu)
 bool halo_enabled();
 int halo_solve(int K, const double *c2, const double *c1, const double *e, const double *f1,
-               const double *f2, const double *b, double *x, int32_t *flags, int64_t *nz,
-               int64_t batch, int64_t n, int64_t ld, int layout, cudaStream_t stream,
-               const int32_t *outer_rows, const double *outer_sub2, const double *outer_sup2,
-               int64_t outer_k);
+               const double *f2, const double *b, double *x, int32_t *flags, int32_t *retry,
+               int32_t *nzpart, int64_t batch, int64_t n, int64_t ld, int layout,
+               cudaStream_t stream, const int32_t *outer_rows, const double *outer_sub2,
+               const double *outer_sup2, int64_t outer_k, int *csize);
 
 // bx_band_ops.cu (reference order, bit-exact building blocks)
 void band_matvec(int bw, int64_t m, const double *c, const double *d, const double *e,

@@ -18,6 +18,11 @@
 #ifndef BX_PART_LA
 #define BX_PART_LA 1  // input groups in flight ahead of the elimination (measured: 1 > 2 > 3)
 #endif
+#ifndef BX_P3_UNROLL
+#define BX_P3_UNROLL 1  // row groups of phase 3 unrolled together
+#endif
+#define BX_PRAGMA_(x) _Pragma(#x)
+#define BX_UNROLL(n) BX_PRAGMA_(unroll n)
 #ifndef BX_TR
 #define BX_TR(slot) \
   do {              \
@@ -303,7 +308,7 @@ struct Chunk {
                                                  const Vec<K> &R) {
     auto st = [&](int q, int j) -> double { return state[(q * M + j) * T + t]; };
   // ---------------- phase 3: x_j = d - W.L - V.R -----------------------------
-#pragma unroll 1
+BX_UNROLL(BX_P3_UNROLL)
   for (int g = 0; g < M / G; ++g) {
     double xv[G];
 #pragma unroll

@@ -20,7 +20,7 @@ def run_one(k, n, batch, steps=10):
     x = torch.empty((batch, n), dtype=torch.float64, device=dev)
     st = torch.empty(batch, dtype=torch.int32, device=dev)
     ix = torch.empty(batch, dtype=torch.int32, device=dev)
-    ws = workspace(1 << 20, dev)
+    ws = workspace(L.bx_workspace_bytes(0 if k == 1 else 1, batch, n, 1, 1), dev)
     s = torch.cuda.current_stream().cuda_stream
 
     def go():
