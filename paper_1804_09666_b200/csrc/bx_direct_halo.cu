@@ -142,6 +142,9 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
             double *__restrict__ xp, int32_t *flags, int32_t *retry, int32_t *nzpart,
             int64_t batch, int64_t n, Lay lay, int csize, Outer outer, double rho_max,
             int pf_ahead) {
+  // the retry pass and the re-solve kernel behind this one may become
+  // resident as this grid drains (they wait for its completion themselves)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   using SM = HaloSmem<K, M, T>;
   using CH = Chunk<K, M, T, VEC, SP, Lay>;
   constexpr int H = kH, NP = SM::NP, NW = SM::NW;

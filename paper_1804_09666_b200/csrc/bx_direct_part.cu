@@ -105,6 +105,10 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   // (bx_direct_halo.cu) -- a small persistent grid whose clusters walk the
   // batch and solve just the systems it marked (only[s * fs + r] != 0 for some
   // r < fs), OR-ing flags into status[s * fs]; fs = 1 otherwise
+  // let the re-solve kernel behind this one become resident early; the retry
+  // pass itself is such a dependent of the interface-iteration kernel
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (only) asm volatile("griddepcontrol.wait;" ::: "memory");
   using SM = Smem<K, M, T>;
   constexpr int NW = SM::NW;
   static_assert(T % 32 == 0 && (NW & (NW - 1)) == 0, "T must be 32 * power of two");
@@ -460,13 +464,15 @@ static int launch(const double *c2, const double *c1, const double *e, const dou
   cfg.blockDim = dim3(T);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = csize;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // retry pass only
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = only ? 2 : 1;
   cudaError_t err = cudaLaunchKernelEx(&cfg, kern, c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n,
                                        lay, csize, outer, only, fs);
   if (err != cudaSuccess) {

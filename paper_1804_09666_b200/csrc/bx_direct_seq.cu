@@ -142,7 +142,10 @@ ntdm_seq_kernel(const double *__restrict__ d, const double *__restrict__ e,
     return;
   }
   // re-solve mode: one warp per scratch slot (CTA), lanes check 32 systems'
-  // flags at a time; flagged ones are solved one after another by their lane
+  // flags at a time; flagged ones are solved one after another by their lane.
+  // Launched with programmatic stream serialization: resident early, held
+  // here until the partitioned kernels before it have completed.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int slot = blockIdx.x, lane = threadIdx.x;
   for (int64_t s0 = (int64_t)slot * 32; s0 < batch; s0 += slots * 32) {
     const int64_t s = s0 + lane;
@@ -309,6 +312,7 @@ penta_seq_kernel(const double *__restrict__ c, const double *__restrict__ d,
                       Scratch{batch}, t);
     return;
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (see ntdm_seq_kernel)
   const int slot = blockIdx.x, lane = threadIdx.x;
   for (int64_t s0 = (int64_t)slot * 32; s0 < batch; s0 += slots * 32) {
     const int64_t s = s0 + lane;
@@ -421,32 +425,53 @@ void penta_seq(bool mod, const double *c, const double *d, const double *e, cons
 constexpr int64_t kFixSlots = 128;
 size_t fixup_scratch_doubles(int kind, int64_t n) { return (size_t)(kind == 0 ? 1 : 2) * kFixSlots * n; }
 
+// launch on `stream` with programmatic stream serialization (the kernel
+// calls griddepcontrol.wait before it touches its predecessors' results)
+template <class... KA, class... A>
+static void launch_dependent(void (*kern)(KA...), dim3 grid, dim3 block, cudaStream_t stream,
+                             A... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KA>(args)...);
+}
+
 void direct_fixup(int kind, const double *c, const double *d, const double *e, const double *f,
                   const double *g, const double *b, double *x, double *scratch,
                   const int32_t *flags, int fs, const int32_t *nzpart, int32_t *st, int32_t *ix,
                   int64_t *nz, int64_t batch, int64_t n, int64_t ld, int layout,
                   cudaStream_t stream) {
-  const dim3 grid((unsigned)kFixSlots);  // one warp per scratch slot
+  const dim3 grid((unsigned)kFixSlots), block(kSeqThreads);  // one warp per scratch slot
   if (kind == 0) {
     if (layout == BX_LAYOUT_INTERLEAVED)
-      ntdm_seq_kernel<<<grid, kSeqThreads, 0, stream>>>(d, e, f, b, x, scratch, st, ix, batch, n,
-                                                       Interleaved{ld}, flags, kFixSlots, fs);
+      launch_dependent(ntdm_seq_kernel<Interleaved>, grid, block, stream, d, e, f, b, x, scratch, st,
+                       ix, batch, n, Interleaved{ld}, flags, kFixSlots, fs);
     else
-      ntdm_seq_kernel<<<grid, kSeqThreads, 0, stream>>>(d, e, f, b, x, scratch, st, ix, batch, n,
-                                                       SystemMajor{ld}, flags, kFixSlots, fs);
+      launch_dependent(ntdm_seq_kernel<SystemMajor>, grid, block, stream, d, e, f, b, x, scratch, st,
+                       ix, batch, n, SystemMajor{ld}, flags, kFixSlots, fs);
     return;
   }
   double *phiw = scratch + kFixSlots * n;
   if (layout == BX_LAYOUT_INTERLEAVED) {
     if (kind == 2)
-      penta_seq_kernel<true><<<grid, kSeqThreads, 0, stream>>>(c, d, e, f, g, b, x, scratch, phiw, st, ix, nz, batch, n, Interleaved{ld}, flags, kFixSlots, fs, nzpart);
+      launch_dependent(penta_seq_kernel<true, Interleaved>, grid, block, stream, c, d, e, f, g, b, x,
+                       scratch, phiw, st, ix, nz, batch, n, Interleaved{ld}, flags, kFixSlots, fs, nzpart);
     else
-      penta_seq_kernel<false><<<grid, kSeqThreads, 0, stream>>>(c, d, e, f, g, b, x, scratch, phiw, st, ix, nz, batch, n, Interleaved{ld}, flags, kFixSlots, fs, nzpart);
+      launch_dependent(penta_seq_kernel<false, Interleaved>, grid, block, stream, c, d, e, f, g, b, x,
+                       scratch, phiw, st, ix, nz, batch, n, Interleaved{ld}, flags, kFixSlots, fs, nzpart);
   } else {
     if (kind == 2)
-      penta_seq_kernel<true><<<grid, kSeqThreads, 0, stream>>>(c, d, e, f, g, b, x, scratch, phiw, st, ix, nz, batch, n, SystemMajor{ld}, flags, kFixSlots, fs, nzpart);
+      launch_dependent(penta_seq_kernel<true, SystemMajor>, grid, block, stream, c, d, e, f, g, b, x,
+                       scratch, phiw, st, ix, nz, batch, n, SystemMajor{ld}, flags, kFixSlots, fs, nzpart);
     else
-      penta_seq_kernel<false><<<grid, kSeqThreads, 0, stream>>>(c, d, e, f, g, b, x, scratch, phiw, st, ix, nz, batch, n, SystemMajor{ld}, flags, kFixSlots, fs, nzpart);
+      launch_dependent(penta_seq_kernel<false, SystemMajor>, grid, block, stream, c, d, e, f, g, b, x,
+                       scratch, phiw, st, ix, nz, batch, n, SystemMajor{ld}, flags, kFixSlots, fs, nzpart);
   }
 }
 

@@ -19,7 +19,7 @@
 #define BX_PART_LA 1  // input groups in flight ahead of the elimination (measured: 1 > 2 > 3)
 #endif
 #ifndef BX_P3_UNROLL
-#define BX_P3_UNROLL 1  // row groups of phase 3 unrolled together
+#define BX_P3_UNROLL 2  // row groups of phase 3 unrolled together (measured: 2 >= 4 > 1)
 #endif
 #define BX_PRAGMA_(x) _Pragma(#x)
 #define BX_UNROLL(n) BX_PRAGMA_(unroll n)
