@@ -121,7 +121,8 @@ __device__ __forceinline__ Port<K> zero_port() {
 // chunks -kH..-1 of the left neighbour, side 1: chunks T..T+kH-1 of the right
 // one) | per warp: itU, itV [kChain + 4][K] interface iterates (slot p + 1
 // for position p of the warp's chain; slots 0 and kChain + 1 stay zero, slot
-// kChain + 2 is the dump of lanes without a second interface) | misc
+// kChain + 2 is the dump of lanes without a second interface; the F sides
+// published across warp boundaries are overlaid on these arrays) | misc
 constexpr int kChain = 32 + 2 * kH - 1;  // left halo kH | 32 primaries | right halo kH - 1
 template <int K, int M, int T>
 struct HaloSmem {
@@ -131,11 +132,22 @@ struct HaloSmem {
   static constexpr int kState = Q * M * T;
   static constexpr int kHalo = 2 * kH * NP;
   static constexpr int kIt = (kChain + 4) * K;  // one array of one warp (+1: the dump slot's right neighbour)
-  static constexpr size_t bytes = sizeof(double) * (size_t)(kState + kHalo + 2 * NW * kIt + 8);
+  // F sides published across every warp boundary inside the CTA: the kH-1
+  // last chunks of the warp before it, the kH first chunks of the warp after
+  static constexpr int kPub = (NW - 1) * (2 * kH - 1) * (NP / 2);
+  static_assert(kPub <= 2 * NW * kIt, "pubF is overlaid on the iterate arrays");
+  // (K=2, M=16, T=64: 45008 B -- 5 CTAs/SM need <= 44 KB each)
+  static constexpr size_t bytes = sizeof(double) * (size_t)(kState + kHalo + 2 * NW * kIt + 2);
 };
 
+// Registers: at most 168 per thread, i.e. 12 warps per SM -- each SM sub-
+// partition owns 16 K registers, so a warp of 169..255-register threads fits
+// only twice per sub-partition (8 warps per SM = 4 of the 64-thread CTAs,
+// measured), one of <= 168 three times.  K = 1 gets no hint: it needs 96
+// (with a minimum of 6 blocks the compiler spent 154: 0.48 -> 0.51 ms on
+// config 5; capped at 102 for 10 blocks it spilled: 0.60 ms).
 template <int K, int M, int T, bool VEC, bool SP, class Lay>
-__global__ void __launch_bounds__(T)
+__global__ void __launch_bounds__(T, K == 2 ? 384 / T : 1)
 halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
             const double *__restrict__ ep, const double *__restrict__ f1p,
             const double *__restrict__ f2p, const double *__restrict__ bp,
@@ -154,6 +166,7 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   double *halo = smem + SM::kState;
   double *itU = halo + SM::kHalo + (threadIdx.x >> 5) * 2 * SM::kIt;  // this warp's arrays
   double *itV = itU + SM::kIt;
+  double *pubF = halo + SM::kHalo;  // overlaid on the iterate arrays (dead until the sweeps)
   int *misc = reinterpret_cast<int *>(halo + SM::kHalo + 2 * NW * SM::kIt);
   // misc: [0] nz counter (int), [2..3] halo mbarrier (8-byte slot)
   uint64_t *cbar = reinterpret_cast<uint64_t *>(misc + 2);
@@ -199,9 +212,20 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   BX_TR(0);
   int32_t bad;
   int nzc;
-  CH::down(state, t, s, base, n, lay, c2p, c1p, ep, f1p, f2p, bp, outer, bad, nzc);
+  TwoPort<K> port;  // this chunk's two-port, out of the down sweep (top tracking)
+  CH::template down<true>(state, t, s, base, n, lay, c2p, c1p, ep, f1p, f2p, bp, outer, bad, nzc, &port);
   BX_TR(1);
-  CH::up(state, t);
+  const int w0 = t - lane;  // the warp's first chunk
+  if (NW > 1) {  // F sides the neighbouring warps will need
+    int slot = -1;
+    if (warp < NW - 1 && lane > 32 - H) slot = warp * (2 * H - 1) + (lane - (32 - H + 1));
+    if (warp > 0 && lane < H) slot = (warp - 1) * (2 * H - 1) + (H - 1) + lane;
+    if (slot >= 0) {
+      const double *v = reinterpret_cast<const double *>(&port.F);
+#pragma unroll
+      for (int c = 0; c < NP / 2; ++c) pubF[slot * (NP / 2) + c] = v[c];
+    }
+  }
   BX_TR(2);
 
   // ---------------- halo exchange ---------------------------------------------
@@ -218,8 +242,7 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
                    : "memory");
     const bool toL = hasL && t < H, toR = hasR && t >= T - H;
     if (toL || toR) {
-      const TwoPort<K> own = CH::port(state, t);
-      const double *v = reinterpret_cast<const double *>(&own);
+      const double *v = reinterpret_cast<const double *>(&port);
       const int peer = toL ? crank - 1 : crank + 1;
       const double *slot = halo + ((toL ? 1 : 0) * H + (toL ? t : t - (T - H))) * NP;
       unsigned ra, rb;
@@ -232,7 +255,7 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
                      : "memory");
     }
   }
-  __syncthreads();  // every chunk's state rows are visible
+  __syncthreads();  // every chunk's state rows and the published F sides are visible
 
   // ---------------- interfaces --------------------------------------------------
   // Every warp iterates its own chain of interfaces without CTA barriers:
@@ -251,11 +274,21 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     for (int c = 0; c < NP / 2; ++c) v[c] = src[c];
     return p;
   };
-  auto chunk_side = [&](int c, bool isE) -> Port<K> {  // chunk c of this CTA's numbering
-    if (c >= 0 && c < T) return CH::port_side(state, c, isE ? M - K : 0);
-    if (c < 0 && hasL) return halo_side(0, c + H, isE);
-    if (c >= T && hasR) return halo_side(1, c - T, isE);
-    return zero_port<K>();
+  auto F_other = [&](int c) -> Port<K> {  // F side of chunk c outside this warp
+    if (c < 0) return hasL ? halo_side(0, c + H, false) : zero_port<K>();
+    if (c >= T) return hasR ? halo_side(1, c - T, false) : zero_port<K>();
+    const int slot = c < w0 ? (warp - 1) * (2 * H - 1) + (c - (w0 - (H - 1)))
+                            : warp * (2 * H - 1) + (H - 1) + (c - (w0 + 32));
+    Port<K> p;
+    double *v = reinterpret_cast<double *>(&p);
+#pragma unroll
+    for (int q = 0; q < NP / 2; ++q) v[q] = pubF[slot * (NP / 2) + q];
+    return p;
+  };
+  auto E_other = [&](int c) -> Port<K> {  // E side of chunk c outside this warp
+    if (c < 0) return hasL ? halo_side(0, c + H, true) : zero_port<K>();
+    if (c >= T) return hasR ? halo_side(1, c - T, true) : zero_port<K>();
+    return CH::port_E_state(state, c);
   };
   bool ok = true;
   MergeInfo<K> mi, mi2;
@@ -264,8 +297,18 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
 #pragma unroll
     for (int c = 0; c < NP; ++c) z[c] = 0.0;
   }
+  Port<K> Fnext, F0;  // F of the next lane's chunk, of the warp's first chunk
+  {
+    const double *src = reinterpret_cast<const double *>(&port.F);
+    double *d1 = reinterpret_cast<double *>(&Fnext), *d0 = reinterpret_cast<double *>(&F0);
+#pragma unroll
+    for (int c = 0; c < NP / 2; ++c) {
+      d1[c] = __shfl_down_sync(0xffffffffu, src[c], 1);
+      d0[c] = __shfl_sync(0xffffffffu, src[c], 0);
+    }
+  }
   const bool prim_early = t < T - 1 || !hasR;  // needs nothing from the halo
-  if (prim_early) ok &= iface<K>(chunk_side(t, true), chunk_side(t + 1, false), mi);
+  if (prim_early) ok &= iface<K>(port.E, lane < 31 ? Fnext : F_other(t + 1), mi);
   BX_TR(3);
   if (hasL || hasR) {
     asm volatile(
@@ -276,16 +319,15 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
         : "memory");
   }
   BX_TR(4);
-  if (!prim_early) ok &= iface<K>(chunk_side(t, true), chunk_side(t + 1, false), mi);
-  const int w0 = t - lane;  // the warp's first chunk
-  int pos2 = kChain + 1;    // dump slot
+  if (!prim_early) ok &= iface<K>(port.E, F_other(t + 1), mi);
+  int pos2 = kChain + 1;  // dump slot
   if (lane < H) {
     const int c = w0 - H + lane;
-    ok &= iface<K>(chunk_side(c, true), chunk_side(c + 1, false), mi2);
+    ok &= iface<K>(E_other(c), lane < H - 1 ? F_other(c + 1) : F0, mi2);
     pos2 = lane;
   } else if (lane >= 32 - H && lane < 31) {
     const int c = w0 + lane + H;
-    ok &= iface<K>(chunk_side(c, true), chunk_side(c + 1, false), mi2);
+    ok &= iface<K>(E_other(c), F_other(c + 1), mi2);
     pos2 = lane + 2 * H;
   }
   double rho = coupling<K>(mi);
@@ -293,6 +335,8 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     const double r2 = coupling<K>(mi2);
     rho = (r2 > rho || r2 != r2) ? r2 : rho;
   }
+
+  if (NW > 1) __syncthreads();  // pubF (overlaid on the iterate arrays) has been read
 
   // ---------------- block-Jacobi sweeps over the warp's chain -------------------
   auto ldv = [&](const double *a, int slot) -> Vec<K> {
@@ -333,7 +377,7 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   BX_TR(5);
 
   // ---------------- phase 3 -------------------------------------------------------
-  CH::write_x(state, t, s, base, n, lay, xp, L, R);
+  CH::write_x_backsub(state, t, s, base, n, lay, xp, L, R);
   BX_TR(6);
 
   // ---------------- flags / counters ----------------------------------------------

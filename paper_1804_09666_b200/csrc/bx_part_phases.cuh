@@ -47,13 +47,32 @@ struct Chunk {
 
   // s: system, base: first row of this thread's chunk; bad: first zero /
   // non-finite chunk-local pivot (-1: none); nzc: rows with sub2 != 0
+  //
+  // TT ("top tracking"): the chunk's first K unknowns are carried along as
+  // affine functions of L and the K newest unknowns,
+  //     x_a = al_a - om_a . L - P_a x_{j+1} - Q_a x_{j+2}      (after row j),
+  // advanced with every normalised row (substitute x_j:  al -= P y_j,
+  // om -= P W_j, (P, Q) <- (Q - P p_j, -P q_j); started from x_a itself), so
+  // that after the last row they are affine in (L, R): the chunk's two-port
+  // comes out of the down sweep alone (no up sweep, no second pass over the
+  // state) and phase 3 is a back-substitution from R (write_x_backsub).
+  template <bool TT = false>
   static __device__ __forceinline__ void down(
       double *__restrict__ state, const int t, const int64_t s, const int64_t base, const int64_t n,
       const Lay lay, const double *__restrict__ c2p, const double *__restrict__ c1p,
       const double *__restrict__ ep, const double *__restrict__ f1p,
       const double *__restrict__ f2p, const double *__restrict__ bp, const Outer outer,
-      int32_t &bad, int &nzc) {
+      int32_t &bad, int &nzc, TwoPort<K> *port = nullptr) {
     auto st = [&](int q, int j) -> double & { return state[(q * M + j) * T + t]; };
+    double tal[K], tom[K][K], tP[K], tQ[K];
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      tal[a] = 0.0;
+      tP[a] = a == 0 ? -1.0 : 0.0;
+      tQ[a] = a == 1 ? -1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) tom[a][k] = 0.0;
+    }
   // ---------------- phase 1: downward elimination --------------------------
   // Gaussian elimination of the chunk against its own normalised rows:
   // x_{j-2} is eliminated with row j-2, then x_{j-1} with row j-1, and the
@@ -225,10 +244,69 @@ struct Chunk {
       W2[k] = W1[k];
       W1[k] = w;
     }
+    if (TT) {
+#pragma unroll
+      for (int a = 0; a < K; ++a) {
+        const double P = tP[a];
+        tal[a] = fma(-P, yn, tal[a]);
+#pragma unroll
+        for (int k = 0; k < K; ++k) tom[a][k] = fma(-P, W1[k], tom[a][k]);  // W1 = this row's W
+        tP[a] = K == 2 ? fma(-P, pn, tQ[a]) : -P * pn;
+        tQ[a] = -P * qn;
+      }
+    }
     f2 = f1; g2 = g1; y2 = y1;
     f1 = pn; g1 = qn; y1 = yn;
     }
   }
+  if (TT) {
+    // F: x_a = al - om.L - (P, Q).R ; E: the last K normalised rows
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      port->F.g.v[a] = tal[a];
+#pragma unroll
+      for (int k = 0; k < K; ++k) port->F.A.m[a][k] = -tom[a][k];
+      port->F.B.m[a][0] = -tP[a];
+      if (K == 2) port->F.B.m[a][K - 1] = -tQ[a];
+    }
+    port->E = port_E_rows(f2, g2, y2, W2, f1, g1, y1, W1);
+  }
+  }
+
+  // E side of a two-port from the chunk's last normalised rows M-2 (p2, q2, y2,
+  // w2; K = 2 only) and M-1 (p1, q1, y1, w1):  x_{M-1} = y1 - w1.L - (p1, q1).R,
+  // x_{M-2} = y2 - w2.L - p2 x_{M-1} - q2 R_0
+  static __device__ __forceinline__ Port<K> port_E_rows(double p2, double q2, double y2,
+                                                        const double *w2, double p1, double q1,
+                                                        double y1, const double *w1) {
+    Port<K> E;
+    E.g.v[K - 1] = y1;
+#pragma unroll
+    for (int k = 0; k < K; ++k) E.A.m[K - 1][k] = -w1[k];
+    E.B.m[K - 1][0] = -p1;
+    if (K == 2) {
+      E.B.m[K - 1][K - 1] = -q1;
+      E.g.v[0] = fma(-p2, y1, y2);
+#pragma unroll
+      for (int k = 0; k < K; ++k) E.A.m[0][k] = -fma(-p2, w1[k], w2[k]);
+      E.B.m[0][0] = -fma(-p2, p1, q2);
+      E.B.m[0][K - 1] = p2 * q1;
+    }
+    return E;
+  }
+  // ... of chunk c, read from the state left by down<true> (any thread's rows)
+  static __device__ __forceinline__ Port<K> port_E_state(const double *__restrict__ state,
+                                                         const int c) {
+    auto at = [&](int q, int j) -> double { return state[(q * M + j) * T + c]; };
+    double w1[K], w2[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      w1[k] = at(K + 1 + k, M - 1);
+      w2[k] = K == 2 ? at(K + 1 + k, M - 2) : 0.0;
+    }
+    return port_E_rows(K == 2 ? at(0, M - 2) : 0.0, K == 2 ? at(1, M - 2) : 0.0,
+                       K == 2 ? at(K, M - 2) : 0.0, w2, at(0, M - 1), K == 2 ? at(1, M - 1) : 0.0,
+                       at(K, M - 1), w1);
   }
 
   static __device__ __forceinline__ void up(double *__restrict__ state, const int t) {
@@ -328,6 +406,41 @@ BX_UNROLL(BX_P3_UNROLL)
         if (i0 + u < n) xp[lay(i0 + u, s)] = xv[u];
     }
   }
+  }
+
+  // phase 3 after down<true>: back-substitution from R through the normalised
+  // rows,  x_j = y_j - W_j.L - p_j x_{j+1} - q_j x_{j+2}  (newest unknown last)
+  static __device__ __forceinline__ void write_x_backsub(const double *__restrict__ state,
+                                                         const int t, const int64_t s,
+                                                         const int64_t base, const int64_t n,
+                                                         const Lay lay, double *__restrict__ xp,
+                                                         const Vec<K> &L, const Vec<K> &R) {
+    auto st = [&](int q, int j) -> double { return state[(q * M + j) * T + t]; };
+    double X1 = R.v[0], X2 = K == 2 ? R.v[K - 1] : 0.0;
+BX_UNROLL(BX_P3_UNROLL)
+    for (int g = M / G - 1; g >= 0; --g) {
+      double xv[G];
+#pragma unroll
+      for (int u = G - 1; u >= 0; --u) {
+        const int j = g * G + u;
+        double v = st(K, j);
+#pragma unroll
+        for (int k = 0; k < K; ++k) v = fma(-st(K + 1 + k, j), L.v[k], v);
+        if (K == 2) v = fma(-st(1, j), X2, v);
+        v = fma(-st(0, j), X1, v);
+        xv[u] = v;
+        X2 = X1;
+        X1 = v;
+      }
+      const int64_t i0 = base + g * G;
+      if (VEC && i0 + G <= n) {
+        st4(xp + lay(i0, s), xv);
+      } else {
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+          if (i0 + u < n) xp[lay(i0 + u, s)] = xv[u];
+      }
+    }
   }
 };
 
