@@ -147,7 +147,7 @@ struct HaloSmem {
 // (with a minimum of 6 blocks the compiler spent 154: 0.48 -> 0.51 ms on
 // config 5; capped at 102 for 10 blocks it spilled: 0.60 ms).
 template <int K, int M, int T, bool VEC, bool SP, class Lay>
-__global__ void __launch_bounds__(T, K == 2 ? 384 / T : 1)
+__global__ void __launch_bounds__(T, K == 2 ? 384 / T : 0)
 halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
             const double *__restrict__ ep, const double *__restrict__ f1p,
             const double *__restrict__ f2p, const double *__restrict__ bp,
