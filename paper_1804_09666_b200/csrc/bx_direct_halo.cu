@@ -153,7 +153,7 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
             const double *__restrict__ f2p, const double *__restrict__ bp,
             double *__restrict__ xp, int32_t *flags, int32_t *retry, int32_t *nzpart,
             int64_t batch, int64_t n, Lay lay, int csize, Outer outer, double rho_max,
-            int pf_ahead) {
+            int pf_ahead, int32_t *index, int64_t *nz_out) {
   // the retry pass and the re-solve kernel behind this one may become
   // resident as this grid drains (they wait for its completion themselves)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -387,6 +387,33 @@ halo_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
   const bool slow = !(rho <= rho_max);
   const int64_t w = s * csize + crank;
   const bool rare = __syncthreads_or(bad >= 0 || slow);
+  if (retry == nullptr) {
+    // no workspace (sparse-outer entry): flags is the caller's status array,
+    // preset to OK / -1 / 0 by the launcher when csize > 1.  A system with any
+    // zero pivot or slow interface is handed to the tree pass, which then
+    // writes its final status / index (bx_direct_part.cu, mark mode).
+    if (csize == 1) {
+      if (t == 0) {
+        flags[s] = rare ? kRetryMark : BX_STATUS_OK;
+        if (index) index[s] = -1;
+      }
+    } else if (rare && t == 0) {
+      flags[s] = kRetryMark;
+    }
+    if (K == 2 && nz_out) {
+      nzc = __reduce_add_sync(0xffffffffu, nzc);
+      if (NW > 1) {
+        if (lane == 0) atomicAdd(&misc[0], nzc);
+        __syncthreads();
+        nzc = misc[0];
+      }
+      if (t == 0) {
+        if (csize == 1) nz_out[s] = nzc;
+        else atomicAdd(reinterpret_cast<unsigned long long *>(nz_out + s), (unsigned long long)nzc);
+      }
+    }
+    return;
+  }
   if (t == 0) {
     flags[w] = BX_STATUS_OK;
     retry[w] = 0;
@@ -431,7 +458,8 @@ template <int K, int M, int T, bool VEC, bool SP, class Lay>
 static int halo_launch(const double *c2, const double *c1, const double *e, const double *f1,
                        const double *f2, const double *b, double *x, int32_t *flags,
                        int32_t *retry, int32_t *nzpart, int64_t batch, int64_t n, Lay lay,
-                       cudaStream_t stream, Outer outer, int *csize_out) {
+                       cudaStream_t stream, Outer outer, int *csize_out, int32_t *index,
+                       int64_t *nz_out) {
   constexpr int rows = M * T;
   const int csize = (int)((n + rows - 1) / rows);
   if (csize > 8) return BX_ERR_UNSUPPORTED;  // (the tree kernel reports the limit)
@@ -446,6 +474,11 @@ static int halo_launch(const double *c2, const double *c1, const double *e, cons
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T, smem);
     fprintf(stderr, "halo_kernel<K=%d,M=%d,T=%d>: smem %zu B, %d CTAs/SM, csize %d\n", K, M, T, smem, nb, csize);
   }
+  if (!retry && csize > 1) {  // no-workspace mode: the caller's arrays carry the words
+    cudaMemsetAsync(flags, 0, sizeof(int32_t) * (size_t)batch, stream);  // BX_STATUS_OK
+    if (index) cudaMemsetAsync(index, 0xff, sizeof(int32_t) * (size_t)batch, stream);  // -1
+    if (nz_out) cudaMemsetAsync(nz_out, 0, sizeof(int64_t) * (size_t)batch, stream);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(batch * csize));
   cfg.blockDim = dim3(T);
@@ -459,7 +492,7 @@ static int halo_launch(const double *c2, const double *c1, const double *e, cons
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t err = cudaLaunchKernelEx(&cfg, kern, c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch,
-                                       n, lay, csize, outer, rho_max_default(), pf_ahead);
+                                       n, lay, csize, outer, rho_max_default(), pf_ahead, index, nz_out);
   if (err != cudaSuccess) {
     bxh::set_error("partitioned solver (interface iteration) launch: %s", cudaGetErrorString(err));
     return BX_ERR_CUDA;
@@ -471,25 +504,26 @@ template <int K, bool VEC, bool SP, class Lay>
 static int halo_shapes(const double *c2, const double *c1, const double *e, const double *f1,
                        const double *f2, const double *b, double *x, int32_t *flags,
                        int32_t *retry, int32_t *nzpart, int64_t batch, int64_t n, Lay lay,
-                       cudaStream_t stream, Outer o, int *cs) {
-  if (n <= 256) return halo_launch<K, 8, 32, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, lay, stream, o, cs);
-  if (n <= 512) return halo_launch<K, 8, 64, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, lay, stream, o, cs);
-  if (n <= 8192) return halo_launch<K, 16, 64, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, lay, stream, o, cs);
-  return halo_launch<K, 16, 128, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, lay, stream, o, cs);
+                       cudaStream_t stream, Outer o, int *cs, int32_t *ix, int64_t *nzo) {
+  if (n <= 256) return halo_launch<K, 8, 32, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, lay, stream, o, cs, ix, nzo);
+  if (n <= 512) return halo_launch<K, 8, 64, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, lay, stream, o, cs, ix, nzo);
+  if (n <= 8192) return halo_launch<K, 16, 64, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, lay, stream, o, cs, ix, nzo);
+  return halo_launch<K, 16, 128, VEC, SP, Lay>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, lay, stream, o, cs, ix, nzo);
 }
 
 template <int K, bool SP>
 static int halo_layouts(const double *c2, const double *c1, const double *e, const double *f1,
                         const double *f2, const double *b, double *x, int32_t *flags,
                         int32_t *retry, int32_t *nzpart, int64_t batch, int64_t n, int64_t ld,
-                        int layout, cudaStream_t stream, Outer o, int *cs) {
+                        int layout, cudaStream_t stream, Outer o, int *cs, int32_t *ix,
+                        int64_t *nzo) {
   auto a32 = [](const void *p) { return p == nullptr || ((uintptr_t)p & 31u) == 0; };
   if (layout == BX_LAYOUT_SYSTEM_MAJOR) {
     const bool vec = ld % 4 == 0 && a32(c2) && a32(c1) && a32(e) && a32(f1) && a32(f2) && a32(b) && a32(x);
-    if (vec) return halo_shapes<K, true, SP>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, SystemMajor{ld}, stream, o, cs);
-    return halo_shapes<K, false, SP>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, SystemMajor{ld}, stream, o, cs);
+    if (vec) return halo_shapes<K, true, SP>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, SystemMajor{ld}, stream, o, cs, ix, nzo);
+    return halo_shapes<K, false, SP>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, SystemMajor{ld}, stream, o, cs, ix, nzo);
   }
-  return halo_shapes<K, false, SP>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, Interleaved{ld}, stream, o, cs);
+  return halo_shapes<K, false, SP>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, Interleaved{ld}, stream, o, cs, ix, nzo);
 }
 
 }  // namespace part
@@ -506,20 +540,23 @@ bool halo_enabled() {
 // flags / retry / nzpart: [batch][*csize] int32 words, one per CTA of a
 // system's cluster (direct_fixup's fs = *csize convention).
 // outer_rows != nullptr: the +-2 diagonals come from the sparse lists (K = 2).
+// retry == nullptr: no workspace -- flags is the caller's status array, index /
+// nz are written here, marked systems carry kRetryMark (see halo_kernel).
 int halo_solve(int K, const double *c2, const double *c1, const double *e, const double *f1,
                const double *f2, const double *b, double *x, int32_t *flags, int32_t *retry,
                int32_t *nzpart, int64_t batch, int64_t n, int64_t ld, int layout,
                cudaStream_t stream, const int32_t *outer_rows, const double *outer_sub2,
-               const double *outer_sup2, int64_t outer_k, int *csize) {
+               const double *outer_sup2, int64_t outer_k, int *csize, int32_t *index,
+               int64_t *nz) {
   const part::Outer o{outer_rows, outer_sub2, outer_sup2, outer_k};
   if (K == 1)
     return part::halo_layouts<1, false>(nullptr, c1, e, f1, nullptr, b, x, flags, retry, nullptr,
-                                        batch, n, ld, layout, stream, o, csize);
-  if (outer_rows)
+                                        batch, n, ld, layout, stream, o, csize, index, nullptr);
+  if (outer_rows || outer_k == 0 && !c2)
     return part::halo_layouts<2, true>(nullptr, c1, e, f1, nullptr, b, x, flags, retry, nzpart,
-                                       batch, n, ld, layout, stream, o, csize);
+                                       batch, n, ld, layout, stream, o, csize, index, nz);
   return part::halo_layouts<2, false>(c2, c1, e, f1, f2, b, x, flags, retry, nzpart, batch, n, ld,
-                                      layout, stream, o, csize);
+                                      layout, stream, o, csize, index, nz);
 }
 
 }  // namespace bx

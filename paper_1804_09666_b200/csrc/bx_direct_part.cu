@@ -100,11 +100,14 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
             const double *__restrict__ f2p, const double *__restrict__ bp,
             double *__restrict__ xp, int32_t *status, int32_t *index, int64_t *nz_out,
             int64_t batch, int64_t n, Lay lay, int csize, Outer outer,
-            const int32_t *__restrict__ only, int fs) {
+            const int32_t *__restrict__ only, int fs, int mark) {
   // only != nullptr: retry pass after the interface-iteration kernel
   // (bx_direct_halo.cu) -- a small persistent grid whose clusters walk the
   // batch and solve just the systems it marked (only[s * fs + r] != 0 for some
-  // r < fs), OR-ing flags into status[s * fs]; fs = 1 otherwise
+  // r < fs), OR-ing flags into status[s * fs]; fs = 1 otherwise.  mark != 0
+  // (no workspace: the sparse-outer entry): `only` is the status array itself,
+  // a system is marked by status[s] == mark and leaves with its final status /
+  // index, exactly what this kernel writes without a first pass.
   // let the re-solve kernel behind this one become resident early; the retry
   // pass itself is such a dependent of the interface-iteration kernel
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -147,7 +150,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
     const int64_t sl = s0 + (int64_t)lane * nclus;
     bool marked = false;
     if (sl < batch)
-      for (int r = 0; r < fs; ++r) marked |= only[sl * fs + r] != 0;
+      for (int r = 0; r < fs; ++r) marked |= mark ? only[sl * fs + r] == mark : only[sl * fs + r] != 0;
     todo = __ballot_sync(0xffffffffu, marked);
   }
   while (todo) {
@@ -387,12 +390,15 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
       if (bad >= 0) atomicMin(&misc[1], bad);
       __syncthreads();
     }
-    if (t == 0 && (any_bad || !only)) {
+    if (t == 0 && (any_bad || !only || mark)) {
       if (status) status[s * fs] = any_bad ? BX_STATUS_ZERO_PIVOT : BX_STATUS_OK;
       if (index) index[s] = any_bad ? misc[1] : -1;
     }
   } else if (__syncthreads_or(bad >= 0)) {
-    if (status) status[s * fs] = BX_STATUS_ZERO_PIVOT;
+    // (mark: the word still holds the mark, which the peers may yet have to
+    // read -- add a bit now, rank 0 settles the word after the cluster barrier)
+    if (mark) { if (bad >= 0) atomicOr(status + s, 0x80); }
+    else if (status) status[s * fs] = BX_STATUS_ZERO_PIVOT;
     if (index && bad >= 0) atomicMin(reinterpret_cast<unsigned int *>(index + s), (unsigned int)bad);
   }
 #ifdef BX_TRACE
@@ -420,6 +426,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
       if (warp != 0) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // pairs the arrive above
       asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");
       asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+      if (mark && crank == 0 && t == 0) status[s] = (status[s] & 0x80) ? BX_STATUS_ZERO_PIVOT : BX_STATUS_OK;
       asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // "started" for the next one
       ph ^= 1u;
     }
@@ -432,6 +439,7 @@ part_kernel(const double *__restrict__ c2p, const double *__restrict__ c1p,
 // launch configuration
 // ----------------------------------------------------------------------------
 static const Outer kNoOuter{nullptr, nullptr, nullptr, 0};
+
 
 template <int K, int M, int T, bool VEC, class Lay, bool SP = false>
 static int launch(const double *c2, const double *c1, const double *e, const double *f1,
@@ -473,8 +481,9 @@ static int launch(const double *c2, const double *c1, const double *e, const dou
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = only ? 2 : 1;
+  // fs < 0: no-workspace retry (marks in the status array, see part_kernel)
   cudaError_t err = cudaLaunchKernelEx(&cfg, kern, c2, c1, e, f1, f2, b, x, st, ix, nz, batch, n,
-                                       lay, csize, outer, only, fs);
+                                       lay, csize, outer, only, fs < 0 ? 1 : fs, fs < 0 ? kRetryMark : 0);
   if (err != cudaSuccess) {
     bxh::set_error("partitioned solver launch: %s", cudaGetErrorString(err));
     return BX_ERR_CUDA;
@@ -526,14 +535,15 @@ static int dispatch2(const double *c2, const double *c1, const double *e, const 
 template <bool VEC, class Lay>
 static int dispatch_sparse(const double *c1, const double *e, const double *f1, const double *b,
                            double *x, int32_t *st, int32_t *ix, int64_t *nz, int64_t batch,
-                           int64_t n, Lay lay, cudaStream_t stream, Outer o) {
+                           int64_t n, Lay lay, cudaStream_t stream, Outer o,
+                           const int32_t *only = nullptr, int fs = 1) {
   if (n <= 256)
-    return launch<2, 8, 32, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
+    return launch<2, 8, 32, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o, only, fs);
   if (n <= 512)
-    return launch<2, 8, 64, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
+    return launch<2, 8, 64, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o, only, fs);
   if (n <= 1024)  // the 1024-row shape measured slower here (n=4096: 0.668 vs 0.632 ms)
-    return launch<2, 16, 64, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
-  return launch<2, 16, 128, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o);
+    return launch<2, 16, 64, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o, only, fs);
+  return launch<2, 16, 128, VEC, Lay, true>(nullptr, c1, e, f1, nullptr, b, x, st, ix, nz, batch, n, lay, stream, o, only, fs);
 }
 
 // one CTA per system: rows whose sub2 (i >= 2) or sup2 (i <= n-3) is nonzero,
@@ -718,14 +728,31 @@ int mnpdm_sparse_part(const int32_t *rows, const double *vsub2, const double *vs
                       double *x, int32_t *st, int32_t *ix, int64_t *nz, int64_t batch, int64_t n,
                       int64_t ld, int layout, cudaStream_t stream) {
   const part::Outer o{rows, vsub2, vsup2, k};
+  // first pass: interface iteration with the status array carrying the retry
+  // marks (this entry has no workspace); the tree pass then solves the marked
+  // systems and writes their final status / index
+  const int32_t *only = nullptr;
+  int fs = 1;
+  if (halo_enabled() && st) {
+    int cs = 1;
+    const int rc = halo_solve(2, nullptr, d, e, f, nullptr, b, x, st, nullptr, nullptr, batch, n, ld,
+                              layout, stream, rows, vsub2, vsup2, k, &cs, ix, nz);
+    if (rc == BX_OK) {
+      only = st;
+      fs = -1;  // marks in the status array
+      nz = nullptr;
+    } else if (rc != BX_ERR_UNSUPPORTED) {
+      return rc;
+    }
+  }
   if (layout == BX_LAYOUT_SYSTEM_MAJOR) {
     const bool vec = ld % 4 == 0 && part::aligned32(d) && part::aligned32(e) && part::aligned32(f) &&
                      part::aligned32(b) && part::aligned32(x);
     if (vec)
-      return part::dispatch_sparse<true>(d, e, f, b, x, st, ix, nz, batch, n, SystemMajor{ld}, stream, o);
-    return part::dispatch_sparse<false>(d, e, f, b, x, st, ix, nz, batch, n, SystemMajor{ld}, stream, o);
+      return part::dispatch_sparse<true>(d, e, f, b, x, st, ix, nz, batch, n, SystemMajor{ld}, stream, o, only, fs);
+    return part::dispatch_sparse<false>(d, e, f, b, x, st, ix, nz, batch, n, SystemMajor{ld}, stream, o, only, fs);
   }
-  return part::dispatch_sparse<false>(d, e, f, b, x, st, ix, nz, batch, n, Interleaved{ld}, stream, o);
+  return part::dispatch_sparse<false>(d, e, f, b, x, st, ix, nz, batch, n, Interleaved{ld}, stream, o, only, fs);
 }
 
 size_t other_workspace_bytes(int solver, int64_t batch, int64_t n) {

@@ -45,7 +45,8 @@ int halo_solve(int K, const double *c2, const double *c1, const double *e, const
                const double *f2, const double *b, double *x, int32_t *flags, int32_t *retry,
                int32_t *nzpart, int64_t batch, int64_t n, int64_t ld, int layout,
                cudaStream_t stream, const int32_t *outer_rows, const double *outer_sub2,
-               const double *outer_sup2, int64_t outer_k, int *csize);
+               const double *outer_sup2, int64_t outer_k, int *csize, int32_t *index = nullptr,
+               int64_t *nz = nullptr);
 
 // bx_band_ops.cu (reference order, bit-exact building blocks)
 void band_matvec(int bw, int64_t m, const double *c, const double *d, const double *e,

@@ -40,6 +40,10 @@ struct Outer {
   int64_t k;
 };
 
+// status word of a system the interface-iteration pass hands to the tree
+// pass when there is no workspace for separate marks (sparse-outer entry)
+constexpr int32_t kRetryMark = 0x7f;
+
 template <int K, int M, int T, bool VEC, bool SP, class Lay>
 struct Chunk {
   static constexpr int G = 4;

@@ -500,3 +500,40 @@ def test_partitioned_tree_pass_alone_still_solves_dominant_systems(cuda, env):
     assert out.returncode == 0, out.stderr[-2000:]
     line = [l for l in out.stdout.splitlines() if l.startswith("KNOB")][-1].split()
     assert line[1] == "True" and float(line[2]) <= REL_TOL and float(line[3]) <= REL_TOL
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("n", [300, 1024, 1500, 4096, 6000])
+def test_mnpdm_sparse_outer_weakly_dominant_retries_on_the_tree(cuda, layout, n):
+    # the sparse-outer entry has no workspace: the retry marks travel in the
+    # status array and the tree pass leaves the final status / index / nz
+    bsz = 10
+    rng = np.random.default_rng(n)
+    s1 = -np.ones((bsz, n)); s1[:, 0] = 0.0
+    p1 = -np.ones((bsz, n)); p1[:, n - 1] = 0.0
+    s2 = np.zeros((bsz, n)); s2[:, n - 2:] = rng.uniform(-1, 1, (bsz, 2))
+    p2 = np.zeros((bsz, n)); p2[:, :2] = rng.uniform(-1, 1, (bsz, 2))
+    main = np.abs(s2) + np.abs(s1) + np.abs(p1) + np.abs(p2) + 1e-3 * (1.0 + rng.uniform(0, 1, (bsz, n)))
+    # every other system strongly dominant: stays with the first pass
+    main[0::2] += 3.0
+    rhs = rng.uniform(-1, 1, (bsz, n))
+    p = (np.ascontiguousarray(s2[:, 2:]), np.ascontiguousarray(s1[:, 1:]), main,
+         np.ascontiguousarray(p1[:, :-1]), np.ascontiguousarray(p2[:, :-2]), rhs)
+    x_ref, _, _ = D.npdm(*p)
+    A = PentaMatrix.from_diagonals(*p[:5], layout=layout).sparse_outer()
+    rep = solve_mnpdm(A, p[5], algo="partitioned")
+    assert (host(rep.status) == 0).all() and (host(rep.index) == -1).all()
+    err = rel_err(host(rep.x), x_ref)
+    assert err[0::2].max() <= REL_TOL and err[1::2].max() <= 1e-9
+    _, _, _, nz = D.mnpdm(*p)
+    assert np.array_equal(host(rep.ops.total), np.array([sum(D.ops_mnpdm(n, int(z)).values()) for z in nz]))
+
+
+def test_mnpdm_sparse_outer_zero_pivot_goes_through_the_retry_pass(cuda):
+    n = 3000
+    p = [a.copy() for a in W.pd_dominant(4, n, seed=3, sparse_outer=True)]
+    p[2][1, 0] = 0.0   # a zero leading pivot: the chunk-local elimination fails too
+    A = PentaMatrix.from_diagonals(*p[:5], layout="system").sparse_outer()
+    rep = solve_mnpdm(A, p[5], algo="partitioned")
+    st = host(rep.status)
+    assert st[1] == 1 and host(rep.index)[1] == 0 and st[0] == 0 and st[2] == 0 and st[3] == 0
