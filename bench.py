@@ -285,7 +285,9 @@ class Direct:
             self.outer_bytes = batch * self.outer_k * (4 + 8 + 8)
         self.units = batch
         # partitioned: the solver kernel + the status / re-solve pass (direct_fixup)
-        self.launches_per_step = 2 if args.algo == "partitioned" and not self.sparse else 1
+        # partitioned: interface-iteration kernel, tree retry pass, re-solve /
+        # status pass (sparse-outer entry: the first two)
+        self.launches_per_step = (2 if self.sparse else 3) if args.algo == "partitioned" else 1
         gb = self.bytes_per_row * batch * n / 1e9
         # inputs that fit the 126 MB L2 (config 1: 42 MB) are flushed out of it
         # before every timed step (a 512 MB write, outside the step's events)
@@ -666,7 +668,7 @@ class Hb:
 class Adi:
     """Config 5: one ADI step on an 8192^2 grid (x-sweep, transpose / all-to-all, y-sweep)."""
     metric, unit, scaling = "systems_solved_per_s", "systems/s", "strong"
-    launches_per_step = 5  # 2 x (partitioned NTDM + status pass) + transpose
+    launches_per_step = 7  # 2 x (interface-iteration kernel + tree retry pass + status pass) + transpose
 
     def __init__(self, args, rank, dev, world, n=8192):
         import torch

@@ -16,7 +16,7 @@ run --impl reference --steps 3 --warmup 3
 run --impl reference --workload sip --steps 2 --warmup 3
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file $OUT/launches_npdm.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:part_kernel -s 3 -c 1 \
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:halo_kernel -s 3 -c 1 \
   -o $OUT/npdm_full python tools/sweep_part.py child 2 4096 8192 > $OUT/ncu_npdm.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:sip_wave -s 1 -c 1 \
   -o $OUT/sip_full python bench.py --workload sip --steps 1 --warmup 1 --no-cpu-baseline > $OUT/ncu_sip.log 2>&1

@@ -25,7 +25,7 @@ for line in open(src):
                 f"{e2e.get('value', float('nan')):.4g} | {e2e.get('pcie_frac', '-')} | "
                 f"{cpu.get('value') if cpu else None} ({cpu.get('cores', '-')} cores) |")
 with open(out, "w") as f:
-    f.write("# Round-1 bench lines (B200, 1 GPU; `tools/bench_all.sh`, driver-style JSON)\n\n")
+    f.write("# Bench lines of the round (B200, 1 GPU; `tools/bench_all.sh`, driver-style JSON)\n\n")
     f.write("| workload | value | unit | ms/step | roofline frac (achieved/peak) | e2e (host buffers) "
             "| PCIe H2D frac | cpu_baseline (C port) |\n|---|---|---|---|---|---|---|---|\n")
     f.write("\n".join(rows) + "\n\nRaw JSON lines:\n\n")
