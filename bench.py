@@ -9,7 +9,8 @@ Default workload: config 2 (BASELINE.json configs[1]) NPDM, B=8192 systems of
 order N=4096 per GPU, float64, seed 1 -- the configuration the headline metric
 is quoted on.  Other workloads (one JSON line each): mnpdm (config 2 sparse
 outer), ntdm (config 1), ntdm8k (one config-5 sweep), sip (config 4:
-512x512 grid, alpha 0.5, wavefront kernel).
+512x512 grid, alpha 0.5; --sip-algo wavefront (default: Algorithm 1 verbatim,
+bit parity) or scan (correction form + row scans, iteration count +-1)).
 
 A step = one batched solve of the whole batch on every rank (weak scaling:
 each rank its own seeded batch, no collective on the path).  Rank 0 prints
@@ -217,9 +218,9 @@ def static_config(args, world):
                           f"{cs['m']} grid (N={cs['n']}, offsets +-1, +-{cs['m']}), Stone alpha="
                           f"{cs['alpha']}, rel. tol 1e-8, <=500 iterations, seed {cs['cfg']}; a step = "
                           "one full sip_solve (ILU(0) + all iterations)"),
-             "solver": "sip", "algo": "wavefront", "batch_per_gpu": cs["batch"], "n": cs["n"],
+             "solver": "sip", "algo": getattr(args, "sip_algo", "wavefront"), "batch_per_gpu": cs["batch"], "n": cs["n"],
              "m": cs["m"], "alpha": cs["alpha"],
-             "l2": "every iteration streams the 22 skewed planes (5.9 GB) > 126 MB L2"}
+             "l2": "every iteration streams the factor / matrix / iterate planes (> 2 GB) > 126 MB L2"}
     elif w in ("stdm", "spdm"):
         bpr = 40 if w == "stdm" else 56
         c = {"workload": (f"config 3 {w.upper()}: B=4096 non-dominant systems, N=2048, 8 decoupled "
@@ -398,7 +399,6 @@ SIP_CFG = dict(batch=64, n=262144, m=512, alpha=0.5, cfg=3)
 
 class Sip:
     metric, unit, scaling = "sip_system_iterations_per_s", "system-iterations/s", "weak"
-    launches_per_step = 1
 
     def __init__(self, args, rank, dev):
         import torch
@@ -419,6 +419,11 @@ class Sip:
         self.res = torch.empty(self.batch, **f64)
         self.status = torch.empty(self.batch, dtype=torch.int32, device=dev)
         self.ws = workspace(_lib.lib().bx_sip_workspace_bytes(self.batch, self.n, m), dev)
+        # scan: correction form + row scans (throughput path, k within +-1 of
+        # the reference loop); wavefront: Algorithm 1 verbatim, bit parity
+        self.algo = args.sip_algo
+        # prefix table, skew/pack, wavefront kernel (setup [+ iterations]) [, scan kernel]
+        self.launches_per_step = 4 if self.algo == "scan" else 3
 
     def solve(self, ins, x):
         import torch
@@ -427,7 +432,8 @@ class Sip:
         _lib.call("bx_sip_f64", *(ptr(t) for t in ins[:5]), ptr(ins[5]), ptr(self.d_tol), ptr(x),
                   None, ptr(self.iters), ptr(self.res), None, ptr(self.status), None, None,
                   self.batch, self.n, self.m, self.alpha, 500, 0, self.n, _lib.LAYOUT_SYSTEM_MAJOR,
-                  2, ptr(self.ws), self.ws.numel(), torch.cuda.current_stream().cuda_stream)
+                  4 if self.algo == "scan" else 2, ptr(self.ws), self.ws.numel(),
+                  torch.cuda.current_stream().cuda_stream)
 
     def step(self):
         self.solve(self.d_in, self.x)
@@ -440,6 +446,13 @@ class Sip:
         idx = np.arange(0, self.batch, max(1, self.batch // 4))
         ref = cport.sip(*cport.rowaligned_penta(*(a[idx] for a in self.arrs[:5]), m=self.m),
                         self.arrs[5][idx], self.tol[idx], m=self.m, alpha=self.alpha)
+        if self.algo == "scan":  # north-star SIP contract: k +-1, residual below the tolerance
+            assert np.all(np.abs(self.iters.cpu().numpy()[idx] - ref["iterations"]) <= 1), "SIP parity gate"
+            assert bool((self.res.cpu().numpy() < self.tol).all()), "SIP parity gate (residual)"
+            x = self.x.cpu().numpy()[idx]
+            err = float(np.max(np.abs(x - ref["x"])) / np.max(np.abs(ref["x"])))
+            assert err <= 1e-7, "SIP parity gate (iterate)"
+            return err
         assert np.array_equal(self.iters.cpu().numpy()[idx], ref["iterations"])
         assert np.array_equal(self.x.cpu().numpy()[idx], ref["x"]), "SIP parity gate"
         return 0.0
@@ -462,10 +475,16 @@ class Sip:
     def roofline(self, mean_launch, peak):
         alg = 104 * self.n * self.total_iters   # 104 B per row-iteration
         ach = alg / mean_launch / 1e9
+        if self.algo == "scan":
+            kern = "bx sip_scan (ILU setup pass + forward/backward row-scan sweeps of every iteration)"
+            note = ("correction form streams 128 B/row-iteration (A, b, L, U, y, x) plus one extra "
+                    "forward sweep per solve; the setup pass is inside the timed solve")
+        else:
+            kern = "bx sip_wave (setup + all iterations, one launch)"
+            note = "Algorithm 1 verbatim streams ~184 B/row-iteration (K, factors, y, A, b, x)"
         return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": None, "kernel": "bx sip_wave (setup + all iterations, one launch)",
-                "algorithmic_bytes_per_launch": alg, "bytes_per_row_iteration": 104,
-                "note": "Algorithm 1 verbatim streams ~184 B/row-iteration (K, factors, y, A, b, x)"}
+                "traffic": None, "kernel": kern,
+                "algorithmic_bytes_per_launch": alg, "bytes_per_row_iteration": 104, "note": note}
 
     def cpu_baseline(self, budget_s=5.0):
         from oracle import cport
@@ -947,6 +966,9 @@ def main():
     ap.add_argument("--algo", default="partitioned", choices=["sequential", "partitioned"])
     ap.add_argument("--layout", default=None, choices=["interleaved", "system"],
                     help="C-ABI storage (default: system-major for partitioned, interleaved for sequential)")
+    ap.add_argument("--sip-algo", default="wavefront", choices=["scan", "wavefront"],
+                    help="SIP workload: scan = correction form + row scans (throughput path); "
+                         "wavefront = Algorithm 1 verbatim (bit parity)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=8,
                     help="system chunks of the overlapped host pipeline (e2e leg)")

@@ -57,7 +57,8 @@ extern "C" {
  * on m); max of the sequential and wavefront requirements. */
 size_t bx_sip_workspace_bytes(int64_t batch, int64_t n, int64_t m) {
   const size_t a = bx::sip_workspace_bytes(batch, n), b = bx::sip_wave_workspace_bytes(batch, n, m);
-  return a > b ? a : b;
+  const size_t c = bx::sip_scan_workspace_bytes(batch, n, m);
+  return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 
 const char *bx_version(void) { return "bandix_b200 0.1.0 (sm_100a)"; }
@@ -448,12 +449,18 @@ int bx_sip_f64(const double *subm, const double *sub1, const double *main, const
                ? BX_ALGO_WAVEFRONT
                : BX_ALGO_SEQUENTIAL;
   }
-  if (algo != BX_ALGO_SEQUENTIAL && algo != BX_ALGO_WAVEFRONT) {
+  if (algo != BX_ALGO_SEQUENTIAL && algo != BX_ALGO_WAVEFRONT && algo != BX_ALGO_SCAN) {
     set_error("bx_sip_f64: unknown algo %d", algo);
     return BX_ERR_ARG;
   }
   const size_t need = algo == BX_ALGO_WAVEFRONT ? bx::sip_wave_workspace_bytes(batch, n, m)
+                      : algo == BX_ALGO_SCAN    ? bx::sip_scan_workspace_bytes(batch, n, m)
                                                 : bx::sip_workspace_bytes(batch, n);
+  if (algo == BX_ALGO_SCAN && need == 0) {
+    set_error("bx_sip_f64: BX_ALGO_SCAN needs a grid width m that is a multiple of 32 in [32, 512] "
+              "and n %% m == 0 (n=%lld, m=%lld)", (long long)n, (long long)m);
+    return BX_ERR_UNSUPPORTED;
+  }
   if (workspace_bytes < need || !workspace) {
     set_error("bx_sip_f64: workspace %zu bytes < required %zu", workspace_bytes, need);
     return BX_ERR_WORKSPACE;
@@ -462,6 +469,11 @@ int bx_sip_f64(const double *subm, const double *sub1, const double *main, const
     bx::sip_seq(subm, sub1, main, sup1, supm, rhs, tol, x, best_x, iterations, residual,
                 best_residual, status, index, history, (double *)workspace, batch, n, m, alpha,
                 max_iter, use_x0, ld, layout, 0, st);
+  } else if (algo == BX_ALGO_SCAN) {
+    rc = bx::sip_scan(subm, sub1, main, sup1, supm, rhs, tol, x, best_x, iterations, residual,
+                      best_residual, status, index, history, (double *)workspace, batch, n, m,
+                      alpha, max_iter, use_x0, ld, layout, st);
+    if (rc) return rc;
   } else {
     rc = bx::sip_wave(subm, sub1, main, sup1, supm, rhs, tol, x, best_x, iterations, residual,
                       best_residual, status, index, history, (double *)workspace, batch, n, m,

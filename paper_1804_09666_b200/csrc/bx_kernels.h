@@ -107,6 +107,16 @@ int sip_wave(const double *a2, const double *a1, const double *e, const double *
              const double *c2, const double *b, const double *tol, double *x, double *best_x,
              int64_t *iters, double *res, double *best_res, int32_t *st, int32_t *ix,
              double *hist, double *ws, int64_t batch, int64_t n, int64_t m, double alpha,
+             int64_t max_iter, int use_x0, int64_t ld, int layout, cudaStream_t stream, double *nat = nullptr,
+             int32_t *setup_ok = nullptr);
+
+// bx_sip_scan.cu (BX_ALGO_SCAN: row-scan sweeps in correction form, tolerance parity)
+bool sip_scan_applicable(int64_t n, int64_t m);
+size_t sip_scan_workspace_bytes(int64_t batch, int64_t n, int64_t m);
+int sip_scan(const double *a2, const double *a1, const double *e, const double *c1,
+             const double *c2, const double *b, const double *tol, double *x, double *best_x,
+             int64_t *iters, double *res, double *best_res, int32_t *st, int32_t *ix,
+             double *hist, double *ws, int64_t batch, int64_t n, int64_t m, double alpha,
              int64_t max_iter, int use_x0, int64_t ld, int layout, cudaStream_t stream);
 
 // bx_exact.cu (kind 1 = STDM, 2 = SPDM)

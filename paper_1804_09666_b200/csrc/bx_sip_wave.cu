@@ -204,7 +204,11 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
                                 double *__restrict__ best_x, int64_t *iters, double *res,
                                 double *best_res, int32_t *status, int32_t *index,
                                 double *history, Skew S, int64_t n, double alpha,
-                                int64_t max_iter, int use_x0, Lay lay, int nst) {
+                                int64_t max_iter, int use_x0, Lay lay, int nst,
+                                double *__restrict__ nat, int32_t *__restrict__ setup_ok) {
+  // nat != nullptr: setup only, for the scan solver (bx_sip_scan.cu) -- the
+  // factors also leave in natural order, planes [l1 l2 mu phi psi][batch][n],
+  // setup_ok[s] says whether system s has them
   extern __shared__ double sh[];
   SIP_TR(0);
   const int64_t m = S.m, R = n / m, T = S.T;
@@ -345,6 +349,15 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
         up[0] = ph;
         up[Wt] = ps;
         up[2 * Wt] = mi;
+        if (nat) {  // (consecutive steps fill neighbouring words of a sector: merged in L2)
+          const int64_t pl = (int64_t)gridDim.x * n;
+          double *o = nat + s * n + (int64_t)p * mi_ + q;
+          o[0] = l1;
+          o[pl] = l2;
+          o[2 * pl] = mi;  // (the scan solver inverts the plane in a pass of its own)
+          o[3 * pl] = ph;
+          o[4 * pl] = ps;
+        }
         smu[sl_cur + q] = mi;
         sphi[sl_cur + q] = ph;
         spsi[sl_cur + q] = ps;
@@ -367,7 +380,12 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
       if (s_notgrid) set_status(status, index, s, BX_STATUS_NOT_GRID, -1);
       else set_status(status, index, s, BX_STATUS_ZERO_PIVOT, s_bad);
       if (iters) iters[s] = 0;
+      if (setup_ok) setup_ok[s] = 0;
     }
+    return;
+  }
+  if (nat) {
+    if (q == 0) setup_ok[s] = 1;
     return;
   }
 
@@ -804,7 +822,8 @@ int sip_wave(const double *a2, const double *a1, const double *e, const double *
              const double *c2, const double *b, const double *tol, double *x, double *best_x,
              int64_t *iters, double *res, double *best_res, int32_t *st, int32_t *ix,
              double *hist, double *ws, int64_t batch, int64_t n, int64_t m, double alpha,
-             int64_t max_iter, int use_x0, int64_t ld, int layout, cudaStream_t stream) {
+             int64_t max_iter, int use_x0, int64_t ld, int layout, cudaStream_t stream,
+             double *nat, int32_t *setup_ok) {
   if (n % m != 0 || m > 512) {
     bxh::set_error("wavefront SIP needs n %% m == 0 and m <= 512 (n=%lld, m=%lld)",
                    (long long)n, (long long)m);
@@ -848,13 +867,13 @@ int sip_wave(const double *a2, const double *a1, const double *e, const double *
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)batch, threads, smem, stream>>>(a2, a1, e, c1, c2, b, tol, x, best_x, iters,
                                                  res, best_res, st, ix, hist, S, n, alpha,
-                                                 max_iter, use_x0, Interleaved{ld}, nst);
+                                                 max_iter, use_x0, Interleaved{ld}, nst, nat, setup_ok);
   } else {
     auto k = m == 2 ? sipw::sip_wave_kernel<SystemMajor, true> : sipw::sip_wave_kernel<SystemMajor, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)batch, threads, smem, stream>>>(a2, a1, e, c1, c2, b, tol, x, best_x, iters,
                                                  res, best_res, st, ix, hist, S, n, alpha,
-                                                 max_iter, use_x0, SystemMajor{ld}, nst);
+                                                 max_iter, use_x0, SystemMajor{ld}, nst, nat, setup_ok);
   }
   return BX_OK;
 }

@@ -176,3 +176,85 @@ def test_sip_wavefront_is_deterministic(cuda):
     x0 = sip_solve(S, g[5], cfg, algo="wavefront").x.cpu().numpy()
     for _ in range(8):
         assert np.array_equal(sip_solve(S, g[5], cfg, algo="wavefront").x.cpu().numpy(), x0)
+
+
+# --------------------------------------------------------------------------
+# BX_ALGO_SCAN: correction form + row scans -- the north star's SIP contract
+# (iteration count within +-1 of the reference loop, final residual below the
+# tolerance), checked against the C restatement
+# --------------------------------------------------------------------------
+def _true_residual(p, m, x):
+    ra = cport.rowaligned_penta(*p[:5], m=m)
+    n = x.shape[1]
+    ax = ra[2] * x
+    ax[:, 1:] += ra[1][:, 1:] * x[:, :-1]
+    ax[:, :-1] += ra[3][:, :-1] * x[:, 1:]
+    ax[:, m:] += ra[0][:, m:] * x[:, :n - m]
+    ax[:, :n - m] += ra[4][:, :n - m] * x[:, m:]
+    return np.max(np.abs(p[5] - ax), axis=1)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("m,rows,alpha", [(32, 9, 0.5), (64, 40, 0.5), (64, 70, 0.0), (128, 21, 0.5),
+                                          (256, 6, 0.5), (96, 33, 0.5), (512, 16, 0.5)])
+def test_scan_matches_reference_loop(cuda, layout, m, rows, alpha):
+    n = m * rows
+    p = W.five_point(5, n, m, seed=9)
+    tol = W.sip_tolerance(p[5])
+    ref = cport.sip(*cport.rowaligned_penta(*p[:5], m=m), p[5], tol, m=m, alpha=alpha)
+    A = StencilMatrix.from_diagonals(*p[:5], m=m, layout=layout)
+    rep = sip_solve(A, p[5], SipConfig(tolerance=tol, max_iterations=500, alpha=alpha),
+                    record_history=True, algo="scan")
+    assert (host(rep.status) == 0).all()
+    assert np.all(np.abs(host(rep.iterations) - ref["iterations"]) <= 1)
+    x = host(rep.x)
+    assert np.all(host(rep.residual_inf) < tol)
+    # the reported residual is the residual of the returned iterate
+    assert np.allclose(_true_residual(p, m, x), host(rep.residual_inf), rtol=1e-6, atol=1e-18)
+    assert np.max(np.abs(x - ref["x"])) <= 1e-7 * np.max(np.abs(ref["x"]))
+    # the recorded history ends with the reported residual
+    h = host(rep.history)
+    for s in range(5):
+        k = int(host(rep.iterations)[s])
+        if k:
+            assert h[s, k - 1] == host(rep.residual_inf)[s]
+
+
+def test_scan_maxiter_reports_best_iterate(cuda):
+    m, rows = 64, 20
+    p = W.five_point(3, m * rows, m, seed=4)
+    A = StencilMatrix.from_diagonals(*p[:5], m=m)
+    rep = sip_solve(A, p[5], SipConfig(tolerance=1e-300, max_iterations=3, alpha=0.5), algo="scan")
+    assert (host(rep.status) == 3).all() and (host(rep.iterations) == 3).all()
+    assert np.allclose(_true_residual(p, m, host(rep.best_x)), host(rep.best_residual), rtol=1e-6)
+
+
+def test_scan_rejects_non_grid_and_zero_pivot(cuda):
+    m, rows = 32, 8
+    p = [a.copy() for a in W.five_point(3, m * rows, m, seed=5)]
+    p[1][1, m - 1] = 0.3      # A[m, m-1]: a coupling across a grid row
+    p[2][2, 0] = 0.0          # a zero leading pivot
+    A = StencilMatrix.from_diagonals(*p[:5], m=m)
+    rep = sip_solve(A, p[5], SipConfig(tolerance=1e-8, alpha=0.5), algo="scan")
+    st = host(rep.status)
+    assert st[0] == 0 and st[1] == 7 and st[2] == 1 and host(rep.index)[2] == 0
+
+
+def test_config4_full_scan(cuda):
+    """Config 4 at full size through the scan solver: iteration counts within
+    +-1 of the C restatement on sampled systems, every system below the
+    relative 1e-8 stopping rule, the residual recomputed on the host."""
+    p = W.five_point(64, 262144, 512, seed=3)
+    tol = W.sip_tolerance(p[5])
+    A = StencilMatrix.from_diagonals(*p[:5], m=512, layout="system")
+    rep = sip_solve(A, p[5], SipConfig(tolerance=tol, max_iterations=500, alpha=0.5), algo="scan")
+    assert (host(rep.status) == 0).all()
+    assert np.all(host(rep.residual_inf) < tol)
+    idx = np.arange(0, 64, 9)
+    ref = cport.sip(*cport.rowaligned_penta(*(x[idx] for x in p[:5]), m=512), p[5][idx], tol[idx],
+                    m=512, alpha=0.5)
+    assert np.all(np.abs(host(rep.iterations)[idx] - ref["iterations"]) <= 1)
+    x = host(rep.x)
+    sub = [a[idx] for a in p]
+    assert np.all(_true_residual(sub, 512, x[idx]) < tol[idx])
+    assert np.max(np.abs(x[idx] - ref["x"])) <= 1e-7 * np.max(np.abs(ref["x"]))

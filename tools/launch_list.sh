@@ -1,9 +1,10 @@
-# Developer tool: per-kernel durations of one partitioned solve (ncu launch list)
-# usage: bash tools/launch_list.sh K N B
-ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file /tmp/ll.csv python tools/sweep_part.py child $1 $2 $3 > /dev/null 2>&1
-python - <<PY
-import csv
-rows=list(csv.DictReader(l for l in open("/tmp/ll.csv") if not l.startswith("==")))
-for r in rows[-8:]:
+# Developer tool: per-kernel durations (ncu launch list) of a command's last kernels
+# usage: bash tools/launch_list.sh N CMD...   (prints the last N launches)
+N=$1; shift
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file /tmp/ll.csv "$@" > /dev/null 2>&1
+python - "$N" <<'PY'
+import csv, sys
+rows = list(csv.DictReader(l for l in open("/tmp/ll.csv") if not l.startswith("==")))
+for r in rows[-int(sys.argv[1]):]:
     print(r["Kernel Name"][:70], r["Metric Value"], r["Metric Unit"])
 PY
