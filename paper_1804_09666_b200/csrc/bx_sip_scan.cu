@@ -33,6 +33,7 @@ namespace bx {
 namespace sipscan {
 
 constexpr int kST = 4;  // grid rows in flight: cp.async ring stages in shared memory
+constexpr int kAhead = 24;  // rows the L2 prefetcher CTA runs in front of its solver
 
 // natural-order planes [batch][n]
 struct Nat {
@@ -145,9 +146,48 @@ sip_scan_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
                 double *__restrict__ best_x, int64_t *iters, double *res, double *best_res,
                 int32_t *status, int32_t *index, double *history, Nat N,
                 const int32_t *__restrict__ setup_ok, int64_t n, int m, int64_t max_iter,
-                int use_x0, Lay lay) {
+                int use_x0, Lay lay, int *prog, int64_t batch) {
+  // CTAs batch .. 2 batch - 1 (only when prog != nullptr; an experiment that is
+  // off by default, see sip_scan): L2 prefetchers, one per system, on SMs the
+  // solve leaves idle.  A solving CTA is fed at what
+  // one SM can pull from HBM on its own requests (~20 B/clk measured); its
+  // prefetcher walks kAhead rows in front of it (the solver publishes its
+  // position in prog[s]) and bulk-prefetches the rows of the planes whose
+  // addresses do not depend on the iteration, so the solver's copies hit L2.
+  if (blockIdx.x >= batch) {
+    const int64_t sp = blockIdx.x - batch;
+    if (threadIdx.x >= 32 || !setup_ok[sp]) return;
+    const int R = (int)(n / m), lane = threadIdx.x;
+    const int64_t o = sp * n;
+    const double *fw[8] = {a2p + lay(0, sp), a1p + lay(0, sp), ep + lay(0, sp), c1p + lay(0, sp),
+                           c2p + lay(0, sp), bp + lay(0, sp), N.l1 + o, N.l2 + o};
+    const double *bw[4] = {N.rmu + o, N.phi + o, N.psi + o, N.y + o};
+    const double *mine_f = fw[lane & 7], *mine_b = bw[lane & 3];
+    int ph = 0, i = 0;
+    for (;;) {
+      const int cur = *reinterpret_cast<volatile int *>(prog + sp);
+      if (cur == 0x7fffffff) return;
+      const int cph = cur / R, ci = cur % R;
+      if (cph > ph) { ph = cph; i = ci; }
+      if (i < R && i <= ci + kAhead) {
+        const int row = (ph & 1) ? R - 1 - i : i;  // odd sweeps run upwards
+        const double *src = ((ph & 1) ? mine_b : mine_f) + (int64_t)row * m;
+        if (lane < ((ph & 1) ? 4 : 8))
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src),
+                       "r"((unsigned)(m * sizeof(double)))
+                       : "memory");
+        ++i;
+      } else {
+        __nanosleep(100);
+      }
+    }
+  }
   const int64_t s = blockIdx.x;
-  if (!setup_ok[s]) return;  // not a grid / zero pivot: reported by the setup pass
+  if (!setup_ok[s]) {  // not a grid / zero pivot: reported by the setup pass
+    if (prog && threadIdx.x == 0) prog[s] = 0x7fffffff;
+    return;
+  }
+  int sweep = 0;  // sweeps started so far (even: forward, odd: backward)
   const int tq = threadIdx.x, lane = tq & 31, warp = tq >> 5, nw = (m / C) >> 5;
   const int q0 = C * tq;  // first own column
   const int R = (int)(n / m);
@@ -281,6 +321,7 @@ sip_scan_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
           if (lane == 31) tot[(p & 1) * nw + warp] = make_double2(A, B);
           const double Ap = __shfl_up_sync(0xffffffffu, A, 1), Bp = __shfl_up_sync(0xffffffffu, B, 1);
           __syncthreads();
+          if (prog && tq == 0) *reinterpret_cast<volatile int *>(prog + s) = sweep * R + p;
           const double cw = carry_in<true>(tot + (p & 1) * nw, warp, lane, nw);
           double yin = lane == 0 ? cw : fma(Ap, cw, Bp);  // y of the column left of the thread's
           double y[C];
@@ -297,6 +338,7 @@ sip_scan_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+    ++sweep;
     return block_max(rmax);
   };
 
@@ -351,6 +393,7 @@ sip_scan_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
           if (lane == 0) tot[(p & 1) * nw + warp] = make_double2(A, B);
           const double Ap = __shfl_down_sync(0xffffffffu, A, 1), Bp = __shfl_down_sync(0xffffffffu, B, 1);
           __syncthreads();
+          if (prog && tq == 0) *reinterpret_cast<volatile int *>(prog + s) = sweep * R + (R - 1 - p);
           const double cw = carry_in<false>(tot + (p & 1) * nw, warp, lane, nw);
           double din = lane == 31 ? cw : fma(Ap, cw, Bp);  // d of the column right of the thread's
           double xo[C];
@@ -365,6 +408,7 @@ sip_scan_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+    ++sweep;
     __syncthreads();  // x_new complete before the next forward pass reads neighbours' cells
   };
 
@@ -396,6 +440,7 @@ sip_scan_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
     }
   }
   if (tq == 0) {
+    if (prog) *reinterpret_cast<volatile int *>(prog + s) = 0x7fffffff;  // releases the prefetcher
     if (iters) iters[s] = k;
     if (res) res[s] = r;
     if (best_res) best_res[s] = best;
@@ -414,7 +459,7 @@ __global__ void invert_plane_kernel(double *mu, const int32_t *__restrict__ setu
 }  // namespace sipscan
 
 // workspace after the wavefront solver's: setup flags | 9 natural planes
-static size_t scan_flag_bytes(int64_t batch) { return ((size_t)batch * 4 + 255) & ~(size_t)255; }
+static size_t scan_flag_bytes(int64_t batch) { return ((size_t)batch * 8 + 255) & ~(size_t)255; }  // setup_ok | prog
 
 bool sip_scan_applicable(int64_t n, int64_t m) { return m >= 32 && m <= 512 && m % 32 == 0 && n % m == 0; }
 
@@ -449,6 +494,20 @@ int sip_scan(const double *a2, const double *a1, const double *e, const double *
   // columns per thread: measured on config 4 (m = 512): C = 1 7.47 ms, C = 2 8.04, C = 4 11.3
   // (fewer warps leave the per-row instruction stream of a warp exposed)
   int C = 1;
+  // L2 prefetcher CTAs (see sip_scan_kernel): when solvers and prefetchers are
+  // all resident at once and the rows are 16-byte aligned (bulk prefetch)
+  int *prog = nullptr;
+  {
+    // developer knob, off: measured on config 4 the prefetchers slow the solve (18.2 vs 7.47 ms)
+    static const int pf = getenv("BX_SCAN_PF") ? atoi(getenv("BX_SCAN_PF")) : 0;
+    auto a16 = [](const void *p) { return ((uintptr_t)p & 15u) == 0; };
+    if (pf && layout == BX_LAYOUT_SYSTEM_MAJOR && 2 * batch <= 148 && ld % 2 == 0 && m % 2 == 0 &&
+        a16(a2) && a16(a1) && a16(e) && a16(c1) && a16(c2) && a16(b)) {
+      prog = ok + batch;
+      cudaMemsetAsync(prog, 0, sizeof(int) * (size_t)batch, stream);
+    }
+  }
+  const unsigned grid = (unsigned)(prog ? 2 * batch : batch);
   if (const char *env = getenv("BX_SCAN_C")) {  // developer knob
     const int c = atoi(env);
     if ((c == 1 || c == 2 || c == 4) && m % (32 * c) == 0) C = c;
@@ -460,9 +519,9 @@ int sip_scan(const double *a2, const double *a1, const double *e, const double *
   do {                                                                                             \
     cudaFuncSetAttribute(sipscan::sip_scan_kernel<LAY, CC, VV>,                                     \
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                   \
-    sipscan::sip_scan_kernel<LAY, CC, VV><<<(unsigned)batch, (unsigned)(m / CC), smem, stream>>>(   \
+    sipscan::sip_scan_kernel<LAY, CC, VV><<<grid, (unsigned)(m / CC), smem, stream>>>(              \
         a2, a1, e, c1, c2, b, tol, x, best_x, iters, res, best_res, st, ix, hist, N, ok, n, (int)m, \
-        max_iter, use_x0, layv);                                                                    \
+        max_iter, use_x0, layv, prog, batch);                                                       \
   } while (0)
   if (layout == BX_LAYOUT_INTERLEAVED) {
     if (C == 4) BX_SCAN_LAUNCH(Interleaved, 4, false, Interleaved{ld});
