@@ -11,8 +11,13 @@ system-major [x][y] and the y-sweep result comes back as u[x][y].
 Multi-GPU (strong scaling): rank r owns grid rows [r*ny/G, (r+1)*ny/G) for the
 x-sweep and grid columns [r*nx/G, (r+1)*nx/G) for the y-sweep; the one
 exchange between the sweeps is an all-to-all of the transposed x-sweep output
-(NCCL over NVLink on the GPU path).  The solver, the transpose and the
-process group are injected so the exchange logic is tested with gloo on CPU.
+(NCCL over NVLink on the GPU path).  The exchange is larger than a rank's
+sweep at 8 GPUs, so the x-sweep runs in ``chunks`` slices of the
+rank's rows: slice c is solved and transposed, its all-to-all is queued
+asynchronously (NCCL's stream picks it up after the transpose) and slice c+1
+is solved meanwhile; the y-sweep starts when the last slice has arrived.
+The solver, the transpose and the process group are injected so the exchange
+logic is tested with gloo on CPU.
 """
 
 from __future__ import annotations
@@ -56,9 +61,11 @@ class ADIStep:
 
     xs: (sub1, main, sup1) row-aligned, shape (ny_local, nx): this rank's rows.
     ys: (sub1, main, sup1) row-aligned, shape (nx_local, ny): this rank's columns.
+    chunks: slices of the x-sweep whose exchanges overlap the next slice's
+    solve (multi-rank only; clipped to ny_local).
     """
 
-    def __init__(self, xs, ys, group=None, backend=None):
+    def __init__(self, xs, ys, group=None, backend=None, chunks=4):
         self.xs, self.ys = xs, ys
         self.group = group
         self.world = torch.distributed.get_world_size(group) if group is not None else 1
@@ -70,22 +77,37 @@ class ADIStep:
         self.backend = backend or CudaBackend(dev)
         f64 = dict(dtype=torch.float64, device=dev)
         self.X = torch.empty((self.nyl, self.nx), **f64)
-        self.XT = torch.empty((self.nx, self.nyl), **f64)
-        self.Y = torch.empty((self.nxl, self.ny), **f64) if self.world > 1 else None
-        self.recv = torch.empty((self.world, self.nxl, self.nyl), **f64) if self.world > 1 else None
         self.U = torch.empty((self.nxl, self.ny), **f64)
+        if self.world == 1:
+            self.XT = torch.empty((self.nx, self.nyl), **f64)
+            return
+        nch = max(1, min(int(chunks), self.nyl))
+        edges = [self.nyl * c // nch for c in range(nch + 1)]
+        self.slices = [(edges[c], edges[c + 1]) for c in range(nch) if edges[c + 1] > edges[c]]
+        # per slice: its transposed block [x][rows of the slice] (contiguous: block r
+        # of it goes to rank r) and what the other ranks send for the same rows
+        self.XTc = [torch.empty((self.nx, b - a), **f64) for a, b in self.slices]
+        self.recv = [torch.empty((self.world, self.nxl, b - a), **f64) for a, b in self.slices]
+        self.Y = torch.empty((self.nxl, self.ny), **f64)
 
     def __call__(self, rhs):
         be = self.backend
-        st_x = be.tri_solve(*self.xs, rhs, self.X)            # x-sweep
-        be.transpose(self.X, self.XT)                          # [x][y_local]
         if self.world == 1:
-            y_in = self.XT
-        else:
-            # block r of XT (columns owned by rank r) goes to rank r
-            torch.distributed.all_to_all_single(self.recv.view(-1), self.XT.view(-1),
-                                                group=self.group)
-            self.Y.view(self.nxl, self.world, self.nyl).copy_(self.recv.transpose(0, 1))
-            y_in = self.Y
-        st_y = be.tri_solve(*self.ys, y_in, self.U)            # y-sweep
-        return self.U, st_x, st_y
+            st_x = be.tri_solve(*self.xs, rhs, self.X)        # x-sweep
+            be.transpose(self.X, self.XT)                      # [x][y]
+            st_y = be.tri_solve(*self.ys, self.XT, self.U)     # y-sweep
+            return self.U, st_x, st_y
+        works, st_parts = [], []
+        for (a, b), xt, rv in zip(self.slices, self.XTc, self.recv):
+            st_parts.append(be.tri_solve(*(d[a:b] for d in self.xs), rhs[a:b], self.X[a:b]))
+            be.transpose(self.X[a:b], xt)                      # [x][rows a..b)
+            # block r of xt (the grid columns rank r owns) goes to rank r; queued
+            # behind the transpose, it runs while the next slice is solved
+            works.append(torch.distributed.all_to_all_single(rv.view(-1), xt.view(-1),
+                                                             group=self.group, async_op=True))
+        Yv = self.Y.view(self.nxl, self.world, self.nyl)
+        for (a, b), rv, w in zip(self.slices, self.recv, works):
+            w.wait()
+            Yv[:, :, a:b].copy_(rv.transpose(0, 1))            # rows a..b) of every source rank
+        st_y = be.tri_solve(*self.ys, self.Y, self.U)          # y-sweep
+        return self.U, torch.cat(st_parts), st_y

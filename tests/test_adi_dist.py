@@ -45,7 +45,7 @@ def _free_port():
         return sk.getsockname()[1]
 
 
-def _worker(rank, world, port, n, out):
+def _worker(rank, world, port, n, out, chunks):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     xs, rhs, ys = problem(n)
@@ -53,7 +53,7 @@ def _worker(rank, world, port, n, out):
     rows = slice(rank * ny_l, (rank + 1) * ny_l)
     cols = slice(rank * nx_l, (rank + 1) * nx_l)
     step = ADIStep([a[rows].contiguous() for a in xs], [a[cols].contiguous() for a in ys],
-                   group=dist.group.WORLD, backend=CpuBackend())
+                   group=dist.group.WORLD, backend=CpuBackend(), chunks=chunks)
     u, _, _ = step(rhs[rows].contiguous())
     gathered = [torch.empty_like(u) for _ in range(world)]
     dist.all_gather(gathered, u)
@@ -63,14 +63,17 @@ def _worker(rank, world, port, n, out):
     dist.destroy_process_group()
 
 
-def test_adi_two_ranks_gloo_equals_single():
+@pytest.mark.parametrize("chunks", [1, 4, 5])
+def test_adi_two_ranks_gloo_equals_single(chunks):
+    # chunks > 1: the x-sweep runs in slices whose all-to-alls are queued
+    # asynchronously (5 does not divide the 32 local rows: ragged slices)
     n = 64
     xs, rhs, ys = problem(n)
     single, _, _ = ADIStep(xs, ys, backend=CpuBackend())(rhs)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, q, chunks)) for r in range(2)]
     for p in procs:
         p.start()
     got = q.get(timeout=120)
