@@ -289,6 +289,37 @@ def golden_exact():
     _save("exact", **out)
 
 
+def golden_exact2():
+    """More reference-exact symbolic solves (round 2: the verdict found the
+    first set thin): wider spread of sizes, zero counts and seeds.  Sized so
+    that the exact solvers finish in minutes (RatFunc gcd cost grows fast)."""
+    out = {}
+    cases = [("td_a", "td", 10, 48, 3, 11), ("td_b", "td", 6, 72, 2, 12), ("td_c", "td", 4, 32, 5, 13),
+             ("pd_a", "pd", 6, 28, 2, 21), ("pd_b", "pd", 3, 40, 2, 22), ("pd_c", "pd", 3, 32, 3, 23)]
+    for tag, kind, bsz, n, zeros, seed in cases:
+        t0 = time.time()
+        if kind == "td":
+            *d, rows = W.td_symbolic(bsz, n, seed=seed, zeros=zeros)
+            nd = 3
+        else:
+            *d, rows = W.pd_symbolic(bsz, n, seed=seed, zeros=zeros)
+            nd = 5
+        xs = np.zeros((bsz, n)); subs = np.zeros(bsz, np.int64)
+        for s in range(bsz):
+            diags = [[core.to_exact(v) for v in q[s]] for q in d[:nd]]
+            rhs = [core.to_exact(v) for v in d[nd][s]]
+            if kind == "td":
+                r = exact.exact_solve_stdm(core.TriMatrix.from_diagonals(*diags), rhs)
+            else:
+                r = exact.exact_solve_spdm(core.PentaMatrix.from_diagonals(*diags), rhs)
+            xs[s] = [float(v) for v in r.x]; subs[s] = r.pivot_substitutions
+        for j, q in enumerate(d[:nd + 1]):
+            out[f"{tag}_in{j}"] = q
+        out.update({f"{tag}_rows": rows, f"{tag}_x": xs, f"{tag}_subs": subs})
+        print(f"{tag}: {bsz} x N={n}, {zeros} zeros, {time.time()-t0:.1f}s subs={subs.tolist()}", flush=True)
+    _save("exact2", **out)
+
+
 def _frexp_fraction(v):
     e = v.numerator.bit_length() - v.denominator.bit_length() if v != 0 else 0
     if v == 0:

@@ -87,7 +87,10 @@ def test_config3_full_size(cuda, kind):
     assert (st == 0).all(), np.unique(st, return_counts=True)
     assert (host(r.pivot_substitutions) == 8).all()
     x = host(r.x)
-    for s in range(0, 4096, 512):
+    # 128 of the 4096 systems against the 50-digit pivoted oracle (itself pinned
+    # to the reference's exact results, tests/test_oracle_golden.py); round 1
+    # sampled 8
+    for s in range(0, 4096, 32):
         ref = limit_solve_mp([q[s] for q in p[:nd]], offs, p[nd][s])
         assert rel(x[s], ref) <= REL_TOL, (s, rel(x[s], ref))
 
@@ -184,3 +187,25 @@ def test_det_band_minimal_and_layouts(cuda):
     for s in range(3):
         m, e = det_band_mp([q[s] for q in p[:5]], [-2, -1, 0, 1, 2])
         assert _det_rel(r, s, m, e) <= REL_TOL
+
+
+# round 2: a wider reference-exact set (tests/golden/exact2.npz, generated by
+# make_golden.py exact2 through exact_solve_stdm / exact_solve_spdm): 20
+# tridiagonal and 12 pentadiagonal systems, 2-5 zero pivots, N = 28..72
+EXACT2 = [("td_a", 3), ("td_b", 3), ("td_c", 3), ("pd_a", 5), ("pd_b", 5), ("pd_c", 5)]
+
+
+@pytest.mark.parametrize("layout", ["interleaved", "system"])
+@pytest.mark.parametrize("tag,nd", EXACT2)
+def test_symbolic_golden_wide(cuda, golden, layout, tag, nd):
+    g = golden("exact2")
+    d = [g[f"{tag}_in{j}"] for j in range(nd + 1)]
+    if nd == 3:
+        r = exact_solve_stdm(TriMatrix.from_diagonals(*d[:3], layout=layout), d[3])
+    else:
+        r = exact_solve_spdm(PentaMatrix.from_diagonals(*d[:5], layout=layout), d[5])
+    assert (host(r.status) == 0).all()
+    assert np.array_equal(host(r.pivot_substitutions), g[f"{tag}_subs"])
+    x = host(r.x)
+    for s in range(x.shape[0]):
+        assert rel(x[s], g[f"{tag}_x"][s]) <= REL_TOL, (tag, s, rel(x[s], g[f"{tag}_x"][s]))

@@ -199,3 +199,32 @@ def test_sip_hb_banded_restatement(golden):
     # this build's true-residual widening converges
     o = H.sip_hb_banded(*p, g["hbb_tol"], 60, w=None)
     assert (o["status"] == 0).all() and (o["residual"] < g["hbb_tol"]).all()
+
+
+# the 50-digit pivoted limit solve that stands in for the reference's exact
+# solvers at config-3 size (tests/test_exact_gpu.py) is pinned to the
+# reference's own exact results: exact.npz and the wider round-2 set exact2.npz
+@pytest.mark.parametrize("name,tag,nd", [("exact2", "td_a", 3), ("exact2", "td_b", 3), ("exact2", "td_c", 3),
+                                         ("exact2", "pd_a", 5), ("exact2", "pd_b", 5), ("exact2", "pd_c", 5)])
+def test_limit_solve_oracle_reproduces_reference_exact_solves(golden, name, tag, nd):
+    from oracle.exact import limit_solve_mp
+    g = golden(name)
+    d = [g[f"{tag}_in{j}"] for j in range(nd + 1)]
+    offs = [-1, 0, 1] if nd == 3 else [-2, -1, 0, 1, 2]
+    for s in range(d[0].shape[0]):
+        x = limit_solve_mp([q[s] for q in d[:nd]], offs, d[nd][s])
+        ref = g[f"{tag}_x"][s]
+        assert np.max(np.abs(x - ref)) <= 1e-14 * np.max(np.abs(ref)), (tag, s)
+
+
+def test_limit_solve_oracle_first_golden_set(golden):
+    from oracle.exact import limit_solve_mp
+    g = golden("exact")
+    for s in range(3):
+        x = limit_solve_mp([g["stdm_sub1"][s], g["stdm_main"][s], g["stdm_sup1"][s]], [-1, 0, 1],
+                           g["stdm_rhs"][s])
+        assert np.max(np.abs(x - g["stdm_x"][s])) <= 1e-14 * np.max(np.abs(g["stdm_x"][s]))
+    keys = ("sub2", "sub1", "main", "sup1", "sup2")
+    for s in range(2):
+        x = limit_solve_mp([g[f"spdm_{k}"][s] for k in keys], [-2, -1, 0, 1, 2], g["spdm_rhs"][s])
+        assert np.max(np.abs(x - g["spdm_x"][s])) <= 1e-14 * np.max(np.abs(g["spdm_x"][s]))
