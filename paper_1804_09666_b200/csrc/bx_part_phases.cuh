@@ -18,6 +18,10 @@
 #ifndef BX_PART_LA
 #define BX_PART_LA 1  // input groups in flight ahead of the elimination (measured: 1 > 2 > 3)
 #endif
+#ifndef BX_SP_REG_ENTRIES
+#define BX_SP_REG_ENTRIES 2  // sparse outer entries of a thread held in registers (more: loads;
+                             // 4 spill under the interface kernel's 168-register cap)
+#endif
 #ifndef BX_P3_UNROLL
 #define BX_P3_UNROLL 2  // row groups of phase 3 unrolled together (measured: 2 >= 4 > 1)
 #endif
@@ -154,13 +158,16 @@ struct Chunk {
       while (oe < k && orow[oe] >= 0 && orow[oe] < base + M) ++oe;
     }
   };
-  // this thread's first 4 entries in registers (rows compared per row, no
-  // memory access on the elimination chain); more than 4 fall back to loads
-  int32_t er[4] = {-1, -1, -1, -1};
-  double es2[4] = {0, 0, 0, 0}, ep2[4] = {0, 0, 0, 0};
+  // this thread's first NE entries in registers (rows compared per row, no
+  // memory access on the elimination chain); more fall back to loads
+  constexpr int NE = BX_SP_REG_ENTRIES;
+  int32_t er[NE];
+  double es2[NE], ep2[NE];
+#pragma unroll
+  for (int q = 0; q < NE; ++q) { er[q] = -1; es2[q] = ep2[q] = 0.0; }
   auto outer_regs = [&]() {
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < NE; ++q)
       if (ob + q < oe) {
         const int64_t o = s * outer.k + ob + q;
         er[q] = __ldg(outer.rows + o);
@@ -199,14 +206,14 @@ struct Chunk {
     double c2 = (K != 2 || SP || j > rend - 3) ? 0.0 : cur.c2[u];
     if (SP) {  // branch-free for the register entries (the row loop stays one block)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < NE; ++q) {
         const bool h = er[q] == (int32_t)i;
         a2 = h ? (i < 2 ? 0.0 : es2[q]) : a2;
         c2 = h ? (i > n - 3 ? 0.0 : ep2[q]) : c2;
       }
     }
-    if (SP && oe - ob > 4) {
-      for (int q = ob + 4; q < oe; ++q)
+    if (SP && oe - ob > NE) {
+      for (int q = ob + NE; q < oe; ++q)
         if (outer.rows[s * outer.k + q] == (int32_t)i) {
           a2 = i < 2 ? 0.0 : outer.sub2[s * outer.k + q];
           c2 = i > n - 3 ? 0.0 : outer.sup2[s * outer.k + q];
