@@ -27,7 +27,9 @@
  *    below; index is the failing row (ZeroPivot.index) or -1.
  *  - Return value: BX_OK, or an argument / launch error (bx_last_error()
  *    gives the message).  Numerical outcomes never fail the call.
- *  - Calls are stream-ordered and asynchronous; they do not allocate on the
+ *  - Calls are stream-ordered and asynchronous (exceptions, stated at their
+ *    declarations: the Hotelling-Bodewig entry points drive their iteration
+ *    from the host and synchronise the stream); they do not allocate on the
  *    hot path -- scratch comes from a caller-provided workspace of at least
  *    bx_workspace_bytes(...) bytes.  Reentrant on distinct buffers/streams.
  */
@@ -66,7 +68,15 @@ extern "C" {
 
 /* algorithms for the direct solvers */
 #define BX_ALGO_SEQUENTIAL 0   /* reference operation order, bit-identical results */
-#define BX_ALGO_PARTITIONED 1  /* on-chip partitioned elimination, tolerance parity */
+/* On-chip partitioned elimination, tolerance parity (<= 1e-10 relative).  Two
+ * passes chosen per system on the device: chunk two-ports coupled by a fixed
+ * number of block-Jacobi sweeps over the chunk interfaces (exact to rounding
+ * when the measured interface coupling is below 2^-13, i.e. for diagonally
+ * dominant systems), then the two-port tree for the systems that fail that
+ * test (exact for any nonsingular reduced system).  Systems with a zero or
+ * non-finite pivot of this elimination order are re-solved in the reference
+ * order, so their x / status / index are the reference's. */
+#define BX_ALGO_PARTITIONED 1
 
 /* solver ids for bx_workspace_bytes */
 #define BX_SOLVER_NTDM 0
