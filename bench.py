@@ -9,8 +9,8 @@ Default workload: config 2 (BASELINE.json configs[1]) NPDM, B=8192 systems of
 order N=4096 per GPU, float64, seed 1 -- the configuration the headline metric
 is quoted on.  Other workloads (one JSON line each): mnpdm (config 2 sparse
 outer), ntdm (config 1), ntdm8k (one config-5 sweep), sip (config 4:
-512x512 grid, alpha 0.5; --sip-algo wavefront (default: Algorithm 1 verbatim,
-bit parity) or scan (correction form + row scans, iteration count +-1)).
+512x512 grid, alpha 0.5; --sip-algo scan (default: correction form + row scans,
+iteration count +-1) or wavefront (Algorithm 1 verbatim, bit parity)).
 
 A step = one batched solve of the whole batch on every rank (weak scaling:
 each rank its own seeded batch, no collective on the path).  Rank 0 prints
@@ -66,6 +66,8 @@ def load_traffic(args):
         with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
             t = json.load(f)
         key = args.workload if args.workload != "npdm" or args.algo == "partitioned" else "npdm_seq"
+        if args.workload == "sip" and args.sip_algo == "scan":
+            key = "sip_scan"
         return t.get(key)
     except Exception:
         return None
@@ -218,7 +220,7 @@ def static_config(args, world):
                           f"{cs['m']} grid (N={cs['n']}, offsets +-1, +-{cs['m']}), Stone alpha="
                           f"{cs['alpha']}, rel. tol 1e-8, <=500 iterations, seed {cs['cfg']}; a step = "
                           "one full sip_solve (ILU(0) + all iterations)"),
-             "solver": "sip", "algo": getattr(args, "sip_algo", "wavefront"), "batch_per_gpu": cs["batch"], "n": cs["n"],
+             "solver": "sip", "algo": getattr(args, "sip_algo", "scan"), "batch_per_gpu": cs["batch"], "n": cs["n"],
              "m": cs["m"], "alpha": cs["alpha"],
              "l2": "every iteration streams the factor / matrix / iterate planes (> 2 GB) > 126 MB L2"}
     elif w in ("stdm", "spdm"):
@@ -966,7 +968,7 @@ def main():
     ap.add_argument("--algo", default="partitioned", choices=["sequential", "partitioned"])
     ap.add_argument("--layout", default=None, choices=["interleaved", "system"],
                     help="C-ABI storage (default: system-major for partitioned, interleaved for sequential)")
-    ap.add_argument("--sip-algo", default="wavefront", choices=["scan", "wavefront"],
+    ap.add_argument("--sip-algo", default="scan", choices=["scan", "wavefront"],
                     help="SIP workload: scan = correction form + row scans (throughput path); "
                          "wavefront = Algorithm 1 verbatim (bit parity)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

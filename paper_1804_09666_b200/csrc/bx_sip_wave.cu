@@ -321,6 +321,18 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
         const double l1 = has1 ? li1 : 0.0, l2 = has2 ? li2 : 0.0;
         // defect K = LU - A (iterative.py:152-200); cross-row products are
         // structural zeros and are skipped
+        if (nat) {
+          // scan solver: the factors in natural order are all it needs (no
+          // defect K, no packed planes); consecutive steps fill neighbouring
+          // words of a sector, merged in L2
+          const int64_t pl = (int64_t)gridDim.x * n;
+          double *o = nat + s * n + (int64_t)p * mi_ + q;
+          o[0] = l1;
+          o[pl] = l2;
+          o[2 * pl] = mi;  // (the scan solver inverts the plane in a pass of its own)
+          o[3 * pl] = ph;
+          o[4 * pl] = ps;
+        } else {
         const double pm = pge1 ? mul(l2, mu_u) : 0.0;
         double p_1 = (ige1 && qge1) ? mul(l1, mu_l) : 0.0;
         if (M2 && pge1) p_1 = add(p_1, mul(l2, phi_u));           // i >= 2
@@ -349,14 +361,6 @@ __global__ void __launch_bounds__(544) sip_wave_kernel(const double *__restrict_
         up[0] = ph;
         up[Wt] = ps;
         up[2 * Wt] = mi;
-        if (nat) {  // (consecutive steps fill neighbouring words of a sector: merged in L2)
-          const int64_t pl = (int64_t)gridDim.x * n;
-          double *o = nat + s * n + (int64_t)p * mi_ + q;
-          o[0] = l1;
-          o[pl] = l2;
-          o[2 * pl] = mi;  // (the scan solver inverts the plane in a pass of its own)
-          o[3 * pl] = ph;
-          o[4 * pl] = ps;
         }
         smu[sl_cur + q] = mi;
         sphi[sl_cur + q] = ph;

@@ -14,6 +14,7 @@ run --workload ntdm --steps 30 --warmup 5   # (a 23-us step: 5 steps are noise)
 for w in mnpdm ntdm8k sip stdm spdm hb adi; do run --workload $w --steps 5 --warmup 3; done
 run --workload npdm --algo sequential --steps 5 --warmup 3
 run --impl reference --steps 3 --warmup 3
+run --workload sip --sip-algo wavefront --steps 5 --warmup 3
 run --impl reference --workload sip --steps 2 --warmup 3
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file $OUT/launches_npdm.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
