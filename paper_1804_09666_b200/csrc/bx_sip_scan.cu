@@ -21,6 +21,9 @@
 // (phi_q / mu_q) d_{q+1} is the mirror image.  Inputs of the next rows are
 // prefetched into registers while a row is scanned.
 //
+// Grids of 128 columns and more are split over a CTA pair (two SMs per system)
+// as a feed-forward pipeline, sip_scan_pair_kernel below.
+//
 // The factors come from the wavefront kernel's setup pass (ILU(0) / Stone
 // alpha, bit-identical to ilu0_penta, iterative.py:62-124), which also leaves
 // them in natural order for this kernel (1/mu instead of mu).
@@ -33,7 +36,6 @@ namespace bx {
 namespace sipscan {
 
 constexpr int kST = 4;  // grid rows in flight: cp.async ring stages in shared memory
-constexpr int kAhead = 24;  // rows the L2 prefetcher CTA runs in front of its solver
 
 // natural-order planes [batch][n]
 struct Nat {
@@ -61,9 +63,12 @@ __device__ __forceinline__ void warp_scan(double &A, double &B, int lane) {
 }
 
 // value entering warp `warp` from the warps before (UP) / after (!UP) it:
-// scan of the warp totals tot[w] = (A, B), start value 0
+// scan of the warp totals tot[w] = (A, B) from the value `start` that enters
+// the first warp in scan order (0 at a system edge, the neighbouring CTA's
+// boundary value in the CTA-pair kernel)
 template <bool UP>
-__device__ __forceinline__ double carry_in(const double2 *tot, int warp, int lane, int nw) {
+__device__ __forceinline__ double carry_in(const double2 *tot, int warp, int lane, int nw,
+                                           double start = 0.0) {
   // Fast path: the previous warp's map forgets what entered it (|A| * |carry|
   // is below the rounding of B: dominant rows decay by the 32 cells of a warp),
   // so the value leaving it is its B alone.  Checked per row, exact otherwise.
@@ -71,10 +76,10 @@ __device__ __forceinline__ double carry_in(const double2 *tot, int warp, int lan
   if (prev >= 0 && prev < nw) {
     const double2 v = tot[prev];
     const int pp = UP ? prev - 1 : prev + 1;
-    const double bprev = (pp >= 0 && pp < nw) ? fabs(tot[pp].y) : 0.0;
+    const double bprev = (pp >= 0 && pp < nw) ? fabs(tot[pp].y) : fabs(start);
     if (fabs(v.x) * bprev <= 0x1p-60 * fabs(v.y) && fabs(v.x) <= 0x1p-40) return v.y;
   } else {
-    return 0.0;
+    return start;
   }
   const int j = UP ? lane : nw - 1 - lane;  // lane 0 holds the first warp in scan order
   double A = 0.0, B = 0.0;
@@ -85,8 +90,9 @@ __device__ __forceinline__ double carry_in(const double2 *tot, int warp, int lan
   }
   warp_scan<true>(A, B, lane);
   const int src = (UP ? warp : nw - 1 - warp) - 1;  // inclusive result of the warp before this one
+  const double a = __shfl_sync(0xffffffffu, A, src < 0 ? 0 : src);
   const double c = __shfl_sync(0xffffffffu, B, src < 0 ? 0 : src);
-  return src < 0 ? 0.0 : c;
+  return src < 0 ? start : fma(a, start, c);
 }
 
 // C doubles at p (32-byte vector access when VEC: C == 4, aligned)
@@ -146,48 +152,9 @@ sip_scan_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
                 double *__restrict__ best_x, int64_t *iters, double *res, double *best_res,
                 int32_t *status, int32_t *index, double *history, Nat N,
                 const int32_t *__restrict__ setup_ok, int64_t n, int m, int64_t max_iter,
-                int use_x0, Lay lay, int *prog, int64_t batch) {
-  // CTAs batch .. 2 batch - 1 (only when prog != nullptr; an experiment that is
-  // off by default, see sip_scan): L2 prefetchers, one per system, on SMs the
-  // solve leaves idle.  A solving CTA is fed at what
-  // one SM can pull from HBM on its own requests (~20 B/clk measured); its
-  // prefetcher walks kAhead rows in front of it (the solver publishes its
-  // position in prog[s]) and bulk-prefetches the rows of the planes whose
-  // addresses do not depend on the iteration, so the solver's copies hit L2.
-  if (blockIdx.x >= batch) {
-    const int64_t sp = blockIdx.x - batch;
-    if (threadIdx.x >= 32 || !setup_ok[sp]) return;
-    const int R = (int)(n / m), lane = threadIdx.x;
-    const int64_t o = sp * n;
-    const double *fw[8] = {a2p + lay(0, sp), a1p + lay(0, sp), ep + lay(0, sp), c1p + lay(0, sp),
-                           c2p + lay(0, sp), bp + lay(0, sp), N.l1 + o, N.l2 + o};
-    const double *bw[4] = {N.rmu + o, N.phi + o, N.psi + o, N.y + o};
-    const double *mine_f = fw[lane & 7], *mine_b = bw[lane & 3];
-    int ph = 0, i = 0;
-    for (;;) {
-      const int cur = *reinterpret_cast<volatile int *>(prog + sp);
-      if (cur == 0x7fffffff) return;
-      const int cph = cur / R, ci = cur % R;
-      if (cph > ph) { ph = cph; i = ci; }
-      if (i < R && i <= ci + kAhead) {
-        const int row = (ph & 1) ? R - 1 - i : i;  // odd sweeps run upwards
-        const double *src = ((ph & 1) ? mine_b : mine_f) + (int64_t)row * m;
-        if (lane < ((ph & 1) ? 4 : 8))
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src),
-                       "r"((unsigned)(m * sizeof(double)))
-                       : "memory");
-        ++i;
-      } else {
-        __nanosleep(100);
-      }
-    }
-  }
+                int use_x0, Lay lay) {
   const int64_t s = blockIdx.x;
-  if (!setup_ok[s]) {  // not a grid / zero pivot: reported by the setup pass
-    if (prog && threadIdx.x == 0) prog[s] = 0x7fffffff;
-    return;
-  }
-  int sweep = 0;  // sweeps started so far (even: forward, odd: backward)
+  if (!setup_ok[s]) return;  // not a grid / zero pivot: reported by the setup pass
   const int tq = threadIdx.x, lane = tq & 31, warp = tq >> 5, nw = (m / C) >> 5;
   const int q0 = C * tq;  // first own column
   const int R = (int)(n / m);
@@ -321,7 +288,6 @@ sip_scan_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
           if (lane == 31) tot[(p & 1) * nw + warp] = make_double2(A, B);
           const double Ap = __shfl_up_sync(0xffffffffu, A, 1), Bp = __shfl_up_sync(0xffffffffu, B, 1);
           __syncthreads();
-          if (prog && tq == 0) *reinterpret_cast<volatile int *>(prog + s) = sweep * R + p;
           const double cw = carry_in<true>(tot + (p & 1) * nw, warp, lane, nw);
           double yin = lane == 0 ? cw : fma(Ap, cw, Bp);  // y of the column left of the thread's
           double y[C];
@@ -338,7 +304,6 @@ sip_scan_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
-    ++sweep;
     return block_max(rmax);
   };
 
@@ -393,7 +358,6 @@ sip_scan_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
           if (lane == 0) tot[(p & 1) * nw + warp] = make_double2(A, B);
           const double Ap = __shfl_down_sync(0xffffffffu, A, 1), Bp = __shfl_down_sync(0xffffffffu, B, 1);
           __syncthreads();
-          if (prog && tq == 0) *reinterpret_cast<volatile int *>(prog + s) = sweep * R + (R - 1 - p);
           const double cw = carry_in<false>(tot + (p & 1) * nw, warp, lane, nw);
           double din = lane == 31 ? cw : fma(Ap, cw, Bp);  // d of the column right of the thread's
           double xo[C];
@@ -408,7 +372,6 @@ sip_scan_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
-    ++sweep;
     __syncthreads();  // x_new complete before the next forward pass reads neighbours' cells
   };
 
@@ -440,12 +403,299 @@ sip_scan_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
     }
   }
   if (tq == 0) {
-    if (prog) *reinterpret_cast<volatile int *>(prog + s) = 0x7fffffff;  // releases the prefetcher
     if (iters) iters[s] = k;
     if (res) res[s] = r;
     if (best_res) best_res[s] = best;
     set_status(status, index, s, st, -1);
   }
+}
+
+// ----------------------------------------------------------------------------
+// CTA-pair variant: the grid columns of a system split over the two CTAs of a
+// cluster (two SMs pull the planes; one SM's ~20 B/clk was the single-CTA
+// kernel's bound together with its per-row chain).  The split is a feed-
+// forward pipeline: in the forward sweep the left half never needs anything
+// from the right half -- it pushes the y of its last column into the right
+// CTA's FIFO (st.async + mbarrier complete_tx) and runs ahead; the right CTA
+// takes it as the start value of its row scan.  Backwards the roles swap.
+// Credits (remote mbarrier arrives) keep the producer at most kFifo rows
+// ahead; DSMEM latency stays off both chains.  One thread per column.
+// ----------------------------------------------------------------------------
+constexpr int kFifo = 8;
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t *b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n}" ::"r"(smem_u32(b)), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ unsigned peer_addr(const void *p, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <class Lay>
+__global__ void __launch_bounds__(256)
+sip_scan_pair_kernel(const double *__restrict__ a2p, const double *__restrict__ a1p,
+                     const double *__restrict__ ep, const double *__restrict__ c1p,
+                     const double *__restrict__ c2p, const double *__restrict__ bp,
+                     const double *__restrict__ tol, double *__restrict__ xout,
+                     double *__restrict__ best_x, int64_t *iters, double *res, double *best_res,
+                     int32_t *status, int32_t *index, double *history, Nat N,
+                     const int32_t *__restrict__ setup_ok, int64_t n, int m, int64_t max_iter,
+                     int use_x0, Lay lay, int nc) {
+  // nc CTAs (2 or 4) of a cluster in a chain: rank r takes the boundary value
+  // of rank r - 1 in the forward sweep and of rank r + 1 in the backward one
+  const int64_t s = blockIdx.x / nc;
+  if (!setup_ok[s]) return;  // (every CTA of the cluster)
+  unsigned rank_;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank_));
+  const int rank = (int)rank_;
+  const bool hasL = rank > 0, hasR = rank < nc - 1;
+  const int mh = m / nc;                  // columns of this CTA
+  const int tq = threadIdx.x, lane = tq & 31, warp = tq >> 5, nw = mh >> 5;
+  const int q = rank * mh + tq;           // own grid column
+  const int R = (int)(n / m);
+  extern __shared__ double sh[];
+  double *xrow = sh;                                             // [2][mh + 2]
+  double2 *tot = reinterpret_cast<double2 *>(sh + 2 * (mh + 2));  // [2][nw]
+  double *red = sh + 2 * (mh + 2) + 4 * nw;                      // [32]
+  double *rmx = red + 32;                                        // [2] residual max per sweep parity
+  double *fifo = rmx + 2;                                        // [2 directions][kFifo]
+  uint64_t *full = reinterpret_cast<uint64_t *>(fifo + 2 * kFifo);  // [2][kFifo]
+  uint64_t *fre = full + 2 * kFifo;                              // [2][kFifo] credits
+  double *ring = reinterpret_cast<double *>(fre + 2 * kFifo);     // [kST][9][mh] + edge [kST][2]
+  double *edge = ring + kST * 9 * mh;
+  const int64_t o = s * n;
+  if (tq == 0) {
+    for (int i = 0; i < 2 * kFifo; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(fre + i, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int p = 0; p < R; ++p) {
+    const int64_t i = (int64_t)p * m + q;
+    N.x[0][o + i] = use_x0 ? xout[lay(i, s)] : 0.0;
+  }
+  __syncthreads();
+  cluster_sync_all();  // barriers live, initial iterate visible to the peer
+
+  auto block_max = [&](double v) -> double {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v = nan_max(v, __shfl_xor_sync(0xffffffffu, v, d));
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double r = red[0];
+    for (int w = 1; w < nw; ++w) r = nan_max(r, red[w]);
+    return r;
+  };
+  auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
+  auto wait_row = [] { asm volatile("cp.async.wait_group %0;" ::"n"(kST - 1) : "memory"); };
+  auto cp8 = [](double *dst, const double *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  };
+  // producer side of a direction (0 forward, 1 backward): value of row number
+  // `cnt` of that direction into the peer's FIFO
+  auto push = [&](int dir, int cnt, double v) {
+    const int peer = dir == 0 ? rank + 1 : rank - 1;
+    const int slot = dir * kFifo + cnt % kFifo;
+    if (cnt >= kFifo) mbar_wait(fre + slot, (unsigned)((cnt / kFifo - 1) & 1));  // the slot was read
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                 ::"r"(peer_addr(fifo + slot, peer)), "d"(v), "r"(peer_addr(full + slot, peer))
+                 : "memory");
+  };
+  auto credit = [&](int dir, int cnt) {  // consumer: row `cnt` of `dir` has been read by every thread
+    const int peer = dir == 0 ? rank - 1 : rank + 1;
+    const int slot = dir * kFifo + cnt % kFifo;
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];"
+                 ::"r"(peer_addr(fre + slot, peer))
+                 : "memory");
+  };
+  int nf = 0, nb = 0;  // rows of the forward / backward direction processed so far
+
+  // ---- forward: values flow from rank r to rank r + 1 -------------------------------
+  auto forward = [&](const double *__restrict__ x, int par) -> double {
+    auto stage = [&](int p) {
+      if (p < R) {
+        double *dst = ring + (int64_t)(p % kST) * 9 * mh + tq;
+        const int64_t i0 = (int64_t)p * m + q;
+        cp8(dst, a2p + lay(i0, s));
+        cp8(dst + mh, a1p + lay(i0, s));
+        cp8(dst + 2 * mh, ep + lay(i0, s));
+        cp8(dst + 3 * mh, c1p + lay(i0, s));
+        cp8(dst + 4 * mh, c2p + lay(i0, s));
+        cp8(dst + 5 * mh, bp + lay(i0, s));
+        cp8(dst + 6 * mh, N.l1 + o + i0);
+        cp8(dst + 7 * mh, N.l2 + o + i0);
+        if (p + 1 < R) cp8(dst + 8 * mh, x + o + i0 + m);
+        else dst[8 * mh] = 0.0;
+        // the neighbouring CTA's boundary column of the next row
+        if (tq == 0 && hasL) {
+          if (p + 1 < R) cp8(edge + (p % kST) * 2, x + o + i0 + m - 1);
+          else edge[(p % kST) * 2] = 0.0;
+        }
+        if (tq == mh - 1 && hasR) {
+          if (p + 1 < R) cp8(edge + (p % kST) * 2 + 1, x + o + i0 + m + 1);
+          else edge[(p % kST) * 2 + 1] = 0.0;
+        }
+      }
+      commit();
+    };
+    for (int u = 0; u < kST - 1; ++u) stage(u);
+    double xm = 0.0, x0 = x[o + q], yab = 0.0, rmax = 0.0;
+    xrow[tq + 1] = x0;
+    if (tq == 0) xrow[0] = hasL ? x[o + q - 1] : 0.0;
+    if (tq == mh - 1) xrow[mh + 1] = hasR ? x[o + q + 1] : 0.0;
+    __syncthreads();
+    for (int p = 0; p < R; ++p, ++nf) {
+      stage(p + kST - 1);
+      wait_row();
+      const int fslot = nf % kFifo;
+      if (hasL && tq == 0) mbar_expect(full + fslot, 8);
+      const double *src = ring + (int64_t)(p % kST) * 9 * mh + tq;
+      const double xp = src[8 * mh];
+      double *xr = xrow + (p & 1) * (mh + 2), *xw = xrow + ((p + 1) & 1) * (mh + 2);
+      xw[tq + 1] = xp;
+      if (tq == 0) xw[0] = hasL ? edge[(p % kST) * 2] : 0.0;
+      if (tq == mh - 1) xw[mh + 1] = hasR ? edge[(p % kST) * 2 + 1] : 0.0;
+      const double xl = xr[tq], xrr = xr[tq + 2];
+      const bool row0 = p == 0, rowl = p == R - 1;
+      const double a2 = row0 ? 0.0 : src[0];
+      const double a1 = (row0 && q == 0) ? 0.0 : src[mh];
+      const double c1 = (rowl && q == m - 1) ? 0.0 : src[3 * mh];
+      const double c2 = rowl ? 0.0 : src[4 * mh];
+      double ax = src[2 * mh] * x0;
+      ax = fma(a1, xl, ax);
+      ax = fma(c1, xrr, ax);
+      ax = fma(a2, xm, ax);
+      ax = fma(c2, xp, ax);
+      const double r = src[5 * mh] - ax;
+      rmax = nan_max(rmax, fabs(r));
+      double A = -src[6 * mh], B = fma(-src[7 * mh], yab, r);
+      warp_scan<true>(A, B, lane);
+      if (lane == 31) tot[(p & 1) * nw + warp] = make_double2(A, B);
+      __syncthreads();
+      double start = 0.0;
+      if (hasL) {
+        // (the sweep's previous row: every thread read it before this row's barrier;
+        // the last row of a sweep is credited after the loop)
+        if (tq == 0 && p > 0) credit(0, nf - 1);
+        mbar_wait(full + fslot, (unsigned)((nf / kFifo) & 1));
+        start = fifo[fslot];
+      }
+      const double y = fma(A, carry_in<true>(tot + (p & 1) * nw, warp, lane, nw, start), B);
+      N.y[o + (int64_t)p * m + q] = y;
+      if (hasR && tq == mh - 1) push(0, nf, y);
+      yab = y;
+      xm = x0;
+      x0 = xp;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    double rl = block_max(rmax);  // (its barriers: every thread has read the last FIFO slot)
+    if (hasL && tq == 0) credit(0, nf - 1);
+    if (tq == 0) rmx[par] = rl;
+    cluster_sync_all();
+    double rall = 0.0;  // the same reduction order in every CTA: identical loop decisions
+    for (int c = 0; c < nc; ++c) {
+      double rp;
+      asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(rp) : "r"(peer_addr(rmx + par, c)));
+      rall = nan_max(rall, rp);
+    }
+    return rall;
+  };
+
+  // ---- backward: values flow from rank r to rank r - 1 ------------------------------
+  auto backward = [&](const double *__restrict__ x, double *__restrict__ xn) {
+    auto stage = [&](int p) {
+      if (p >= 0) {
+        double *dst = ring + (int64_t)(p % kST) * 9 * mh + tq;
+        const int64_t i0 = o + (int64_t)p * m + q;
+        cp8(dst, N.y + i0);
+        cp8(dst + mh, N.rmu + i0);
+        cp8(dst + 2 * mh, N.phi + i0);
+        cp8(dst + 3 * mh, N.psi + i0);
+        cp8(dst + 4 * mh, x + i0);
+      }
+      commit();
+    };
+    for (int u = 0; u < kST - 1; ++u) stage(R - 1 - u);
+    double dbl = 0.0;
+    for (int p = R - 1; p >= 0; --p, ++nb) {
+      stage(p - (kST - 1));
+      wait_row();
+      const int bslot = kFifo + nb % kFifo;
+      if (hasR && tq == 0) mbar_expect(full + bslot, 8);
+      const double *src = ring + (int64_t)(p % kST) * 9 * mh + tq;
+      const double rmu = src[mh];
+      double A = -src[2 * mh] * rmu, B = fma(-src[3 * mh], dbl, src[0]) * rmu;
+      warp_scan<false>(A, B, lane);
+      if (lane == 0) tot[(p & 1) * nw + warp] = make_double2(A, B);
+      __syncthreads();
+      double start = 0.0;
+      if (hasR) {
+        if (tq == 0 && p < R - 1) credit(1, nb - 1);
+        mbar_wait(full + bslot, (unsigned)((nb / kFifo) & 1));
+        start = fifo[bslot];
+      }
+      const double dl = fma(A, carry_in<false>(tot + (p & 1) * nw, warp, lane, nw, start), B);
+      xn[o + (int64_t)p * m + q] = src[4 * mh] + dl;
+      if (hasL && tq == 0) push(1, nb, dl);
+      dbl = dl;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    if (hasR && tq == 0) credit(1, nb - 1);
+    cluster_sync_all();  // x_new of every part visible before the next forward sweep
+  };
+
+  int cur = 0, best_buf = 0, par = 0;
+  double r = forward(N.x[0], par);
+  par ^= 1;
+  const double r0 = r, tl = tol[s];
+  double best = r;
+  int64_t k = 0;
+  int32_t st = BX_STATUS_OK;
+  while (r >= tl) {
+    if (k >= max_iter) { st = BX_STATUS_MAX_ITER; break; }
+    int nxt = 0;
+    while (nxt == cur || nxt == best_buf) ++nxt;
+    backward(N.x[cur], N.x[nxt]);
+    cur = nxt;
+    r = forward(N.x[cur], par);
+    par ^= 1;
+    ++k;
+    if (history && tq == 0 && rank == 0) history[s * max_iter + (k - 1)] = r;
+    if (r < best) { best = r; best_buf = cur; }
+    if (r0 > 0 && r > 1e6 * r0) { st = BX_STATUS_DIVERGED; break; }
+  }
+  for (int p = 0; p < R; ++p) {
+    const int64_t i = (int64_t)p * m + q;
+    xout[lay(i, s)] = N.x[cur][o + i];
+    if (best_x) best_x[lay(i, s)] = N.x[best_buf][o + i];
+  }
+  if (tq == 0 && rank == 0) {
+    if (iters) iters[s] = k;
+    if (res) res[s] = r;
+    if (best_res) best_res[s] = best;
+    set_status(status, index, s, st, -1);
+  }
+  cluster_sync_all();  // no CTA leaves while its peer may still address its shared memory
 }
 
 // mu -> 1/mu in place over the natural plane (systems the setup rejected are skipped)
@@ -459,7 +709,7 @@ __global__ void invert_plane_kernel(double *mu, const int32_t *__restrict__ setu
 }  // namespace sipscan
 
 // workspace after the wavefront solver's: setup flags | 9 natural planes
-static size_t scan_flag_bytes(int64_t batch) { return ((size_t)batch * 8 + 255) & ~(size_t)255; }  // setup_ok | prog
+static size_t scan_flag_bytes(int64_t batch) { return ((size_t)batch * 4 + 255) & ~(size_t)255; }
 
 bool sip_scan_applicable(int64_t n, int64_t m) { return m >= 32 && m <= 512 && m % 32 == 0 && n % m == 0; }
 
@@ -494,20 +744,50 @@ int sip_scan(const double *a2, const double *a1, const double *e, const double *
   // columns per thread: measured on config 4 (m = 512): C = 1 7.47 ms, C = 2 8.04, C = 4 11.3
   // (fewer warps leave the per-row instruction stream of a warp exposed)
   int C = 1;
-  // L2 prefetcher CTAs (see sip_scan_kernel): when solvers and prefetchers are
-  // all resident at once and the rows are 16-byte aligned (bulk prefetch)
-  int *prog = nullptr;
-  {
-    // developer knob, off: measured on config 4 the prefetchers slow the solve (18.2 vs 7.47 ms)
-    static const int pf = getenv("BX_SCAN_PF") ? atoi(getenv("BX_SCAN_PF")) : 0;
-    auto a16 = [](const void *p) { return ((uintptr_t)p & 15u) == 0; };
-    if (pf && layout == BX_LAYOUT_SYSTEM_MAJOR && 2 * batch <= 148 && ld % 2 == 0 && m % 2 == 0 &&
-        a16(a2) && a16(a1) && a16(e) && a16(c1) && a16(c2) && a16(b)) {
-      prog = ok + batch;
-      cudaMemsetAsync(prog, 0, sizeof(int) * (size_t)batch, stream);
+  const unsigned grid = (unsigned)batch;
+  // CTA pair per system (two SMs per system) when the halves are whole warps
+  // (developer knob BX_SCAN_PAIR: 0 = one CTA per system, 4 = four)
+  static const int pair = getenv("BX_SCAN_PAIR") ? atoi(getenv("BX_SCAN_PAIR")) : 1;
+  if (pair && m % 64 == 0 && m >= 128) {
+    // 2 CTAs per system; 4 (BX_SCAN_PAIR=4, developer knob) measured slower on
+    // config 4: 6.06 vs 5.79 ms (two CTAs share an SM, the chain gets longer)
+    const int nc = (pair == 4 && m % 128 == 0 && m >= 256) ? 4 : 2;
+    const int mh = (int)m / nc;
+    const size_t psmem = sizeof(double) * (size_t)(2 * (mh + 2) + 4 * (mh / 32) + 32 + 2 + 2 * sipscan::kFifo) +
+                         sizeof(uint64_t) * 4 * sipscan::kFifo +
+                         sizeof(double) * (size_t)(sipscan::kST * 9 * mh + sipscan::kST * 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nc * batch));
+    cfg.blockDim = dim3((unsigned)mh);
+    cfg.dynamicSmemBytes = psmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = nc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t err;
+    if (layout == BX_LAYOUT_INTERLEAVED) {
+      auto kern = sipscan::sip_scan_pair_kernel<Interleaved>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+      err = cudaLaunchKernelEx(&cfg, kern, a2, a1, e, c1, c2, b, tol, x, best_x, iters, res, best_res,
+                               st, ix, hist, N, (const int32_t *)ok, n, (int)m, max_iter, use_x0,
+                               Interleaved{ld}, nc);
+    } else {
+      auto kern = sipscan::sip_scan_pair_kernel<SystemMajor>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+      err = cudaLaunchKernelEx(&cfg, kern, a2, a1, e, c1, c2, b, tol, x, best_x, iters, res, best_res,
+                               st, ix, hist, N, (const int32_t *)ok, n, (int)m, max_iter, use_x0,
+                               SystemMajor{ld}, nc);
     }
+    if (err != cudaSuccess) {
+      bxh::set_error("scan SIP (CTA pair) launch: %s", cudaGetErrorString(err));
+      return BX_ERR_CUDA;
+    }
+    return BX_OK;
   }
-  const unsigned grid = (unsigned)(prog ? 2 * batch : batch);
   if (const char *env = getenv("BX_SCAN_C")) {  // developer knob
     const int c = atoi(env);
     if ((c == 1 || c == 2 || c == 4) && m % (32 * c) == 0) C = c;
@@ -521,7 +801,7 @@ int sip_scan(const double *a2, const double *a1, const double *e, const double *
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                   \
     sipscan::sip_scan_kernel<LAY, CC, VV><<<grid, (unsigned)(m / CC), smem, stream>>>(              \
         a2, a1, e, c1, c2, b, tol, x, best_x, iters, res, best_res, st, ix, hist, N, ok, n, (int)m, \
-        max_iter, use_x0, layv, prog, batch);                                                       \
+        max_iter, use_x0, layv);                                                                    \
   } while (0)
   if (layout == BX_LAYOUT_INTERLEAVED) {
     if (C == 4) BX_SCAN_LAUNCH(Interleaved, 4, false, Interleaved{ld});
