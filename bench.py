@@ -889,13 +889,33 @@ def run_ours(args):
     barrier()
     flush = getattr(wl, "flush_l2", False)
     scrub = torch.empty(64 << 20, dtype=torch.float64, device=dev) if flush else None  # 512 MB
+    # launch-latency-sized steps (config 1: ~20 us of kernels behind three
+    # launches): replay the step from a CUDA graph so that host enqueue jitter
+    # stays out of the device-side events
+    step_fn, graphed = wl.step, False
+    if flush:
+        try:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                wl.step()
+            torch.cuda.current_stream().wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                wl.step()
+            g.replay()
+            torch.cuda.synchronize()
+            step_fn, graphed = g.replay, True
+        except Exception as exc:  # capture not possible: time the direct launches
+            sys.stderr.write(f"bench: CUDA graph capture of the step failed ({exc}); direct launches\n")
+            torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
     for k in range(args.steps):
         if flush:
             scrub.fill_(float(k))
         ev[k][0].record()
-        wl.step()
+        step_fn()
         ev[k][1].record()
     t1.record()
     barrier()
@@ -936,6 +956,9 @@ def run_ours(args):
         cpu = wl.cpu_baseline()
     if rank == 0:
         cfg = static_config(args, world)
+        if flush:
+            cfg["launch"] = ("step replayed from a CUDA graph (launch-latency-sized work)" if graphed
+                             else "direct launches (graph capture failed)")
         line = {
             "metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,

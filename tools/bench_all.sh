@@ -22,6 +22,6 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:halo
   -o $OUT/npdm_full python tools/sweep_part.py child 2 4096 8192 > $OUT/ncu_npdm.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:sip_wave -s 1 -c 1 \
   -o $OUT/sip_full python bench.py --workload sip --sip-algo wavefront --steps 1 --warmup 1 --no-cpu-baseline > $OUT/ncu_sip.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:sip_scan_kernel -s 1 -c 1 \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:sip_scan -s 1 -c 1 \
   -o $OUT/sip_scan_full python bench.py --workload sip --steps 1 --warmup 1 --no-cpu-baseline > $OUT/ncu_sip_scan.log 2>&1
 echo done
