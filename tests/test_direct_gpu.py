@@ -433,7 +433,8 @@ def _weakly_dominant(k, bsz, n, margin, seed):
 
 
 @pytest.mark.parametrize("layout", LAYOUTS)
-@pytest.mark.parametrize("n", [200, 1024, 4096, 6000])
+# (1500, 2500: the two passes cut the system into different numbers of CTAs)
+@pytest.mark.parametrize("n", [200, 1024, 1500, 2500, 4096, 6000])
 @pytest.mark.parametrize("k", [1, 2])
 def test_partitioned_weakly_dominant_retries_on_the_tree(cuda, layout, k, n):
     d = _weakly_dominant(k, 12, n, 1e-3, seed=n + k)
