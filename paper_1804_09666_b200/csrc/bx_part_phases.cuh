@@ -15,6 +15,9 @@
 #include "bx_common.cuh"
 #include "bx_twoport.cuh"
 
+#ifndef BX_PART_LA_SP
+#define BX_PART_LA_SP 1  // ... of the sparse-outer variant (2 spills under the 168-register cap: 0.497 vs 0.460 ms)
+#endif
 #ifndef BX_PART_LA
 #define BX_PART_LA 1  // input groups in flight ahead of the elimination (measured: 1 > 2 > 3)
 #endif
@@ -100,7 +103,10 @@ struct Chunk {
   // register ring of input groups, LA groups in flight ahead of the one being
   // eliminated; the g loop is fully unrolled so the ring slots are fixed
   // registers (a copy between loop iterations would wait for the load)
-  constexpr int LA = BX_PART_LA < M / G ? BX_PART_LA : M / G - 1 > 0 ? M / G - 1 : 1;
+  // (sparse outer diagonals: four arrays per group instead of six -- a second
+  // group of lookahead fits the same registers)
+  constexpr int LA0 = (SP && K == 2) ? BX_PART_LA_SP : BX_PART_LA;
+  constexpr int LA = LA0 < M / G ? LA0 : M / G - 1 > 0 ? M / G - 1 : 1;
   constexpr int RG = LA + 1;
   struct Grp {
     double a2[G], a1[G], e[G], c1[G], c2[G], b[G];
