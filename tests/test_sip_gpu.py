@@ -220,8 +220,9 @@ def test_scan_matches_reference_loop(cuda, layout, m, rows, alpha):
             assert h[s, k - 1] == host(rep.residual_inf)[s]
 
 
-def test_scan_maxiter_reports_best_iterate(cuda):
-    m, rows = 64, 20
+@pytest.mark.parametrize("m", [64, 256])
+def test_scan_maxiter_reports_best_iterate(cuda, m):
+    rows = 20
     p = W.five_point(3, m * rows, m, seed=4)
     A = StencilMatrix.from_diagonals(*p[:5], m=m)
     rep = sip_solve(A, p[5], SipConfig(tolerance=1e-300, max_iterations=3, alpha=0.5), algo="scan")
@@ -229,8 +230,9 @@ def test_scan_maxiter_reports_best_iterate(cuda):
     assert np.allclose(_true_residual(p, m, host(rep.best_x)), host(rep.best_residual), rtol=1e-6)
 
 
-def test_scan_rejects_non_grid_and_zero_pivot(cuda):
-    m, rows = 32, 8
+@pytest.mark.parametrize("m", [32, 128])   # one CTA per system / a CTA pair
+def test_scan_rejects_non_grid_and_zero_pivot(cuda, m):
+    rows = 8
     p = [a.copy() for a in W.five_point(3, m * rows, m, seed=5)]
     p[1][1, m - 1] = 0.3      # A[m, m-1]: a coupling across a grid row
     p[2][2, 0] = 0.0          # a zero leading pivot
