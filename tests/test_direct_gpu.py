@@ -538,3 +538,24 @@ def test_mnpdm_sparse_outer_zero_pivot_goes_through_the_retry_pass(cuda):
     rep = solve_mnpdm(A, p[5], algo="partitioned")
     st = host(rep.status)
     assert st[1] == 1 and host(rep.index)[1] == 0 and st[0] == 0 and st[2] == 0 and st[3] == 0
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_partitioned_scaling_and_zero_rhs(cuda, k):
+    """The first pass's coupling guard is a ratio: rows scaled by 1e+-150 stay
+    on it; a zero right-hand side gives exact zeros; one system is a batch."""
+    n = 4096
+    base = W.td_dominant(3, n, seed=31) if k == 1 else W.pd_dominant(3, n, seed=31)
+    nd = 3 if k == 1 else 5
+    solve = solve_ntdm if k == 1 else solve_npdm
+    make = TriMatrix.from_diagonals if k == 1 else PentaMatrix.from_diagonals
+    ref = (D.ntdm if k == 1 else D.npdm)(*base)[0]
+    for scale in (1e150, 1e-150):
+        d = [a * scale for a in base[:nd]]
+        rep = solve(make(*d, layout="system"), base[nd] * scale, algo="partitioned")
+        assert (host(rep.status) == 0).all()
+        assert rel_err(host(rep.x), ref).max() <= REL_TOL
+    rep = solve(make(*base[:nd], layout="system"), np.zeros_like(base[nd]), algo="partitioned")
+    assert (host(rep.x) == 0.0).all() and (host(rep.status) == 0).all()
+    one = solve(make(*(a[:1] for a in base[:nd]), layout="system"), base[nd][:1], algo="partitioned")
+    assert rel_err(host(one.x), ref[:1]).max() <= REL_TOL
