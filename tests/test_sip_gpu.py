@@ -258,3 +258,21 @@ def test_config4_full_scan(cuda):
     x = host(rep.x)
     assert np.all(_true_residual(p, 512, x) < tol)
     assert np.max(np.abs(x - ref["x"])) <= 1e-7 * np.max(np.abs(ref["x"]))
+
+
+@pytest.mark.parametrize("m,rows,bsz", [(128, 64, 100), (256, 32, 200), (128, 8, 1)])
+def test_scan_pair_many_clusters_deterministic(cuda, m, rows, bsz):
+    """More CTA pairs than SMs, repeated solves: the FIFO / credit protocol of
+    the pair kernel gives the same bits every time (race detector substitute)
+    and the reference loop's iteration counts +-1."""
+    p = W.five_point(bsz, m * rows, m, seed=m + bsz)
+    tol = W.sip_tolerance(p[5])
+    A = StencilMatrix.from_diagonals(*p[:5], m=m, layout="system")
+    ref = cport.sip(*cport.rowaligned_penta(*p[:5], m=m), p[5], tol, m=m, alpha=0.5)
+    cfg = SipConfig(tolerance=tol, max_iterations=500, alpha=0.5)
+    x0 = host(sip_solve(A, p[5], cfg, algo="scan").x)
+    assert np.max(np.abs(x0 - ref["x"])) <= 1e-7 * np.max(np.abs(ref["x"]))
+    for _ in range(5):
+        rep = sip_solve(A, p[5], cfg, algo="scan")
+        assert np.array_equal(host(rep.x), x0)
+        assert np.all(np.abs(host(rep.iterations) - ref["iterations"]) <= 1)
